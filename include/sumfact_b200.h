@@ -1,0 +1,115 @@
+/*
+ * sumfact_b200 — C ABI of the B200-native SIPG sum-factorisation hot path.
+ *
+ * One shared library (paper_2407_09621_b200/libsumfact_b200.so, sm_100a).  Every
+ * entry point takes DEVICE pointers owned by the caller (torch allocates them),
+ * plain sizes and a cudaStream_t passed as void*; it only enqueues work and
+ * returns 0 or a negative SF_E* code (text in sf_last_error()).  No global
+ * mutable state; host-thread-safe across streams.
+ *
+ * Reference mapping (paths relative to /root/reference/pkg/src/sumfact):
+ *   The reference's native plugin point is _core/__init__.py:12-24, which binds
+ *   contract_f8/contract_f4 (_core/_contract.pyx:14-45): one batched 1-D
+ *   contraction per call on host arrays.  That boundary is μs-grained and
+ *   host-resident, so the drop-in sits one level up, at the operator calls the
+ *   reference's Python API makes.  Each entry below names the
+ *   reference function it replaces.
+ *
+ * Vectors: flat lexicographic (z, y, x) arrays, x fastest, exactly the
+ * reference layout (discretization.py:93-100, 135-145).  Storage dtype is
+ * double for mode 0 (fp64) and float for modes 1..3 (precision.py:36-39).
+ * Modes: 0 fp64, 1 fp32, 2 fp16, 3 fp16_ec (precision.py:29-33, 206-230).
+ * Degrees: k = 1..SF_MAX_DEGREE (K = k+1 nodes per cell and axis).
+ */
+#ifndef SUMFACT_B200_H
+#define SUMFACT_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_ABI_VERSION 1
+#define SF_MAX_DEGREE 7
+
+#define SF_OK 0
+#define SF_EINVAL (-1)        /* bad argument (reference: ValueError/TypeError/IndexError) */
+#define SF_EUNSUPPORTED (-2)  /* degree/mode outside the compiled set */
+#define SF_ECUDA (-3)         /* CUDA launch/runtime error */
+
+/* The local cell grid of one level.  nx, ny, nz: cells per axis (even, >= 2).
+ * ghost_lo / ghost_hi: optional device arrays holding the K dof planes just
+ * below z = 0 / above the top z plane (z-slab decomposition, NCCL halo); NULL
+ * means that side is the domain boundary (Nitsche terms). */
+typedef struct sf_grid {
+  int nx, ny, nz;
+  const void* ghost_lo;
+  const void* ghost_hi;
+} sf_grid;
+
+/* Host-side matrix blocks (double, row-major), built once per level by the
+ * Python host from the reference's 1-D matrices (basis.py, discretization.py:108-131):
+ *   level_op : M_cell[K*K] | D[K*K] | ucol[K] | urow[K] | bl[K] | br[K]
+ *              D = L_smooth[(F,F)][:K,:K], U = F_cross[:K,K:], ucol = U[:,0], urow = U[K-1,:],
+ *              bl = (B_left-H_left)[:,0], br = (B_right-H_right)[:,K-1]   (cell-wise form)
+ *   patch_eig: V[4][2K][2K] | lam[4][2K]   kind = 2*left_bnd + right_bnd, eigh(L_smooth[kind], M_patch)
+ *   embedding: P[2K][K]                     basis.py:243-252
+ */
+
+int sf_abi_version(void);
+const char* sf_last_error(void);
+
+/* v = A u on the grid (batch vectors at stride nx*ny*nz*K^3).
+ * Replaces apply_operator(hier, level, u, mode)            discretization.py:216-266
+ * (and, batched over unit vectors, materialize_operator   discretization.py:269-279). */
+int sf_vmult(int mode, int k, const sf_grid* grid, const double* level_op, const void* u, void* v, int batch,
+             void* stream);
+
+/* One colour of the multiplicative vertex-patch smoother: x_new = x_old + sum over
+ * the colour's patches of P^-1 (b - A x_old)|patch; uncovered cells copied.
+ * shift[i] in {0,1} along tensor axis i (x = 0).  x_old != x_new.
+ * Replaces one iteration of the colour loop of MultigridPreconditioner.smooth
+ *                                                          multigrid.py:186-203 (PatchSolver.apply_batch :71-83). */
+int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, const double* level_op,
+                     const double* patch_eig, const void* x_old, const void* b, void* x_new, void* stream);
+
+/* coarse = R (b - A x) (x != NULL) or R b (x == NULL), R = P^T on each axis.
+ * Replaces `r = b - apply_operator(x); restrict(r)`        multigrid.py:249-250, 112-125. */
+int sf_residual_restrict(int mode, int k, const sf_grid* fine_grid, const double* level_op,
+                         const double* embedding, const void* x, const void* b, void* coarse, void* stream);
+
+/* fine += P e (P on each axis).
+ * Replaces `x + prolongate(hier, level-1, e, mode)`        multigrid.py:252, 128-143. */
+int sf_prolongate_add(int mode, int k, const sf_grid* coarse_grid, const double* embedding, const void* e,
+                      void* fine, void* stream);
+
+/* out = P^-1 in on `count` contiguous (2K)^3 patches (numpy order z,y,x) sharing one boundary
+ * kind per axis; kinds[i] for tensor axis i (x = 0), kind = 2*left_bnd + right_bnd.
+ * Replaces PatchSolver.apply_batch(w, kinds, mode)          multigrid.py:71-83. */
+int sf_patch_apply(int mode, int k, long long count, const int* kinds, const double* patch_eig, const void* in,
+                   void* out, void* stream);
+
+/* ---- vector kernels for FGMRES and the V-cycle boundary (krylov.py:49-137, multigrid.py:262-266) ---- */
+
+/* out = (dtype_out) in, dtype 0 = double, 1 = float.  Replaces np.asarray(x, dtype=...). */
+int sf_convert(long long n, const void* in, int in_dtype, void* out, int out_dtype, void* stream);
+
+/* Deterministic (fixed-order, atomic-free) double dot product x.y written to *out_dev.
+ * scratch_dev: SF_DOT_SCRATCH doubles of device memory owned by the caller.
+ * Replaces `V[i] @ w` and np.linalg.norm's sum of squares   krylov.py:54,73-84. */
+#define SF_DOT_SCRATCH 1024
+int sf_dot(long long n, const double* x, const double* y, double* out_dev, double* scratch_dev, void* stream);
+
+/* y += coef * x with coef = sign * (*coef_dev) (device scalar, so MGS never syncs the host).
+ * Replaces `w = w - H[i, j] * V[i]`                          krylov.py:76,83. */
+int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream);
+
+/* y = alpha * x + beta * y (host scalars; y may alias nothing).  Replaces b / beta, w / h_next, x += y_i Z_i. */
+int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream);
+
+/* float variant used inside low-precision V-cycles: y = alpha * x + beta * y (fp32). */
+int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUMFACT_B200_H */

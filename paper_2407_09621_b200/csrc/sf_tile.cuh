@@ -1,0 +1,360 @@
+// The tile engine: one CTA evaluates the SIPG Laplacian on TPC tiles of
+// 2x2x2 cells ((2K)^3 dofs each) with sum factorisation on CUDA cores.
+//
+// Schedule per tile, x = fastest axis:
+//   stage 0  load u tile -> smem (coalesced rows)
+//   stage 1  face traces of the 6 neighbouring cell layers (alpha = face value,
+//            beta = the U-row dot product over the neighbour's K nodes); domain
+//            boundary faces are skipped (the line stages apply Nitsche instead)
+//   stage 1b tangential masses on the y-face (Mx) and z-face (My Mx) trace planes
+//   stage 2  x lines:  a = Mx u,  b = Dx* u
+//   stage 3  y lines:  c = My a,  dd = Dy* a + My b
+//   stage 4  z lines:  v = Dz* c + Mz dd
+// where Dt* is the block-tridiagonal 1-D operator along t restricted to the
+// tile's 2K-line plus the rank-2 couplings to the face neighbours (or the
+// Nitsche boundary correction).  Every contraction follows the mode's operand
+// semantics (sf_common.cuh).
+#pragma once
+#include "sf_common.cuh"
+
+namespace sf {
+
+template <int K, int MODE>
+__device__ __forceinline__ void mass_line(const LevelOp<K, MODE>& op, const Op<MODE>* w, Acc<MODE>* acc) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[c * K + i].fma(op.M[i][j], w[c * K + j]);
+}
+
+// Line operator along one axis over the tile's two cells (2K values).
+// lo side of cell 0: neighbour (alpha_lo prepared, beta_lo finished value) or Nitsche;
+// hi side of cell 1 likewise.
+template <int K, int MODE>
+__device__ __forceinline__ void stiff_line(const LevelOp<K, MODE>& op, const Op<MODE>* w, Acc<MODE>* acc,
+                                           bool lo_bnd, const Op<MODE>& a_lo, typename MT<MODE>::C b_lo,
+                                           bool hi_bnd, const Op<MODE>& a_hi, typename MT<MODE>::C b_hi) {
+  // diagonal blocks
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[c * K + i].fma(op.D[i][j], w[c * K + j]);
+  // the face inside the tile: cell 0 <- U w1, cell 1 <- U^T w0
+#pragma unroll
+  for (int i = 0; i < K; ++i) acc[i].fma(op.ucol[i], w[K]);
+#pragma unroll
+  for (int j = 1; j < K; ++j) acc[K - 1].fma(op.urow[j], w[K + j]);
+#pragma unroll
+  for (int i = 0; i < K; ++i) acc[K + i].fma(op.urow[i], w[K - 1]);
+#pragma unroll
+  for (int j = 0; j < K - 1; ++j) acc[K].fma(op.ucol[j], w[j]);
+  // low end of cell 0
+  if (lo_bnd) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[i].fma(op.bl[i], w[0]);
+#pragma unroll
+    for (int j = 1; j < K; ++j) acc[0].fma(op.bl[j], w[j]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[i].fma(op.urow[i], a_lo);
+    acc[0].add(b_lo);
+  }
+  // high end of cell 1
+  if (hi_bnd) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[K + i].fma(op.br[i], w[2 * K - 1]);
+#pragma unroll
+    for (int j = 0; j < K - 1; ++j) acc[2 * K - 1].fma(op.br[j], w[K + j]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[K + i].fma(op.ucol[i], a_hi);
+    acc[2 * K - 1].add(b_hi);
+  }
+}
+
+// Generic cell-local contraction of a B-line with a per-cell K x K matrix table.
+template <int K, int MODE>
+__device__ __forceinline__ void cell_line(const ME<MODE> (*Mt)[K], const Op<MODE>* w, Acc<MODE>* acc) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[c * K + i].fma(Mt[i][j], w[c * K + j]);
+}
+
+template <int K, int MODE, int TPC>
+struct TileEngine {
+  static constexpr int B = 2 * K;
+  static constexpr int P = B + 1;          // padded row pitch (conflict-free x lines)
+  static constexpr int VOL = B * B * P;    // one padded tile
+  static constexpr int PL = B * P;         // one padded face plane
+  using C = typename MT<MODE>::C;
+  using S = typename MT<MODE>::S;
+
+  static constexpr size_t smem_bytes() { return sizeof(C) * TPC * (2 * VOL + 12 * PL); }
+
+  C* su;  // [TPC][VOL]
+  C* sb;  // [TPC][VOL]
+  C* tr;  // [TPC][6][2][PL]
+  int ntiles_total;
+  int tile0;
+  long long sy, sz;
+
+  __device__ __forceinline__ TileEngine(char* smem, const Geom& g) {
+    su = reinterpret_cast<C*>(smem);
+    sb = su + TPC * VOL;
+    tr = sb + TPC * VOL;
+    ntiles_total = g.ntx * g.nty * g.ntz;
+    tile0 = blockIdx.x * TPC;
+    sy = (long long)g.nx * K;
+    sz = sy * (long long)g.ny * K;
+  }
+
+  __device__ __forceinline__ static int idx(int z, int y, int x) { return (z * B + y) * P + x; }
+
+  // tile -> first cell per axis
+  __device__ __forceinline__ bool tile_cells(const Geom& g, int t, int& cx, int& cy, int& cz) const {
+    int id = tile0 + t;
+    if (id >= ntiles_total) return false;
+    int tx = id % g.ntx;
+    int r = id / g.ntx;
+    int ty = r % g.nty;
+    int tz = r / g.nty;
+    cx = g.tx0 + 2 * tx;
+    cy = g.ty0 + 2 * ty;
+    cz = g.tz0 + 2 * tz;
+    return true;
+  }
+
+  // 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary
+  __device__ __forceinline__ static int face_src(const Geom& g, int axis, int hi, int c0) {
+    int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
+    int c = hi ? c0 + 2 : c0 - 1;
+    if (c >= 0 && c < n) return 0;
+    if (hi ? g.bnd_hi[axis] : g.bnd_lo[axis]) return 2;
+    return 1;
+  }
+
+  // ---------------------------------------------------------------- stage 0
+  __device__ __forceinline__ void load(const Geom& g, const S* __restrict__ u) {
+    for (int i = threadIdx.x; i < TPC * B * B * B; i += blockDim.x) {
+      int x = i % B;
+      int r = i / B;
+      int t = r % TPC;
+      r /= TPC;
+      int y = r % B;
+      int z = r / B;
+      int cx, cy, cz;
+      C val = C(0);
+      if (tile_cells(g, t, cx, cy, cz))
+        val = (C)u[(long long)(cz * K + z) * sz + (long long)(cy * K + y) * sy + (cx * K + x)];
+      su[t * VOL + idx(z, y, x)] = val;
+    }
+  }
+
+  // ---------------------------------------------------------------- stage 1
+  __device__ __forceinline__ void traces(const Geom& g, const LevelOp<K, MODE>& op, const S* __restrict__ u) {
+    for (int i = threadIdx.x; i < TPC * 6 * B * B; i += blockDim.x) {
+      int q = i % B;
+      int p = (i / B) % B;
+      int f = (i / (B * B)) % 6;
+      int t = i / (6 * B * B);
+      int cx, cy, cz;
+      if (!tile_cells(g, t, cx, cy, cz)) continue;
+      int axis = f >> 1, hi = f & 1;
+      int c0 = axis == 0 ? cx : (axis == 1 ? cy : cz);
+      int src = face_src(g, axis, hi, c0);
+      if (src == 2) continue;
+      // dof coordinates of the face position and the neighbour line start
+      int X = cx * K, Y = cy * K, Z = cz * K;
+      long long step;
+      if (axis == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
+      else if (axis == 1) { Z += p; X += q; Y += hi ? B : -K; step = sy; }
+      else { Y += p; X += q; Z += hi ? B : -K; step = sz; }
+      const S* base;
+      if (src == 0) {
+        base = u + (long long)Z * sz + (long long)Y * sy + X;
+      } else if (hi) {
+        base = reinterpret_cast<const S*>(g.ghost_hi) + (long long)(Z - g.nz * K) * sz + (long long)Y * sy + X;
+      } else {
+        base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
+      }
+      C w[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) w[j] = (C)base[j * step];
+      Acc<MODE> beta;
+      C alpha;
+      if (hi) {  // neighbour above: alpha = w[0], beta = sum_{j>=1} urow[j] w[j]
+        alpha = w[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) beta.fma(op.urow[j], prep<MODE>(w[j]));
+      } else {   // neighbour below: alpha = w[K-1], beta = sum_{j<=K-2} ucol[j] w[j]
+        alpha = w[K - 1];
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) beta.fma(op.ucol[j], prep<MODE>(w[j]));
+      }
+      C* pl = tr + ((t * 6 + f) * 2) * PL;
+      pl[p * P + q] = alpha;
+      pl[PL + p * P + q] = beta.result();
+    }
+  }
+
+  // tangential masses: y faces (2,3): Mx along q; z faces (4,5): Mx along q then My along p
+  __device__ __forceinline__ void trace_masses(const Geom& g, const LevelOp<K, MODE>& op) {
+    for (int i = threadIdx.x; i < TPC * 4 * 2 * B; i += blockDim.x) {
+      int row = i % B;
+      int pl_id = (i / B) % 2;
+      int f = 2 + (i / (2 * B)) % 4;
+      int t = i / (8 * B);
+      int cx, cy, cz;
+      if (!tile_cells(g, t, cx, cy, cz)) continue;
+      int axis = f >> 1, hi = f & 1;
+      if (face_src(g, axis, hi, axis == 1 ? cy : cz) == 2) continue;
+      C* r = tr + ((t * 6 + f) * 2 + pl_id) * PL + row * P;
+      Op<MODE> w[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) w[j] = prep<MODE>(r[j]);
+      Acc<MODE> acc[B];
+      mass_line<K, MODE>(op, w, acc);
+#pragma unroll
+      for (int j = 0; j < B; ++j) r[j] = acc[j].result();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < TPC * 2 * 2 * B; i += blockDim.x) {
+      int col = i % B;
+      int pl_id = (i / B) % 2;
+      int f = 4 + (i / (2 * B)) % 2;
+      int t = i / (4 * B);
+      int cx, cy, cz;
+      if (!tile_cells(g, t, cx, cy, cz)) continue;
+      if (face_src(g, 2, f & 1, cz) == 2) continue;
+      C* r = tr + ((t * 6 + f) * 2 + pl_id) * PL + col;
+      Op<MODE> w[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) w[j] = prep<MODE>(r[j * P]);
+      Acc<MODE> acc[B];
+      mass_line<K, MODE>(op, w, acc);
+#pragma unroll
+      for (int j = 0; j < B; ++j) r[j * P] = acc[j].result();
+    }
+  }
+
+  __device__ __forceinline__ void face_in(const Geom& g, int t, int f, int c0, int pq, bool& bnd, Op<MODE>& a,
+                                          C& b) const {
+    bnd = face_src(g, f >> 1, f & 1, c0) == 2;
+    if (!bnd) {
+      const C* pl = tr + ((t * 6 + f) * 2) * PL;
+      a = prep<MODE>(pl[pq]);
+      b = pl[PL + pq];
+    } else {
+      a = prep<MODE>(C(0));
+      b = C(0);
+    }
+  }
+
+  // ---------------------------------------------------------------- stage 2
+  __device__ __forceinline__ void xlines(const Geom& g, const LevelOp<K, MODE>& op) {
+    for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
+      int y = i % B;
+      int z = (i / B) % B;
+      int t = i / (B * B);
+      int cx, cy, cz;
+      if (!tile_cells(g, t, cx, cy, cz)) continue;
+      C* row = su + t * VOL + idx(z, y, 0);
+      Op<MODE> w[B];
+#pragma unroll
+      for (int x = 0; x < B; ++x) w[x] = prep<MODE>(row[x]);
+      bool lb, hb;
+      Op<MODE> al, ah;
+      C bl_, bh_;
+      face_in(g, t, 0, cx, z * P + y, lb, al, bl_);
+      face_in(g, t, 1, cx, z * P + y, hb, ah, bh_);
+      Acc<MODE> a[B], b[B];
+      mass_line<K, MODE>(op, w, a);
+      stiff_line<K, MODE>(op, w, b, lb, al, bl_, hb, ah, bh_);
+      C* rowb = sb + t * VOL + idx(z, y, 0);
+#pragma unroll
+      for (int x = 0; x < B; ++x) {
+        row[x] = a[x].result();
+        rowb[x] = b[x].result();
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- stage 3
+  __device__ __forceinline__ void ylines(const Geom& g, const LevelOp<K, MODE>& op) {
+    for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
+      int x = i % B;
+      int z = (i / B) % B;
+      int t = i / (B * B);
+      int cx, cy, cz;
+      if (!tile_cells(g, t, cx, cy, cz)) continue;
+      C* ca = su + t * VOL + idx(z, 0, x);
+      C* cb = sb + t * VOL + idx(z, 0, x);
+      Op<MODE> wa[B], wb[B];
+#pragma unroll
+      for (int y = 0; y < B; ++y) {
+        wa[y] = prep<MODE>(ca[y * P]);
+        wb[y] = prep<MODE>(cb[y * P]);
+      }
+      bool lb, hb;
+      Op<MODE> al, ah;
+      C bl_, bh_;
+      face_in(g, t, 2, cy, z * P + x, lb, al, bl_);
+      face_in(g, t, 3, cy, z * P + x, hb, ah, bh_);
+      Acc<MODE> c[B], d[B], e[B];
+      mass_line<K, MODE>(op, wa, c);
+      stiff_line<K, MODE>(op, wa, d, lb, al, bl_, hb, ah, bh_);
+      mass_line<K, MODE>(op, wb, e);
+#pragma unroll
+      for (int y = 0; y < B; ++y) {
+        ca[y * P] = c[y].result();
+        cb[y * P] = d[y].result() + e[y].result();
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- stage 4
+  // z line (t, y, x) -> v[0..B) in registers.  Returns false for idle threads.
+  __device__ __forceinline__ void zline(const Geom& g, const LevelOp<K, MODE>& op, int t, int y, int x, int cz,
+                                        C* v) const {
+    const C* cc = su + t * VOL + idx(0, y, x);
+    const C* cd = sb + t * VOL + idx(0, y, x);
+    Op<MODE> wc[B], wd[B];
+#pragma unroll
+    for (int z = 0; z < B; ++z) {
+      wc[z] = prep<MODE>(cc[z * B * P]);
+      wd[z] = prep<MODE>(cd[z * B * P]);
+    }
+    bool lb, hb;
+    Op<MODE> al, ah;
+    C bl_, bh_;
+    face_in(g, t, 4, cz, y * P + x, lb, al, bl_);
+    face_in(g, t, 5, cz, y * P + x, hb, ah, bh_);
+    Acc<MODE> s[B], m[B];
+    stiff_line<K, MODE>(op, wc, s, lb, al, bl_, hb, ah, bh_);
+    mass_line<K, MODE>(op, wd, m);
+#pragma unroll
+    for (int z = 0; z < B; ++z) v[z] = s[z].result() + m[z].result();
+  }
+
+  // full A u on the tile up to (and excluding) stage 4; caller runs zline per thread
+  __device__ __forceinline__ void apply_to_zstage(const Geom& g, const LevelOp<K, MODE>& op, const S* __restrict__ u) {
+    load(g, u);
+    traces(g, op, u);
+    __syncthreads();
+    trace_masses(g, op);
+    __syncthreads();
+    xlines(g, op);
+    __syncthreads();
+    ylines(g, op);
+    __syncthreads();
+  }
+};
+
+}  // namespace sf

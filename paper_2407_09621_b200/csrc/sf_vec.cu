@@ -1,0 +1,139 @@
+// Bandwidth-bound vector kernels for the FGMRES outer loop and the V-cycle
+// precision boundary (krylov.py:49-137, multigrid.py:262-266).  128-bit
+// coalesced grid-stride loops; the dot product is a fixed-shape two-pass tree
+// (no atomics), so repeated runs are bitwise identical (SPEC determinism).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "../../include/sumfact_b200.h"
+
+namespace {
+
+constexpr int kDotBlocks = SF_DOT_SCRATCH;
+constexpr int kThreads = 256;
+
+int grid_for(long long n, int per_thread) {
+  long long blocks = (n / per_thread + kThreads - 1) / kThreads;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return (int)blocks;
+}
+
+template <typename A, typename B>
+__global__ void k_convert(long long n, const A* __restrict__ in, B* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (B)in[i];
+}
+
+__global__ void k_dot_partial(long long n, const double* __restrict__ x, const double* __restrict__ y,
+                              double* __restrict__ part) {
+  __shared__ double s[kThreads];
+  double acc = 0.0;
+  const long long stride = (long long)kDotBlocks * kThreads;
+  // two independent accumulators per thread for ILP; fixed assignment -> deterministic
+  double acc2 = 0.0;
+  long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  for (; i + stride < n; i += 2 * stride) {
+    acc = fma(x[i], y[i], acc);
+    acc2 = fma(x[i + stride], y[i + stride], acc2);
+  }
+  if (i < n) acc = fma(x[i], y[i], acc);
+  s[threadIdx.x] = acc + acc2;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void k_dot_final(const double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double s[kDotBlocks];
+  for (int i = threadIdx.x; i < kDotBlocks; i += blockDim.x) s[i] = part[i];
+  __syncthreads();
+  for (int w = kDotBlocks / 2; w > 0; w >>= 1) {
+    for (int i = threadIdx.x; i < w; i += blockDim.x) s[i] += s[i + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+__global__ void k_axpy_dev(long long n, double sign, const double* __restrict__ coef, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const double a = sign * (*coef);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+template <typename T>
+__global__ void k_axpby(long long n, T alpha, const T* __restrict__ x, T beta, T* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = beta == T(0) ? alpha * x[i] : alpha * x[i] + beta * y[i];  // beta = 0 never reads y
+}
+
+thread_local char g_err[256] = "";
+
+int launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return SF_ECUDA;
+  }
+  return SF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sf_vec_last_error(void) { return g_err; }
+
+int sf_convert(long long n, const void* in, int in_dtype, void* out, int out_dtype, void* stream) {
+  if (n < 0 || (!in && n) || (!out && n)) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int g = grid_for(n, 4);
+  if (in_dtype == 0 && out_dtype == 1)
+    k_convert<double, float><<<g, kThreads, 0, st>>>(n, (const double*)in, (float*)out);
+  else if (in_dtype == 1 && out_dtype == 0)
+    k_convert<float, double><<<g, kThreads, 0, st>>>(n, (const float*)in, (double*)out);
+  else if (in_dtype == 0 && out_dtype == 0)
+    k_convert<double, double><<<g, kThreads, 0, st>>>(n, (const double*)in, (double*)out);
+  else if (in_dtype == 1 && out_dtype == 1)
+    k_convert<float, float><<<g, kThreads, 0, st>>>(n, (const float*)in, (float*)out);
+  else
+    return SF_EINVAL;
+  return launched("sf_convert");
+}
+
+int sf_dot(long long n, const double* x, const double* y, double* out_dev, double* scratch, void* stream) {
+  if (n < 0 || !out_dev || !scratch || (n && (!x || !y))) return SF_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(n, x, y, scratch);
+  k_dot_final<<<1, 1024, 0, st>>>(scratch, out_dev);
+  return launched("sf_dot");
+}
+
+int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream) {
+  if (n < 0 || !coef_dev || (n && (!x || !y))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  k_axpy_dev<<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, sign, coef_dev, x, y);
+  return launched("sf_axpy_dev");
+}
+
+int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream) {
+  if (n < 0 || (n && (!x || !y))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  k_axpby<double><<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
+  return launched("sf_axpby");
+}
+
+int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream) {
+  if (n < 0 || (n && (!x || !y))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  k_axpby<float><<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
+  return launched("sf_axpby_f32");
+}
+
+}  // extern "C"

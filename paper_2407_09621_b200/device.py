@@ -1,0 +1,96 @@
+"""Device plumbing: torch owns memory and streams; the kernels come from libsumfact_b200.so.
+
+Public functions accept numpy arrays (copied to the current CUDA device and
+back -- the reference-facing path) or CUDA tensors (zero copy).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2407_09621_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
+    _native.lib()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def as_device(x, dtype: torch.dtype, n: int | None = None) -> tuple[torch.Tensor, bool]:
+    """Return (contiguous CUDA tensor of dtype, was_host)."""
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            t = x.detach().to(device="cuda", dtype=dtype).contiguous()
+            host = True
+        else:
+            t = x.detach().reshape(-1)
+            if t.dtype != dtype:
+                t = t.to(dtype)
+            t = t.contiguous()
+            host = False
+    else:
+        arr = np.asarray(x)
+        t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1))).to(device="cuda", dtype=dtype)
+        host = True
+    t = t.reshape(-1)
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} entries, got {t.numel()}")
+    return t, host
+
+
+def to_host(t: torch.Tensor, np_dtype) -> np.ndarray:
+    return t.detach().cpu().numpy().astype(np_dtype, copy=False)
+
+
+def ptr(t: torch.Tensor) -> int:
+    assert t.is_cuda and t.is_contiguous()
+    return t.data_ptr()
+
+
+class Scratch:
+    """Per-device scratch for the deterministic reductions."""
+
+    _buf: dict = {}
+
+    @classmethod
+    def dot(cls) -> torch.Tensor:
+        dev = torch.cuda.current_device()
+        if dev not in cls._buf:
+            cls._buf[dev] = torch.empty(_native.SF_DOT_SCRATCH, dtype=torch.float64, device="cuda")
+        return cls._buf[dev]
+
+
+def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Deterministic fp64 dot into a 1-element device tensor (no host sync)."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().sf_dot(x.numel(), ptr(x), ptr(y), out.data_ptr(), ptr(Scratch.dot()), stream_ptr()),
+                  "sf_dot")
+    return out
+
+
+def axpy_dev(sign: float, coef: torch.Tensor, x: torch.Tensor, y: torch.Tensor):
+    """y += sign * coef[0] * x, coef on the device."""
+    _native.check(_native.lib().sf_axpy_dev(x.numel(), sign, coef.data_ptr(), ptr(x), ptr(y), stream_ptr()),
+                  "sf_axpy_dev")
+
+
+def axpby(alpha: float, x: torch.Tensor, beta: float, y: torch.Tensor):
+    """y = alpha x + beta y (dtype of y: fp64 or fp32)."""
+    L = _native.lib()
+    if y.dtype == torch.float64:
+        rc = L.sf_axpby(x.numel(), float(alpha), ptr(x), float(beta), ptr(y), stream_ptr())
+    else:
+        rc = L.sf_axpby_f32(x.numel(), float(alpha), ptr(x), float(beta), ptr(y), stream_ptr())
+    _native.check(rc, "sf_axpby")
+
+
+def convert(src: torch.Tensor, dst: torch.Tensor):
+    code = {torch.float64: 0, torch.float32: 1}
+    _native.check(_native.lib().sf_convert(src.numel(), ptr(src), code[src.dtype], ptr(dst), code[dst.dtype],
+                                           stream_ptr()), "sf_convert")

@@ -1,0 +1,329 @@
+"""Mesh hierarchy and the matrix-free SIPG Laplacian on the B200.
+
+Mirror of the reference's src/discretization.py API (MeshHierarchy,
+build_hierarchy, apply_operator, materialize_operator) with the vmult executed
+by the sm_100a kernel ``sf_vmult`` (csrc/sf_ops.cu).  The reference evaluates
+the operator patch-wise (aligned tiling + Nitsche rim + three shifted face
+passes, discretization.py:216-266); the kernel evaluates the algebraically
+identical cell-wise form one 2x2x2-cell tile per CTA.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native, device
+from .basis import (Basis1D, basis_1d, cell_matrices_1d, cellwise_operator, embedding_1d, face_pieces,
+                    patch_matrices_1d, smoother_matrices_1d)
+from .precision import PrecisionMode
+
+
+@dataclass
+class LevelMatrices:
+    """Per-level 1-D matrices (discretization.py:42-55) plus the packed kernel blocks."""
+
+    h: float
+    n_cells: int
+    M_cell: np.ndarray
+    L_cell: np.ndarray
+    M_patch: np.ndarray
+    L_tile: np.ndarray
+    B_left: np.ndarray
+    B_right: np.ndarray
+    F_cross: np.ndarray
+    L_smooth: dict = field(default_factory=dict)
+    cell_op: np.ndarray | None = None  # M | D | ucol | urow | bl | br  (include/sumfact_b200.h)
+
+
+class MeshHierarchy:
+    """Nested uniform DG levels on [0,1]^3 (discretization.py:58-166)."""
+
+    def __init__(self, max_level: int, degree: int, dim: int = 3, min_level: int = 1, max_dofs: int = 2**24):
+        if max_level < 1:
+            raise ValueError("need max_level >= 1 (vertex patches want 2 cells per axis)")
+        if degree < 1:
+            raise ValueError("degree must be at least 1")
+        if dim not in (2, 3):
+            raise ValueError("dim must be 2 or 3")
+        if dim != 3:
+            raise NotImplementedError("the B200 path is three-dimensional (2-D is out of scope, DESIGN.md §7)")
+        if degree > _native.MAX_DEGREE:
+            raise NotImplementedError(f"kernels are compiled for degree 1..{_native.MAX_DEGREE}")
+        if min_level < 1 or min_level > max_level:
+            raise ValueError("need 1 <= min_level <= max_level")
+        self.max_level, self.min_level, self.degree, self.dim = max_level, min_level, degree, dim
+        if self.n_dofs(max_level) > max_dofs:
+            raise ValueError(f"level {max_level} has {self.n_dofs(max_level)} DoFs, cap is {max_dofs}")
+        self.basis: Basis1D = basis_1d(degree)
+        self.embedding = embedding_1d(degree)
+        self.embedding_c = np.ascontiguousarray(self.embedding, dtype=np.float64)
+        self._levels = {lvl: self._build_level(lvl) for lvl in range(min_level, max_level + 1)}
+
+    # geometry (discretization.py:86-106)
+    def n_cells(self, level: int) -> int:
+        return 2**level
+
+    def h(self, level: int) -> float:
+        return 2.0**-level
+
+    def axis_dofs(self, level: int) -> int:
+        return self.n_cells(level) * (self.degree + 1)
+
+    def n_dofs(self, level: int) -> int:
+        return self.axis_dofs(level) ** self.dim
+
+    def shape(self, level: int):
+        return (self.axis_dofs(level),) * self.dim
+
+    def levels(self):
+        return range(self.min_level, self.max_level + 1)
+
+    def matrices(self, level: int) -> LevelMatrices:
+        return self._levels[level]
+
+    def grid(self, level: int) -> _native.SfGrid:
+        n = self.n_cells(level)
+        return _native.SfGrid(n, n, n, None, None)
+
+    def _build_level(self, level: int) -> LevelMatrices:
+        """discretization.py:108-131."""
+        k, h = self.degree, self.h(level)
+        M_cell, L_cell = cell_matrices_1d(k, h)
+        interior = patch_matrices_1d(k, h, "interior")
+        left = patch_matrices_1d(k, h, "left")
+        right = patch_matrices_1d(k, h, "right")
+        names = {(False, False): "interior", (True, False): "left", (False, True): "right", (True, True): "both"}
+        smooth = {key: smoother_matrices_1d(k, h, kind).L for key, kind in names.items()}
+        pieces = face_pieces(k, h)
+        lm = LevelMatrices(h=h, n_cells=self.n_cells(level), M_cell=M_cell, L_cell=L_cell, M_patch=interior.M,
+                           L_tile=interior.L, B_left=left.L - interior.L, B_right=right.L - interior.L,
+                           F_cross=pieces.F_center, L_smooth=smooth)
+        lm.cell_op = cellwise_operator(M_cell, smooth, pieces.F_center, pieces)
+        return lm
+
+    # index maps (discretization.py:135-166)
+    def cell_dof_indices(self, level: int, cell) -> np.ndarray:
+        K, A = self.degree + 1, self.axis_dofs(level)
+        idx = np.zeros((K,) * 3, dtype=np.int64)
+        for a in range(3):
+            shp = [1, 1, 1]
+            shp[2 - a] = K
+            idx = idx + ((cell[a] * K + np.arange(K, dtype=np.int64)) * A**a).reshape(shp)
+        return idx.reshape(-1)
+
+    def patch_dof_indices(self, level: int, shift, patch) -> np.ndarray:
+        K, A = self.degree + 1, self.axis_dofs(level)
+        B = 2 * K
+        idx = np.zeros((B,) * 3, dtype=np.int64)
+        for a in range(3):
+            shp = [1, 1, 1]
+            shp[2 - a] = B
+            idx = idx + (((2 * patch[a] + shift[a]) * K + np.arange(B, dtype=np.int64)) * A**a).reshape(shp)
+        return idx.reshape(-1)
+
+    def patch_counts(self, level: int, shift):
+        return tuple(self.n_cells(level) // 2 - s for s in shift)
+
+
+def build_hierarchy(max_level: int, degree: int, dim: int = 3, min_level: int = 1,
+                    max_dofs: int = 2**24) -> MeshHierarchy:
+    return MeshHierarchy(max_level, degree, dim=dim, min_level=min_level, max_dofs=max_dofs)
+
+
+# ------------------------------------------------------------------ vmult
+
+
+def vmult_device(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Tensor, mode: PrecisionMode,
+                 batch: int = 1, grid: _native.SfGrid | None = None):
+    """Enqueue v = A u on the current stream (device tensors of the storage dtype)."""
+    lm = hier.matrices(level)
+    g = grid if grid is not None else hier.grid(level)
+    rc = _native.lib().sf_vmult(mode.code, hier.degree, g, _native.host_ptr(lm.cell_op), device.ptr(u),
+                                device.ptr(v), batch, device.stream_ptr())
+    _native.check(rc, "sf_vmult")
+
+
+def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = PrecisionMode.FP64):
+    """Matrix-free interior-penalty Laplacian at one level (discretization.py:216-266).
+
+    numpy in -> numpy out (storage dtype of ``mode``); CUDA tensor in -> CUDA
+    tensor out.  Raises ValueError on a length mismatch, like the reference.
+    """
+    n = hier.n_dofs(level)
+    size = u.numel() if isinstance(u, torch.Tensor) else np.asarray(u).size
+    if size != n:
+        raise ValueError(f"expected {n} entries, got {size}")
+    device.require_cuda()
+    t, host = device.as_device(u, mode.torch_dtype, n)
+    v = torch.empty_like(t)
+    vmult_device(hier, level, t, v, mode)
+    return device.to_host(v, mode.storage_dtype) if host else v
+
+
+def materialize_device(hier: MeshHierarchy, level: int, mode: PrecisionMode = PrecisionMode.FP64,
+                       chunk: int = 1024) -> torch.Tensor:
+    """Dense operator on the device: column j = A e_j via batched vmults (discretization.py:269-279)."""
+    device.require_cuda()
+    n = hier.n_dofs(level)
+    A = torch.empty((n, n), dtype=mode.torch_dtype, device="cuda")
+    for j0 in range(0, n, chunk):
+        m = min(chunk, n - j0)
+        E = torch.zeros((m, n), dtype=mode.torch_dtype, device="cuda")
+        E[torch.arange(m, device="cuda"), torch.arange(j0, j0 + m, device="cuda")] = 1.0
+        out = torch.empty_like(E)
+        vmult_device(hier, level, E, out, mode, batch=m)
+        A[:, j0:j0 + m] = out.T
+    return A
+
+
+def materialize_operator(hier: MeshHierarchy, level: int, mode: PrecisionMode = PrecisionMode.FP64) -> np.ndarray:
+    """Dense fp64 operator matrix (small levels only), discretization.py:269-279."""
+    return materialize_device(hier, level, mode).double().cpu().numpy()
+
+
+# ----------------------------------------------------- pre/post-processing
+# Load vector, interpolation, error norms and the manufactured problem
+# (discretization.py:317-531).  These are setup/reporting steps outside the
+# hot path (SURVEY.md §8f "next"); round 1 evaluates them on the host with the
+# same sum-factorised quadrature as the reference.
+
+
+def _cells_view(arr, n, q):
+    return np.ascontiguousarray(arr.reshape(n, q, n, q, n, q).transpose(0, 2, 4, 1, 3, 5))
+
+
+def _cells_back(w, n, q):
+    return w.transpose(0, 3, 1, 4, 2, 5).reshape(n * q, n * q, n * q)
+
+
+def _contract_last3(w, mats):
+    """mats[a] along tensor axis a (numpy axis 5-a), x first."""
+    w = np.einsum("ik,...k->...i", mats[0], w)
+    w = np.einsum("ik,...kx->...ix", mats[1], w)
+    return np.einsum("ik,...kyx->...iyx", mats[2], w)
+
+
+def _axis_points(hier, level, pts):
+    n, h = hier.n_cells(level), hier.h(level)
+    return ((np.arange(n)[:, None] + np.asarray(pts)[None, :]) * h).ravel()
+
+
+def _coords(axis_pts):
+    Z, Y, X = np.meshgrid(axis_pts, axis_pts, axis_pts, indexing="ij")
+    return X, Y, Z
+
+
+def _weights(hier, level, rule):
+    wa = np.tile(rule.weights, hier.n_cells(level)) * hier.h(level)
+    return wa[:, None, None] * wa[None, :, None] * wa[None, None, :]
+
+
+def assemble_rhs(hier: MeshHierarchy, level: int, f, g=None, quad_points: int | None = None) -> np.ndarray:
+    """Load vector: cell integrals of f v (+ Nitsche data terms for g), discretization.py:317-394."""
+    from .basis import gauss_rule, lagrange_derivatives, lagrange_values, penalty
+
+    k, n, h = hier.degree, hier.n_cells(level), hier.h(level)
+    K = k + 1
+    rule = gauss_rule(quad_points or (k + 2))
+    q = len(rule.points)
+    S = lagrange_values(hier.basis.nodes, rule.points)
+    ax = _axis_points(hier, level, rule.points)
+    vals = np.broadcast_to(np.asarray(f(*_coords(ax)), dtype=np.float64), (n * q,) * 3) * _weights(hier, level, rule)
+    b = _cells_back(_contract_last3(_cells_view(vals, n, q), [S.T] * 3), n, K)
+    if g is not None:
+        nodes = hier.basis.nodes
+        gamma = penalty(k, h, h)
+        coef = {0: gamma * lagrange_values(nodes, [0.0])[0] + lagrange_derivatives(nodes, [0.0])[0] / h,
+                1: gamma * lagrange_values(nodes, [1.0])[0] - lagrange_derivatives(nodes, [1.0])[0] / h}
+        wa = np.tile(rule.weights, n) * h
+        for a in range(3):
+            d_np = 2 - a
+            for side in (0, 1):
+                t1, t2 = [np.meshgrid(ax, ax, indexing="ij")[i] for i in (0, 1)]
+                coords = [None, None, None]
+                tang = sorted([bb for bb in range(3) if bb != a], reverse=True)
+                coords[tang[0]], coords[tang[1]] = t1, t2
+                coords[a] = np.full_like(t1, float(side))
+                gv = np.broadcast_to(np.asarray(g(*coords), dtype=np.float64), (n * q, n * q))
+                gv = gv * wa[:, None] * wa[None, :]
+                w2 = np.ascontiguousarray(gv.reshape(n, q, n, q).transpose(0, 2, 1, 3))
+                w2 = np.einsum("ik,...k->...i", S.T, w2)
+                w2 = np.einsum("ik,...kx->...ix", S.T, w2)
+                tan = w2.transpose(0, 2, 1, 3).reshape(n * K, n * K)
+                sl = [slice(None)] * 3
+                sl[d_np] = slice(0, K) if side == 0 else slice(n * K - K, None)
+                cshape = [1, 1, 1]
+                cshape[d_np] = K
+                tshape = list(tan.shape)
+                tshape.insert(d_np, 1)
+                b[tuple(sl)] += coef[side].reshape(cshape) * tan.reshape(tshape)
+    return b.reshape(-1)
+
+
+def interpolate(hier: MeshHierarchy, level: int, func) -> np.ndarray:
+    """Nodal interpolant on the Gauss-Lobatto product grid (discretization.py:397-402)."""
+    ax = _axis_points(hier, level, hier.basis.nodes)
+    return np.broadcast_to(np.asarray(func(*_coords(ax)), dtype=np.float64), hier.shape(level)).reshape(-1).copy()
+
+
+def _qvalues(hier, level, u, pts, deriv_axis=None):
+    from .basis import lagrange_derivatives, lagrange_values
+
+    n, h, K = hier.n_cells(level), hier.h(level), hier.degree + 1
+    S = lagrange_values(hier.basis.nodes, pts)
+    D = lagrange_derivatives(hier.basis.nodes, pts) / h
+    uh = u.detach().double().cpu().numpy() if isinstance(u, torch.Tensor) else np.asarray(u, dtype=np.float64)
+    w = _cells_view(uh.reshape(hier.shape(level)), n, K)
+    return _cells_back(_contract_last3(w, [D if deriv_axis == a else S for a in range(3)]), n, len(pts))
+
+
+def l2_error(hier: MeshHierarchy, level: int, u_h, exact, quad_points: int | None = None) -> float:
+    """discretization.py:431-441."""
+    from .basis import gauss_rule
+
+    rule = gauss_rule(quad_points or (hier.degree + 3))
+    ax = _axis_points(hier, level, rule.points)
+    diff = _qvalues(hier, level, u_h, rule.points) - exact(*_coords(ax))
+    return float(math.sqrt(np.sum(_weights(hier, level, rule) * diff**2)))
+
+
+def h1_seminorm_error(hier: MeshHierarchy, level: int, u_h, grad_exact, quad_points: int | None = None) -> float:
+    """discretization.py:444-459."""
+    from .basis import gauss_rule
+
+    rule = gauss_rule(quad_points or (hier.degree + 3))
+    ax = _axis_points(hier, level, rule.points)
+    W = _weights(hier, level, rule)
+    grads = grad_exact(*_coords(ax))
+    total = 0.0
+    for a in range(3):
+        c = _qvalues(hier, level, u_h, rule.points, deriv_axis=a) - np.asarray(grads[a], float)
+        total += float(np.sum(W * c**2))
+    return math.sqrt(total)
+
+
+@dataclass
+class ModelProblem:
+    exact: callable
+    rhs: callable
+    gradient: callable
+    boundary: callable | None = None
+
+
+def sine_product_problem(dim: int = 3) -> ModelProblem:
+    """Product-of-sines solution, f = 3 pi^2 u, zero Dirichlet data (discretization.py:504-531)."""
+    if dim != 3:
+        raise NotImplementedError("the B200 path is three-dimensional")
+    pi = np.pi
+    exact = lambda x, y, z: np.sin(pi * x) * np.sin(pi * y) * np.sin(pi * z)
+    rhs = lambda x, y, z: 3.0 * pi**2 * exact(x, y, z)
+
+    def gradient(x, y, z):
+        return (pi * np.cos(pi * x) * np.sin(pi * y) * np.sin(pi * z),
+                pi * np.sin(pi * x) * np.cos(pi * y) * np.sin(pi * z),
+                pi * np.sin(pi * x) * np.sin(pi * y) * np.cos(pi * z))
+
+    return ModelProblem(exact=exact, rhs=rhs, gradient=gradient)

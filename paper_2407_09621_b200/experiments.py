@@ -1,0 +1,57 @@
+"""Solve driver (mirror of src/experiments.py:44-103, run_solve)."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .discretization import (MeshHierarchy, assemble_rhs, build_hierarchy, h1_seminorm_error, l2_error,
+                             sine_product_problem, vmult_device)
+from .krylov import fgmres, gmres
+from .multigrid import MultigridPreconditioner, VCycleConfig
+from .precision import PrecisionMode
+
+
+@dataclass
+class SolveOutcome:
+    degree: int
+    level: int
+    mode: PrecisionMode
+    solver: str
+    dofs: int
+    report: object
+    l2: float
+    h1: float
+    x: object = None
+
+
+def make_operator(hier: MeshHierarchy, level: int):
+    """fp64 vmult on device tensors: the apply_A the solve hands to (F)GMRES."""
+    def apply_A(v: torch.Tensor) -> torch.Tensor:
+        out = torch.empty_like(v)
+        vmult_device(hier, level, v, out, PrecisionMode.FP64)
+        return out
+    return apply_A
+
+
+def run_solve(degree: int, level: int, mode: PrecisionMode = PrecisionMode.FP64, solver: str = "fgmres",
+              tol: float = 1e-8, maxit: int = 100, coarse_level: int = 1, pre_smooth: int = 1,
+              post_smooth: int = 1, hier: MeshHierarchy | None = None, keep_solution: bool = False) -> SolveOutcome:
+    """Solve the manufactured Poisson problem with a V-cycle preconditioner (experiments.py:57-103).
+
+    The Krylov vectors never leave the device; the rhs is uploaded once and
+    the solution downloaded once for the error norms.
+    """
+    if solver not in ("fgmres", "gmres"):
+        raise ValueError(f"unknown solver {solver!r}")
+    hier = hier or build_hierarchy(level, degree)
+    prob = sine_product_problem(hier.dim)
+    b = torch.from_numpy(assemble_rhs(hier, level, prob.rhs)).cuda()
+    mg = MultigridPreconditioner(hier, VCycleConfig(pre_smooth_steps=pre_smooth, post_smooth_steps=post_smooth,
+                                                    coarse_level=coarse_level, mode=mode))
+    run = fgmres if solver == "fgmres" else gmres
+    x, report = run(make_operator(hier, level), lambda v: mg.apply(v, level), b, tol=tol, maxit=maxit)
+    report.l2_error = l2_error(hier, level, x, prob.exact)
+    report.h1_error = h1_seminorm_error(hier, level, x, prob.gradient)
+    return SolveOutcome(degree=degree, level=level, mode=mode, solver=solver, dofs=hier.n_dofs(level),
+                        report=report, l2=report.l2_error, h1=report.h1_error, x=x if keep_solution else None)

@@ -1,0 +1,151 @@
+"""GPU parity of the smoother, transfers, coarse solve and V-cycle."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2407_09621_b200 as sf
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+P = sf.PrecisionMode
+SM_CASES = [(1, 2), (2, 2), (3, 2), (7, 2), (1, 3)]
+
+
+def unit(rng, n):
+    x = rng.standard_normal(n)
+    return x / np.linalg.norm(x)
+
+
+@pytest.mark.parametrize("k,lvl", SM_CASES)
+def test_fp64_smoother_matches_reference(gold, k, lvl):
+    hier = sf.build_hierarchy(lvl, k)
+    D = hier.n_dofs(lvl)
+    x, b = unit(np.random.default_rng(1), D), unit(np.random.default_rng(2), D)
+    out = sf.MultigridPreconditioner(hier).smooth(lvl, x, b, P.FP64)
+    assert rel_l2(out, gold("smoother")[f"smooth_k{k}_l{lvl}_fp64"]) <= 1e-11
+
+
+@pytest.mark.parametrize("k,lvl", SM_CASES)
+@pytest.mark.parametrize("mode", [P.FP32, P.FP16, P.FP16_EC])
+def test_low_precision_smoother_band(gold, k, lvl, mode):
+    hier = sf.build_hierarchy(lvl, k)
+    D = hier.n_dofs(lvl)
+    x, b = unit(np.random.default_rng(1), D), unit(np.random.default_rng(2), D)
+    out = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).smooth(lvl, x, b, mode)
+    g = gold("smoother")
+    ref64, ref_low = g[f"smooth_k{k}_l{lvl}_fp64"], g[f"smooth_k{k}_l{lvl}_{mode.value}"]
+    assert out.dtype == np.float32
+    assert rel_l2(out, ref64) <= 4.0 * rel_l2(ref_low, ref64) + 1e-6
+
+
+@pytest.mark.parametrize("k,lvl", SM_CASES)
+@pytest.mark.parametrize("mode", [P.FP64, P.FP32, P.FP16, P.FP16_EC])
+def test_transfers_match_reference(gold, k, lvl, mode):
+    hier = sf.build_hierarchy(lvl, k)
+    g = gold("smoother")
+    x = unit(np.random.default_rng(1), hier.n_dofs(lvl))
+    e = np.random.default_rng(3).standard_normal(hier.n_dofs(lvl - 1))
+    tol = 1e-13 if mode is P.FP64 else (1e-6 if mode is not P.FP16 else 4e-3)
+    r = sf.restrict(hier, lvl, x, mode)
+    p = sf.prolongate(hier, lvl - 1, e, mode)
+    assert r.dtype == mode.storage_dtype and p.dtype == mode.storage_dtype
+    assert rel_l2(r, g[f"restrict_k{k}_l{lvl}_{mode.value}"]) <= tol
+    assert rel_l2(p, g[f"prolong_k{k}_l{lvl}_{mode.value}"]) <= tol
+
+
+def test_transfer_duality_and_polynomial_exactness():
+    hier = sf.build_hierarchy(2, 3)
+    rng = np.random.default_rng(8)
+    e = rng.standard_normal(hier.n_dofs(1))
+    r = rng.standard_normal(hier.n_dofs(2))
+    assert sf.prolongate(hier, 1, e) @ r == pytest.approx(e @ sf.restrict(hier, 2, r), rel=1e-12)
+    coef = rng.standard_normal((4, 4, 4))
+    poly = lambda x, y, z: np.polynomial.polynomial.polyval3d(x, y, z, coef)
+    fine = sf.prolongate(hier, 1, sf.interpolate(hier, 1, poly))
+    assert np.allclose(fine, sf.interpolate(hier, 2, poly), atol=1e-11)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_patch_solver_matches_dense_lu(k):
+    hier = sf.build_hierarchy(2, k)
+    lm = hier.matrices(2)
+    solver = sf.PatchSolver(lm.M_patch, lm.L_smooth)
+    B = 2 * (k + 1)
+    rng = np.random.default_rng(1)
+    kv = [(False, False), (True, False), (False, True), (True, True)]
+    for kinds in [(a, b, c) for a in kv for b in kv for c in kv][::5]:
+        mats = [lm.L_smooth[q] for q in kinds]
+        Aop = (np.kron(np.kron(mats[0], lm.M_patch), lm.M_patch) + np.kron(np.kron(lm.M_patch, mats[1]), lm.M_patch)
+               + np.kron(np.kron(lm.M_patch, lm.M_patch), mats[2]))
+        r = rng.standard_normal(B**3)
+        e = sf.patch_inverse_apply(solver, r.reshape(B, B, B), kinds).reshape(-1)
+        assert rel_l2(e, np.linalg.solve(Aop, r)) <= 1e-10
+
+
+def test_smoother_fixed_point_determinism_and_direct_solve():
+    hier = sf.build_hierarchy(2, 1)
+    mg = sf.MultigridPreconditioner(hier)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(hier.n_dofs(2))
+    b = sf.apply_operator(hier, 2, x)
+    assert np.allclose(mg.smooth(2, x, b), x, atol=1e-10)
+    b2 = rng.standard_normal(hier.n_dofs(2))
+    assert np.array_equal(mg.smooth(2, np.zeros_like(b2), b2), mg.smooth(2, np.zeros_like(b2), b2))
+    h1 = sf.build_hierarchy(1, 2)
+    b1 = rng.standard_normal(h1.n_dofs(1))
+    x1 = sf.MultigridPreconditioner(h1).smooth(1, np.zeros_like(b1), b1)
+    assert np.linalg.norm(b1 - sf.apply_operator(h1, 1, x1)) <= 1e-9 * np.linalg.norm(b1)
+
+
+def test_smoothing_reduces_residual_monotonically():
+    hier = sf.build_hierarchy(2, 1)
+    mg = sf.MultigridPreconditioner(hier)
+    b = np.random.default_rng(5).standard_normal(hier.n_dofs(2))
+    x = np.zeros_like(b)
+    norms = [np.linalg.norm(b)]
+    for _ in range(4):
+        x = mg.smooth(2, x, b)
+        norms.append(np.linalg.norm(b - sf.apply_operator(hier, 2, x)))
+    assert all(n1 < n0 for n0, n1 in zip(norms, norms[1:]))
+
+
+def test_coarse_solve(gold):
+    hier = sf.build_hierarchy(2, 1)
+    mg = sf.MultigridPreconditioner(hier)
+    b = np.random.default_rng(9).standard_normal(hier.n_dofs(1))
+    x = mg.coarse_solve(b, P.FP64)
+    assert np.linalg.norm(b - sf.apply_operator(hier, 1, x)) <= 1e-10 * np.linalg.norm(b)
+    A_ref = gold("sipg_dense")["k1_l1"]
+    assert np.allclose(A_ref @ x, b, atol=1e-9 * np.linalg.norm(b))
+    assert mg.coarse_solve(np.ones(hier.n_dofs(1)), P.FP16).dtype == np.float32
+
+
+@pytest.mark.parametrize("k,lvl", [(1, 3), (3, 3), (2, 2), (7, 2)])
+@pytest.mark.parametrize("mode", [P.FP64, P.FP32, P.FP16, P.FP16_EC])
+def test_vcycle_matches_reference(gold, k, lvl, mode):
+    hier = sf.build_hierarchy(lvl, k)
+    b = unit(np.random.default_rng(4), hier.n_dofs(lvl))
+    out = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).apply(b, lvl)
+    g = gold("vcycle")
+    ref = g[f"vcycle_k{k}_l{lvl}_{mode.value}"]
+    assert out.dtype == np.float64
+    if mode is P.FP64:
+        assert rel_l2(out, ref) <= 1e-10
+    else:
+        ref64 = g[f"vcycle_k{k}_l{lvl}_fp64"]
+        assert rel_l2(out, ref64) <= 4.0 * rel_l2(ref, ref64) + 1e-6
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_vcycle_contraction(k):
+    """tests/test_multigrid.py:243-256: error contraction <= 0.5 per cycle."""
+    hier = sf.build_hierarchy(3, k)
+    mg = sf.MultigridPreconditioner(hier)
+    rng = np.random.default_rng(13)
+    x_true = rng.standard_normal(hier.n_dofs(3))
+    b = sf.apply_operator(hier, 3, x_true)
+    x = np.zeros_like(b)
+    e0 = np.linalg.norm(x_true)
+    for _ in range(3):
+        x = mg.vcycle(x, b, 3)
+    assert np.linalg.norm(x - x_true) <= 0.5**3 * e0

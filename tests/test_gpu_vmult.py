@@ -1,0 +1,129 @@
+"""GPU parity of the vmult (sf_vmult) against the reference's golden vectors,
+the CPU oracle, and size-independent properties at large sizes."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2407_09621_b200 as sf
+from conftest import rel_l2
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+P = sf.PrecisionMode
+CASES = [(1, 1), (1, 2), (2, 2), (3, 2), (3, 3), (7, 1), (7, 2)]
+
+# error band of the reference's own low-precision vmults (golden), per mode:
+# ours must land within a factor of it (cell-wise schedule, same operand semantics)
+BAND = {P.FP32: 4.0, P.FP16: 4.0, P.FP16_EC: 4.0}
+
+
+@pytest.mark.parametrize("k,lvl", CASES)
+def test_fp64_vmult_matches_reference_1e12(gold, k, lvl):
+    hier = sf.build_hierarchy(lvl, k)
+    u = np.random.default_rng(0).standard_normal(hier.n_dofs(lvl))
+    v = sf.apply_operator(hier, lvl, u)
+    assert v.dtype == np.float64
+    assert rel_l2(v, gold("vmult")[f"k{k}_l{lvl}_fp64"]) <= 1e-12
+
+
+@pytest.mark.parametrize("k,lvl", CASES)
+@pytest.mark.parametrize("mode", [P.FP32, P.FP16, P.FP16_EC])
+def test_low_precision_vmult_error_band(gold, k, lvl, mode):
+    hier = sf.build_hierarchy(lvl, k)
+    u = np.random.default_rng(0).standard_normal(hier.n_dofs(lvl))
+    ref64 = gold("vmult")[f"k{k}_l{lvl}_fp64"]
+    ref_low = gold("vmult")[f"k{k}_l{lvl}_{mode.value}"]
+    v = sf.apply_operator(hier, lvl, u, mode)
+    assert v.dtype == np.float32
+    err, ref_err = rel_l2(v, ref64), rel_l2(ref_low, ref64)
+    assert err <= BAND[mode] * ref_err + 1e-7, (err, ref_err)
+
+
+def test_precision_ordering_like_reference():
+    """tests/test_discretization.py:261-276: fp32 < 1e-5, fp32 < fp16 < 0.1, ec < fp16."""
+    hier = sf.build_hierarchy(2, 2)
+    u = np.random.default_rng(2).standard_normal(hier.n_dofs(2))
+    ref = sf.apply_operator(hier, 2, u, P.FP64)
+    r32 = rel_l2(sf.apply_operator(hier, 2, u, P.FP32), ref)
+    r16 = rel_l2(sf.apply_operator(hier, 2, u, P.FP16), ref)
+    rec = rel_l2(sf.apply_operator(hier, 2, u, P.FP16_EC), ref)
+    assert r32 < 1e-5 and r32 < r16 < 0.1 and rec < r16
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (2, 3), (4, 2), (5, 2), (6, 2)])
+def test_fp64_vmult_matches_oracle(k, lvl):
+    H = port.Hierarchy(lvl, k)
+    u = np.random.default_rng(7).standard_normal(H.n_dofs(lvl))
+    ref = port.apply_operator(H, lvl, u)
+    v = sf.apply_operator(sf.build_hierarchy(lvl, k), lvl, u)
+    assert rel_l2(v, ref) <= 1e-12
+
+
+def test_dense_assembly_oracle(gold):
+    """Independent dense SIPG assembly of the reference (tests/sipg_oracle.py)."""
+    g = gold("sipg_dense")
+    for k, lvl, key in [(1, 1, "k1_l1"), (1, 2, "k1_l2"), (2, 1, "k2_l1")]:
+        A = sf.materialize_operator(sf.build_hierarchy(lvl, k), lvl)
+        assert rel_l2(A, g[key]) <= 1e-12
+        assert np.allclose(A, A.T, atol=1e-12 * np.abs(A).max())
+
+
+def test_zero_and_length_guard():
+    hier = sf.build_hierarchy(1, 2)
+    assert np.all(sf.apply_operator(hier, 1, np.zeros(hier.n_dofs(1))) == 0)
+    with pytest.raises(ValueError):
+        sf.apply_operator(hier, 1, np.zeros(10))
+
+
+def test_constants_annihilated_in_interior():
+    hier = sf.build_hierarchy(2, 1)
+    r = sf.apply_operator(hier, 2, np.ones(hier.n_dofs(2))).reshape(hier.shape(2))
+    K = 2
+    assert np.abs(r[K:-K, K:-K, K:-K]).max() <= 1e-10
+    assert np.abs(r).max() > 0.1
+
+
+def test_tensor_in_tensor_out_and_determinism():
+    hier = sf.build_hierarchy(3, 7)
+    u = torch.randn(hier.n_dofs(3), dtype=torch.float64, device="cuda")
+    v1 = sf.apply_operator(hier, 3, u)
+    v2 = sf.apply_operator(hier, 3, u)
+    assert v1.is_cuda and torch.equal(v1, v2)
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 6), (3, 7)])
+def test_large_vmult_symmetry_and_linearity(k, lvl):
+    """At the bench sizes (1.3e8 DoF) parity is checked through properties."""
+    hier = sf.build_hierarchy(lvl, k, max_dofs=2**31)
+    n = hier.n_dofs(lvl)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    u = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    w = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    Au, Aw = sf.apply_operator(hier, lvl, u), sf.apply_operator(hier, lvl, w)
+    a, b = float(torch.dot(Au, w)), float(torch.dot(u, Aw))
+    assert abs(a - b) <= 1e-11 * abs(a)
+    Auw = sf.apply_operator(hier, lvl, 2.0 * u - 3.0 * w)
+    assert float(torch.linalg.norm(Auw - (2.0 * Au - 3.0 * Aw)) / torch.linalg.norm(Auw)) <= 1e-13
+    assert float(torch.dot(u, Au)) > 0
+
+
+def test_slab_ghosts_reproduce_the_full_operator():
+    """Two z-slabs with K-plane ghost layers (the multi-GPU layout) == one domain."""
+    from paper_2407_09621_b200 import _native
+    from paper_2407_09621_b200.discretization import vmult_device
+
+    k, lvl = 3, 3
+    hier = sf.build_hierarchy(lvl, k)
+    K, n, A = k + 1, 2**lvl, hier.axis_dofs(lvl)
+    u = torch.randn(hier.n_dofs(lvl), dtype=torch.float64, device="cuda")
+    full = sf.apply_operator(hier, lvl, u).reshape(A, A, A)
+    U = u.reshape(A, A, A)
+    half = A // 2
+    lo, hi = U[:half].contiguous(), U[half:].contiguous()
+    g_lo = U[half:half + K].contiguous()   # planes above the lower slab
+    g_hi = U[half - K:half].contiguous()   # planes below the upper slab
+    out_lo, out_hi = torch.empty_like(lo), torch.empty_like(hi)
+    vmult_device(hier, lvl, lo, out_lo, P.FP64, grid=_native.SfGrid(n, n, n // 2, None, g_lo.data_ptr()))
+    vmult_device(hier, lvl, hi, out_hi, P.FP64, grid=_native.SfGrid(n, n, n // 2, g_hi.data_ptr(), None))
+    got = torch.cat([out_lo, out_hi])
+    assert float(torch.linalg.norm(got - full) / torch.linalg.norm(full)) <= 1e-14
