@@ -1,0 +1,343 @@
+"""Benchmark of the B200 SIPG hot path (driver contract: one JSON line on rank 0).
+
+Headline workload (N=1): FP64 Q7 DG-SIPG Laplace vmult on the 128^3-cell unit
+cube, 1,073,741,824 DoF (BASELINE.json configs[1], "~1e9 DoF on 1 B200").
+value = GDoF/s with u and v resident in HBM (8.6 GB each, far larger than the
+126 MB L2, so no flush is needed between steps).  e2e = the same vmult through
+the public API ``apply_operator`` with pinned HOST buffers, H2D + D2H inside
+the timed region.
+
+N>1 (torchrun): weak scaling -- every rank owns a 128^3-cell z-slab of a
+128 x 128 x (128 N) brick, exchanges its K-plane ghost layers with the z
+neighbours over NCCL each step, then runs the vmult with ghost pointers.
+
+--impl reference: the reference algorithm's CPU implementation (the numpy
+oracle port of src/discretization.py:216-266, all host threads) on a bounded
+sample of the same workload (Q7 level 5, 16.8 M DoF), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Laplace vmult GDoF/s & TFLOPS (FP64/FP16); FGMRES+MG time-to-solution"
+UNIT = "GDoF/s"
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA.8x8x4 peak, profiles/r01_microbench_fp64.md (MEASURED_PEAKS has no fp64)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ref_flops_per_dof(k, level):
+    """the reference schedule, 36N + 18N/p flop/DoF (N = 2(k+1), p = 2^(l-1))."""
+    N = 2 * (k + 1)
+    return 36 * N + 18 * N / 2 ** (level - 1)
+
+
+def kernel_flops_per_dof(k):
+    """Flops the cell-wise tile kernel executes per DoF (interior tiles):
+    line stages 7K + 9 - 3/K MACs, face traces 3(K-1)/K, trace-plane masses 6, plus 2 adds."""
+    K = k + 1
+    macs = 7 * K + 9 - 3.0 / K + 3.0 * (K - 1) / K + 6.0
+    return 2 * macs + 2
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.fh = open(self.path, "w")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx = max(mx, float(f[1]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, f[4:8]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        except FileNotFoundError:
+            pass
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(threads=None, level=5, k=7, reps=2):
+    """Reference algorithm on the host: numpy port of apply_operator, all host threads."""
+    from oracle import port
+
+    threads = threads or port.default_threads()
+    H = port.Hierarchy(level, k)
+    u = np.random.default_rng(0).standard_normal(H.n_dofs(level))
+    port.apply_operator(H, level, u, "fp64", threads)  # warm-up
+    best = math.inf
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        port.apply_operator(H, level, u, "fp64", threads)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": H.n_dofs(level) / best / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"Q{k} level {level} ({H.n_dofs(level)} DoF) fp64 vmult, oracle/port.py (numpy einsum, "
+                      f"outer batch split over {threads} threads), best of {reps}",
+            "seconds_per_vmult": best}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    res = None
+    for _ in range(args.warmup):
+        cpu_baseline(reps=1)
+    for _ in range(args.steps):
+        res = cpu_baseline(reps=1)
+        steps.append(res["value"])
+    value = float(np.median(steps))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["seconds_per_vmult"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "Q7 SIPG Laplace vmult, fp64 (bounded CPU sample: Q7 level 5, 16.8M DoF)",
+                       "degree": 7, "level": 5, "dofs": 16777216},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--degree", type=int, default=7)
+    ap.add_argument("--level", type=int, default=7)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_09621_b200 as sf
+    from paper_2407_09621_b200 import _native
+    from paper_2407_09621_b200.discretization import vmult_device
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    k, lvl = args.degree, args.level
+    K = k + 1
+    hier = sf.build_hierarchy(lvl, k, max_dofs=2**34, min_level=lvl)
+    n = hier.n_cells(lvl)
+    A = hier.axis_dofs(lvl)
+    D = hier.n_dofs(lvl)
+    P = sf.PrecisionMode
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    u = torch.randn(D, dtype=torch.float64, device="cuda", generator=gen)
+    v = torch.empty_like(u)
+    plane = A * A
+    if world > 1:
+        glo = torch.empty(K * plane, dtype=torch.float64, device="cuda")
+        ghi = torch.empty(K * plane, dtype=torch.float64, device="cuda")
+        grid = _native.SfGrid(n, n, n, glo.data_ptr() if rank > 0 else None,
+                              ghi.data_ptr() if rank < world - 1 else None)
+    else:
+        grid = hier.grid(lvl)
+
+    def exchange():
+        ops = []
+        if rank > 0:
+            ops.append(dist.P2POp(dist.isend, u[:K * plane], rank - 1))
+            ops.append(dist.P2POp(dist.irecv, glo, rank - 1))
+        if rank < world - 1:
+            ops.append(dist.P2POp(dist.isend, u[D - K * plane:], rank + 1))
+            ops.append(dist.P2POp(dist.irecv, ghi, rank + 1))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def step():
+        if world > 1:
+            exchange()
+        vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * D / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant (only) kernel in the step: executed-flop model vs measured FP64 peak
+    kflops = kernel_flops_per_dof(k) * D
+    achieved_tf = kflops / (ms * 1e-3) / 1e12 if world == 1 else None
+    hbm, hbm_src = peaks()
+    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None, "traffic": None,
+                "kernel": "k_vmult<8,0>" if k == 7 else f"k_vmult<{K},0>",
+                "flops_per_dof": kernel_flops_per_dof(k),
+                "peak_source": "measured DMMA microbenchmark (profiles/r01_microbench_fp64.md)",
+                "hbm": {"achieved": 16 * D / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": 16 * D / (ms * 1e-3) / 1e9 / hbm, "peak_source": hbm_src}}
+    traffic = os.path.join(ROOT, "profiles", "vmult_traffic.json")
+    if os.path.exists(traffic):
+        try:
+            roofline["traffic"] = json.load(open(traffic)).get(f"k{k}_l{lvl}_fp64")
+        except Exception:
+            pass
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (u ~ N(0,1), seeded)",
+           "config": {"workload": f"Q{k} DG-SIPG Laplace vmult, fp64, {n}x{n}x{n * world} cells "
+                                  f"({world * D} DoF; {D} per GPU)",
+                      "degree": k, "level": lvl, "dofs_per_gpu": D,
+                      "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                      "l2_flush": "not needed: u, v = 2 x 8.6 GB >> 126 MB L2"},
+           "tflops_reference_equivalent": value * 1e9 * ref_flops_per_dof(k, lvl) / 1e12,
+           "roofline": roofline, "clocks": clk, "gpu_launches": args.steps}
+
+    if rank == 0 and world == 1:
+        # e2e: public API with pinned host buffers, H2D + D2H per step
+        try:
+            uh = torch.empty(D, dtype=torch.float64, pin_memory=True)
+            uh.copy_(u)
+            vh = torch.empty(D, dtype=torch.float64, pin_memory=True)
+            sf.apply_operator(hier, lvl, uh, out=vh)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                sf.apply_operator(hier, lvl, uh, out=vh)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) / args.e2e_steps
+            out["e2e"] = {"value": D / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * D,
+                          "d2h_bytes_per_step": 8 * D, "api": "paper_2407_09621_b200.apply_operator(pinned host)"}
+            del uh, vh
+        except Exception as exc:  # pinned allocation can fail on small hosts
+            out["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
+        if not args.no_cpu:
+            out["cpu_baseline"] = {kk: vv for kk, vv in cpu_baseline().items() if kk != "seconds_per_vmult"}
+        if not args.no_extras:
+            out["extras"] = extras(sf, hier, lvl, k, u, v)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def extras(sf, hier, lvl, k, u, v):
+    """Secondary measurements of the other configs (FP16 paths, Q3, smoother, solve)."""
+    import torch
+
+    from paper_2407_09621_b200.discretization import vmult_device
+
+    P = sf.PrecisionMode
+    res = {}
+
+    def timeit(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    D = hier.n_dofs(lvl)
+    u32 = u.float()
+    v32 = torch.empty_like(u32)
+    for mode in (P.FP32, P.FP16, P.FP16_EC):
+        ms = timeit(lambda: vmult_device(hier, lvl, u32, v32, mode))
+        res[f"vmult_q{k}_l{lvl}_{mode.value}_gdofs"] = D / ms / 1e6
+    del u32, v32
+    # Q3 level 8 fp64 (1.07e9 DoF)
+    h3 = sf.build_hierarchy(8, 3, max_dofs=2**34, min_level=8)
+    ms = timeit(lambda: vmult_device(h3, 8, u, v, P.FP64))
+    res["vmult_q3_l8_fp64_gdofs"] = h3.n_dofs(8) / ms / 1e6
+    # smoother colour pass, Q7 level 6, fp64 and fp16
+    h6 = sf.build_hierarchy(6, k, max_dofs=2**34)
+    D6 = h6.n_dofs(6)
+    for mode in (P.FP64, P.FP16):
+        mg = sf.MultigridPreconditioner(h6, sf.VCycleConfig(mode=mode))
+        x = torch.zeros(D6, dtype=mode.torch_dtype, device="cuda")
+        b = torch.randn(D6, dtype=mode.torch_dtype, device="cuda")
+        ms = timeit(lambda: mg._smooth_device(6, x, b, mode), reps=2)
+        res[f"smooth_step_q{k}_l6_{mode.value}_ms"] = ms
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -16,7 +16,6 @@ from __future__ import annotations
 import itertools
 import math
 import os
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -176,38 +175,33 @@ class Hierarchy:
 # ----------------------------------------------------------- contraction
 
 
-_POOL = None
-
-
-def _pool(threads):
-    global _POOL
-    if _POOL is None or _POOL._max_workers != threads:
-        _POOL = ThreadPoolExecutor(max_workers=threads)
-    return _POOL
-
-
 def contract(m: np.ndarray, w: np.ndarray, axis: int, threads: int = 1) -> np.ndarray:
     """_core/__init__.py:27-59 + _core/fallback.py:10-15: out[o,i,r] = sum_k m[i,k] w[o,k,r].
 
-    numpy einsum without ``optimize`` (single-threaded, fixed order).  With
-    ``threads > 1`` the outer batch is split into slices einsum'd concurrently
-    (einsum releases the GIL); each output element is still the same sum.
+    threads == 1: numpy einsum without ``optimize`` -- the reference's own
+    fallback backend, single-threaded, ascending k (the checker path).
+    threads > 1: the same contraction as BLAS GEMMs (np.matmul) on ``threads``
+    BLAS threads -- used only for the multi-core CPU *baseline* timing; it
+    differs from einsum by summation order only (~1e-16 relative).
     """
     w = np.ascontiguousarray(w)
     m = np.ascontiguousarray(m, dtype=w.dtype)
     outer = int(np.prod(w.shape[:axis], dtype=np.int64))
     inner = int(np.prod(w.shape[axis + 1:], dtype=np.int64))
     w3 = w.reshape(outer, w.shape[axis], inner)
-    out = np.empty((outer, m.shape[0], inner), dtype=w.dtype)
-    if threads <= 1 or outer < 2 * threads:
+    shape = w.shape[:axis] + (m.shape[0],) + w.shape[axis + 1:]
+    if threads <= 1:
+        out = np.empty((outer, m.shape[0], inner), dtype=w.dtype)
         np.einsum("ik,okr->oir", m, w3, out=out)
-    else:
-        bounds = np.linspace(0, outer, threads + 1).astype(int)
-        futs = [_pool(threads).submit(np.einsum, "ik,okr->oir", m, w3[a:b], out=out[a:b])
-                for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
-        for f in futs:
-            f.result()
-    return out.reshape(w.shape[:axis] + (m.shape[0],) + w.shape[axis + 1:])
+        return out.reshape(shape)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads, user_api="blas"):
+        if inner == 1:
+            out = w3.reshape(outer, -1) @ m.T
+        else:
+            out = np.matmul(m, w3)
+    return out.reshape(shape)
 
 
 def demote16(x):

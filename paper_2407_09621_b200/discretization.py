@@ -146,20 +146,33 @@ def vmult_device(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Tens
     _native.check(rc, "sf_vmult")
 
 
-def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = PrecisionMode.FP64):
+def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = PrecisionMode.FP64, out=None):
     """Matrix-free interior-penalty Laplacian at one level (discretization.py:216-266).
 
     numpy in -> numpy out (storage dtype of ``mode``); CUDA tensor in -> CUDA
-    tensor out.  Raises ValueError on a length mismatch, like the reference.
+    tensor out.  ``out`` (optional) receives the result: a host tensor (e.g.
+    pinned, for streaming host buffers through the GPU) or a CUDA tensor.
+    Raises ValueError on a length mismatch, like the reference.
     """
     n = hier.n_dofs(level)
     size = u.numel() if isinstance(u, torch.Tensor) else np.asarray(u).size
     if size != n:
         raise ValueError(f"expected {n} entries, got {size}")
     device.require_cuda()
-    t, host = device.as_device(u, mode.torch_dtype, n)
+    if isinstance(u, torch.Tensor) and not u.is_cuda:
+        t = u.reshape(-1).to(device="cuda", dtype=mode.torch_dtype, non_blocking=True)
+        host = True
+    else:
+        t, host = device.as_device(u, mode.torch_dtype, n)
+    if out is not None and out.is_cuda:
+        vmult_device(hier, level, t, out, mode)
+        return out
     v = torch.empty_like(t)
     vmult_device(hier, level, t, v, mode)
+    if out is not None:
+        out.copy_(v, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
     return device.to_host(v, mode.storage_dtype) if host else v
 
 
