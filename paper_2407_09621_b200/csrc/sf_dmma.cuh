@@ -1,0 +1,386 @@
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) tile toolkit for Q7 (K = 8):
+// one 2x2x2-cell tile = 16^3 dofs per CTA, 8 warps, two CTAs per SM.
+//
+// Every line contraction of the tile is a small GEMM  Y[line][out] = X[line][k] Op^T[k][out]
+// on 8-line groups: A = data (8 lines x 4 k) from shared memory, B = operator
+// fragment in registers, C/D = 8 lines x 8 outputs in registers.  The 16x16
+// line operators are the patch matrices themselves:
+//   mass       M_patch = blockdiag(M_cell, M_cell)      (4 DMMA per group)
+//   stiffness  L_smooth[kind]  (principal submatrix of the global 1-D operator,
+//              Nitsche rows at domain-boundary ends)    (8 DMMA per group)
+// and the coupling to the face neighbours outside the tile is the rank-2 U/U^T
+// update from the neighbour's face traces (alpha, beta), added to the C
+// fragment.  Schedule (cell-wise sum factorisation):
+//   prologue: tile -> smem (cp.async), neighbour face traces straight from
+//             L2/HBM (all loads in flight at once), tangential masses of the
+//             y/z trace planes on DMMA
+//   x:  a = Mx u,   b = Lx u (+ x halo)             -- warp owns z planes, in place
+//   y:  c = My a,  dd = Ly a (+ y halo) + My b      -- same warp, same planes, in place
+//   z:  v = Lz c (+ z halo) + Mz dd                 -- warp owns y rows, lines along x
+// Shared-memory layouts are XOR swizzles (the paper's conflict-free idea,
+// P:319) chosen so every A-fragment LDS.64 and C-fragment store of the three
+// stages is bank-conflict free:
+//   U layout : z*256 + y*16 + (x ^ 4(y&3))
+//   A layout : z*256 + y*16 + (x ^ {0,8,4,12}[y&3])
+//   C layout : z*256 + y*16 + (x ^ 4(((y>>1)+z)&3))
+#pragma once
+#include "sf_common.cuh"
+#include "sf_tile.cuh"
+
+namespace sf {
+namespace dm {
+
+constexpr int K = 8, B = 16, PLANE = 256, VOL = 4096;
+constexpr int TRP = 320;   // one trace plane: 16 rows x pitch 20 (pitch = 4 mod 16)
+constexpr int TRW = 20;
+constexpr int kThreads = 256;
+constexpr size_t kSmemTile = sizeof(double) * (2 * VOL + 12 * TRP + 4 * 8 * 32);
+
+__device__ __forceinline__ int idxU(int z, int y, int x) { return z * PLANE + y * 16 + (x ^ ((y & 3) << 2)); }
+__device__ __forceinline__ int swA(int y) { return ((y & 1) << 3) | ((y & 2) << 1); }  // {0,8,4,12}[y&3]
+__device__ __forceinline__ int idxA(int z, int y, int x) { return z * PLANE + y * 16 + (x ^ swA(y)); }
+__device__ __forceinline__ int idxC(int z, int y, int x) {
+  return z * PLANE + y * 16 + (x ^ ((((y >> 1) + z) & 3) << 2));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  // not volatile: no side effects, so ptxas may interleave independent DMMAs of several groups
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Operator fragments held by one lane.
+struct Frags {
+  double m[2];     // M_cell[lane>>2][4*kc + (lane&3)], kc = 0,1 (both cells)
+  double l[2][4];  // L[8nb + (lane>>2)][4kc + (lane&3)]
+};
+
+// acc[nb][2]: outputs 8nb + 2(lane&3) + {0,1} of line (lane>>2)
+// k-chunk outer, output block inner: consecutive DMMAs are independent
+__device__ __forceinline__ void mass_group(const Frags& f, const double* a, double (*acc)[2]) {
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) dmma(acc[nb][0], acc[nb][1], a[2 * nb + kc], f.m[kc]);
+}
+__device__ __forceinline__ void stiff_group(const Frags& f, const double* a, double (*acc)[2]) {
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) dmma(acc[nb][0], acc[nb][1], a[kc], f.l[nb][kc]);
+}
+
+// Shared state of one tile (pointers into the CTA's shared memory + geometry).
+struct Tile {
+  double* sU;   // u -> a -> c   (VOL)
+  double* sB;   // b -> dd       (VOL)
+  double* tr;   // 12 trace planes: (face*2 + {alpha,beta}) * TRP + p*TRW + q
+  double* sLf;  // L_smooth fragments [kind][nb*4+kc][lane]
+  int cx, cy, cz;
+  long long sy, sz;
+  unsigned nbm;             // bit 2*axis+hi: face neighbour present (inside the array or ghost)
+  int kind[3];
+  int r, k4, c2, lane, warp;
+};
+
+// 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary
+__device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0) {
+  int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
+  int c = hi ? c0 + 2 : c0 - 1;
+  if (c >= 0 && c < n) return 0;
+  if (hi ? g.bnd_hi[axis] : g.bnd_lo[axis]) return 2;
+  return 1;
+}
+
+__device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
+  if (tile_id >= g.ntx * g.nty * g.ntz) return false;
+  const int tx = tile_id % g.ntx, rr = tile_id / g.ntx;
+  T.cx = g.tx0 + 2 * tx;
+  T.cy = g.ty0 + 2 * (rr % g.nty);
+  T.cz = g.tz0 + 2 * (rr / g.nty);
+  T.sy = (long long)g.nx * K;
+  T.sz = T.sy * (long long)g.ny * K;
+  const int c0[3] = {T.cx, T.cy, T.cz};
+  T.nbm = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (face_src(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
+    if (face_src(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    T.kind[a] = patch_kind(g, a, c0[a]);
+  }
+  T.lane = threadIdx.x & 31;
+  T.warp = threadIdx.x >> 5;
+  T.r = T.lane >> 2;
+  T.k4 = T.lane & 3;
+  T.c2 = 2 * T.k4;
+  return true;
+}
+
+__device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g, int tile_id) {
+  T.sU = smem;
+  T.sB = smem + VOL;
+  T.tr = T.sB + VOL;
+  T.sLf = T.tr + 12 * TRP;
+  return tile_geom(T, g, tile_id);
+}
+
+// named barriers (id 0 is __syncthreads)
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// L_smooth[kind] as per-lane fragments: 4 kinds x 8 (nb,kc) x 32 lanes (conflict-free loads)
+__device__ __forceinline__ void stage_l_frags(const Tile& T, const double* Lsrc /* [4][16][16] */) {
+  for (int i = threadIdx.x; i < 4 * 8 * 32; i += kThreads) {
+    const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
+    const int nb = fr >> 2, kc = fr & 3;
+    T.sLf[i] = Lsrc[kind * 256 + (8 * nb + (ln >> 2)) * 16 + 4 * kc + (ln & 3)];
+  }
+}
+
+__device__ __forceinline__ void load_l(const Tile& T, Frags& f, int kind) {
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) f.l[nb][kc] = T.sLf[(kind * 8 + nb * 4 + kc) * 32 + T.lane];
+}
+
+// ---------------------------------------------------------------------------
+// Producer side of a tile: cp.async u -> sU (U layout); neighbour face traces
+// (alpha, beta) straight from L2/HBM into tr; then the tangential masses of the
+// y (Mx) and z (My Mx) trace planes on DMMA.  Executed by NP threads (tid in
+// [0, NP)); `bar` synchronises exactly those threads.
+template <int NP, class OpT, class Bar>
+__device__ __forceinline__ void produce(const Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                       const Frags& f, int tid, Bar bar) {
+  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  for (int c = tid; c < VOL / 2; c += NP) {
+    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
+    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
+  }
+  constexpr int IPT = 512 / NP;  // items per thread per axis (2 faces x 256 positions)
+#pragma unroll
+  for (int axis = 0; axis < 3; ++axis) {
+    double w[IPT][K];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int it = tid + NP * j;
+      const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
+      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
+      int X = T.cx * K, Y = T.cy * K, Z = T.cz * K;
+      long long step;
+      if (axis == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
+      else if (axis == 1) { Z += p; X += q; Y += hi ? B : -K; step = T.sy; }
+      else { Y += p; X += q; Z += hi ? B : -K; step = T.sz; }
+      const double* base;
+      if (axis == 2 && (Z < 0 || Z >= g.nz * K)) {
+        base = hi ? reinterpret_cast<const double*>(g.ghost_hi) + (long long)(Z - g.nz * K) * T.sz
+                  : reinterpret_cast<const double*>(g.ghost_lo) + (long long)(Z + K) * T.sz;
+        base += (long long)Y * T.sy + X;
+      } else {
+        base = u + (long long)Z * T.sz + (long long)Y * T.sy + X;
+      }
+      if (axis == 0) {
+#pragma unroll
+        for (int c = 0; c < K / 2; ++c) {
+          const double2 v2 = __ldg(reinterpret_cast<const double2*>(base + 2 * c));
+          w[j][2 * c] = v2.x;
+          w[j][2 * c + 1] = v2.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < K; ++c) w[j][c] = __ldg(base + c * step);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int it = tid + NP * j;
+      const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
+      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
+      double alpha, beta = 0.0;
+      if (hi) {
+        alpha = w[j][0];
+#pragma unroll
+        for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[j][c], beta);
+      } else {
+        alpha = w[j][K - 1];
+#pragma unroll
+        for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[j][c], beta);
+      }
+      double* pl = T.tr + (2 * axis + hi) * 2 * TRP;
+      pl[p * TRW + q] = alpha;
+      pl[TRP + p * TRW + q] = beta;
+    }
+  }
+  cp_async_wait_all();
+  bar();
+  // Mx along q on the y-face (2,3) and z-face (4,5) planes: 8 planes x 2 row groups
+  const int pw = tid >> 5;
+  for (int task = pw; task < 16; task += NP / 32) {
+    const int plane = 4 + (task >> 1);
+    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
+    double* P = T.tr + plane * TRP + (task & 1) * 8 * TRW;
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = P[T.r * TRW + 4 * kc + T.k4];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    mass_group(f, a, acc);
+    __syncwarp();
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      P[T.r * TRW + 8 * nb + T.c2] = acc[nb][0];
+      P[T.r * TRW + 8 * nb + T.c2 + 1] = acc[nb][1];
+    }
+  }
+  bar();
+  // My along p on the z-face planes: 4 planes x 2 column groups
+  for (int task = pw; task < 8; task += NP / 32) {
+    const int plane = 8 + (task >> 1);
+    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
+    double* P = T.tr + plane * TRP + (task & 1) * 8;
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = P[(4 * kc + T.k4) * TRW + T.r];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    mass_group(f, a, acc);
+    __syncwarp();
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      P[(8 * nb + T.c2) * TRW + T.r] = acc[nb][0];
+      P[(8 * nb + T.c2 + 1) * TRW + T.r] = acc[nb][1];
+    }
+  }
+}
+
+// whole CTA as producer (non-specialised kernels)
+template <class OpT>
+__device__ __forceinline__ void prologue(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                         const Frags& f) {
+  produce<kThreads>(T, g, op, u, f, threadIdx.x, [] { __syncthreads(); });
+  __syncthreads();
+}
+
+// rank-2 halo update of a stiffness fragment (lo neighbour -> cell 0, hi -> cell 1)
+struct Halo {
+  double ur[2], uc[2];
+  __device__ __forceinline__ void apply(const Tile& T, double (*acc)[2], int axis, int t) const {
+    if ((T.nbm >> (2 * axis)) & 1) {
+      const double* pl = T.tr + (2 * axis) * 2 * TRP;
+      const double alo = pl[t], blo = pl[TRP + t];
+      acc[0][0] = fma(ur[0], alo, acc[0][0]);
+      acc[0][1] = fma(ur[1], alo, acc[0][1]);
+      if (T.c2 == 0) acc[0][0] += blo;
+    }
+    if ((T.nbm >> (2 * axis + 1)) & 1) {
+      const double* pl = T.tr + (2 * axis + 1) * 2 * TRP;
+      const double ahi = pl[t], bhi = pl[TRP + t];
+      acc[1][0] = fma(uc[0], ahi, acc[1][0]);
+      acc[1][1] = fma(uc[1], ahi, acc[1][1]);
+      if (T.c2 + 1 == K - 1) acc[1][1] += bhi;
+    }
+  }
+};
+
+// x and y stages on the warp's two z planes (in place: U <- a <- c, B <- b <- dd)
+__device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h) {
+  for (int zz = 0; zz < 2; ++zz) {
+    const int z = 2 * T.warp + zz;
+    load_l(T, f, T.kind[0]);
+    double ra[2][2][2], rb[2][2][2];
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int y = 8 * g8 + T.r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU(z, y, 4 * kc + T.k4)];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
+      mass_group(f, a, ra[g8]);
+      stiff_group(f, a, rb[g8]);
+      h.apply(T, rb[g8], 0, z * TRW + y);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int y = 8 * g8 + T.r;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int i = idxA(z, y, 8 * nb + T.c2);
+        *reinterpret_cast<double2*>(&T.sU[i]) = make_double2(ra[g8][nb][0], ra[g8][nb][1]);
+        *reinterpret_cast<double2*>(&T.sB[i]) = make_double2(rb[g8][nb][0], rb[g8][nb][1]);
+      }
+    }
+    __syncwarp();
+    load_l(T, f, T.kind[1]);
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + T.r;
+      double a[4], b[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        a[kc] = T.sU[idxA(z, 4 * kc + T.k4, x)];
+        b[kc] = T.sB[idxA(z, 4 * kc + T.k4, x)];
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
+      mass_group(f, a, ra[g8]);   // c = My a
+      stiff_group(f, a, rb[g8]);  // d = Ly a
+      h.apply(T, rb[g8], 1, z * TRW + x);
+      mass_group(f, b, rb[g8]);   // dd = d + My b
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + T.r;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int j = idxC(z, 8 * nb + T.c2 + i, x);
+          T.sU[j] = ra[g8][nb][i];
+          T.sB[j] = rb[g8][nb][i];
+        }
+    }
+    __syncwarp();
+  }
+}
+
+// z stage for one group: lines x = x0 + r at row y; acc = (A u) C fragment [line][z]
+__device__ __forceinline__ void z_group(const Tile& T, const Frags& f, const Halo& h, int y, int x0,
+                                       double (*acc)[2]) {
+  const int x = x0 + T.r;
+  double cc[4], dd[4];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) {
+    cc[kc] = T.sU[idxC(4 * kc + T.k4, y, x)];
+    dd[kc] = T.sB[idxC(4 * kc + T.k4, y, x)];
+  }
+  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+  stiff_group(f, cc, acc);
+  h.apply(T, acc, 2, y * TRW + x);
+  mass_group(f, dd, acc);
+}
+
+template <class OpT>
+__device__ __forceinline__ void init_frags(const Tile& T, const OpT& op, Frags& f, Halo& h) {
+  f.m[0] = op.M[T.r][T.k4].h;
+  f.m[1] = op.M[T.r][4 + T.k4].h;
+  h.ur[0] = op.urow[T.c2].h;
+  h.ur[1] = op.urow[T.c2 + 1].h;
+  h.uc[0] = op.ucol[T.c2].h;
+  h.uc[1] = op.ucol[T.c2 + 1].h;
+}
+
+}  // namespace dm
+}  // namespace sf

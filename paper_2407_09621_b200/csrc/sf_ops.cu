@@ -11,6 +11,8 @@
 #include "sf_common.cuh"
 #include "sf_tile.cuh"
 #include "../../include/sumfact_b200.h"
+#include "sf_internal.h"
+#include <cstdlib>
 
 namespace sf {
 
@@ -60,12 +62,6 @@ __device__ __forceinline__ void full_line(const ME<MODE>* A, const Op<MODE>* w, 
     for (int j = 0; j < B; ++j) acc[i].fma(TRANS ? A[j * B + i] : A[i * B + j], w[j]);
 }
 
-__device__ __forceinline__ int patch_kind(const Geom& g, int axis, int c0) {
-  int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
-  int lb = (c0 == 0 && g.bnd_lo[axis]) ? 1 : 0;
-  int rb = (c0 + 2 == n && g.bnd_hi[axis]) ? 1 : 0;
-  return 2 * lb + rb;
-}
 
 // --------------------------------------------------- smoother colour pass
 // One colour (tiling shift) of the multiplicative vertex-patch smoother,
@@ -543,11 +539,26 @@ static int set_smem(F* kern, size_t bytes) {
   return SF_OK;
 }
 
+// SUMFACT_B200_GENERIC=1 forces the CUDA-core tile engine (A/B testing of the tensor-core paths)
+static bool use_generic() {
+  static int v = [] {
+    const char* e = getenv("SUMFACT_B200_GENERIC");
+    return (e && *e && *e != '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 template <int K, int MODE>
 static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   Geom g;
   int rc = make_geom(gr, K, 0, 0, 0, g);
   if (rc) return rc;
+  if constexpr (K == 8 && MODE == MODE_FP64) {
+    if (!use_generic()) {
+      if (launch_vmult_dmma8(g, opd, u, v, batch, st)) return check_launch("sf_vmult (dmma)");
+      return SF_OK;
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   auto op = pack_op<K, MODE>(opd);

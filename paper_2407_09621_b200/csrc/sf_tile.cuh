@@ -87,6 +87,14 @@ __device__ __forceinline__ void cell_line(const ME<MODE> (*Mt)[K], const Op<MODE
       for (int j = 0; j < K; ++j) acc[c * K + i].fma(Mt[i][j], w[c * K + j]);
 }
 
+// boundary kind of a 2-cell patch along an axis: 2*left_at_domain_boundary + right_at_domain_boundary
+__device__ __forceinline__ int patch_kind(const Geom& g, int axis, int c0) {
+  int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
+  int lb = (c0 == 0 && g.bnd_lo[axis]) ? 1 : 0;
+  int rb = (c0 + 2 == n && g.bnd_hi[axis]) ? 1 : 0;
+  return 2 * lb + rb;
+}
+
 template <int K, int MODE, int TPC>
 struct TileEngine {
   static constexpr int B = 2 * K;

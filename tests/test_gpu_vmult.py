@@ -127,3 +127,22 @@ def test_slab_ghosts_reproduce_the_full_operator():
     vmult_device(hier, lvl, hi, out_hi, P.FP64, grid=_native.SfGrid(n, n, n // 2, g_hi.data_ptr(), None))
     got = torch.cat([out_lo, out_hi])
     assert float(torch.linalg.norm(got - full) / torch.linalg.norm(full)) <= 1e-14
+
+
+def test_tensor_core_path_matches_cuda_core_path(tmp_path):
+    """The DMMA Q7 kernel and the generic CUDA-core tile engine agree (SUMFACT_B200_GENERIC=1)."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); import paper_2407_09621_b200 as sf; "
+            "h = sf.build_hierarchy(3, 7); u = np.random.default_rng(11).standard_normal(h.n_dofs(3)); "
+            "np.save(%r, sf.apply_operator(h, 3, u))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"v{flag}.npy")
+        env = dict(os.environ, SUMFACT_B200_GENERIC=flag)
+        subprocess.run([sys.executable, "-c", code % (root, path)], check=True, env=env)
+        outs.append(np.load(path))
+    assert rel_l2(outs[0], outs[1]) <= 1e-14
