@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "sf_dmma.cuh"
 #include "sf_internal.h"
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* 
   const int tid = threadIdx.x;
   Tile T;
   T.sB = sB;
-  T.sLf = sLf;
+  T.sLf = sLf;  // written below through the non-const alias
   tile_geom(T, g, 0);  // lane/warp fields
   for (int i = tid; i < 4 * 8 * 32; i += kWsThreads) {
     const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
@@ -179,6 +181,235 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident operator fragment tables of one level (fp64, K = 8).
+// Fragment slot fr = 4*nb + kc of lane ln holds B[k][n] = Op[8nb + (ln>>2)][k-index]:
+//   std : k-index = 4kc + (ln&3)             (A fragment loaded from shared memory)
+//   perm: k-index = 8(kc>>1) + 2(ln&3) + (kc&1)  (A fragment = the previous C fragment,
+//         so two contractions along the same axis chain in registers)
+struct Tables8 {
+  double L[4][8][32];    // L_smooth[kind], std
+  double Vf[4][8][32];   // Op = V^T (forward transform), std
+  double Vfp[4][8][32];  // Op = V^T, perm
+  double Vb[4][8][32];   // Op = V (backward transform), std
+  double Vbp[4][8][32];  // Op = V, perm
+  double lam[4][16];     // generalised eigenvalues per kind
+};
+
+__device__ __forceinline__ void load_frag(const double* tab /* [8][32] */, double (*l)[4], int lane) {
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) l[nb][kc] = __ldg(tab + (nb * 4 + kc) * 32 + lane);
+}
+
+// acc += A . Op^T with 16 inputs (4 k-chunks) and 16 outputs (2 n-blocks)
+__device__ __forceinline__ void full_group(const double (*l)[4], const double* a, double (*acc)[2]) {
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) dmma(acc[nb][0], acc[nb][1], a[kc], l[nb][kc]);
+}
+
+// One colour of the vertex-patch smoother on DMMA (multigrid.py:186-203): per
+// patch tile r = b - A x_old, x_new = x_old + (V_z V_y V_x) Lambda^-1 (V_x^T V_y^T V_z^T) r.
+// Stage order: residual z-lines -> V_z^T (registers) | V_y^T | V_x^T, 1/lambda,
+// V_x (registers) | V_y | V_z -> +x_old -> HBM; '|' = shared-memory transpose.
+__global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __restrict__ xo,
+                                                             const double* __restrict__ b, double* __restrict__ xn,
+                                                             Geom g, LevelOp<K, MODE_FP64> op,
+                                                             const Tables8* __restrict__ tab) {
+  extern __shared__ __align__(128) double smem[];
+  Tile T;
+  if (!tile_setup(T, smem, g, blockIdx.x)) return;
+  T.sLf = &tab->L[0][0][0];
+  Frags f;
+  Halo h;
+  init_frags(T, op, f, h);
+  prologue(T, g, op, xo, f);
+  xy_stages(T, f, h);
+  __syncthreads();
+  const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
+  const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
+  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  double V[2][4];
+  // ---- z lines: residual and forward V_z^T (chained in registers), out in T layout
+  load_l(T, f, kz);
+  load_frag(&tab->Vfp[kz][0][0], V, lane);
+  {
+    double t[2][2][2][2];
+#pragma unroll
+    for (int yy = 0; yy < 2; ++yy) {
+      const int y = 2 * w + yy;
+#pragma unroll
+      for (int g8 = 0; g8 < 2; ++g8) {
+        double acc[2][2];
+        z_group(T, f, h, y, 8 * g8, acc);
+        const int x = 8 * g8 + r;
+        double a[4];
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const int z = 8 * (kc >> 1) + c2 + (kc & 1);
+          a[kc] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - acc[kc >> 1][kc & 1];
+        }
+        double (*o)[2] = t[yy][g8];
+        o[0][0] = o[0][1] = o[1][0] = o[1][1] = 0.0;
+        full_group(V, a, o);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+      for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) T.sU[idxT(8 * nb + c2 + i, 2 * w + yy, 8 * g8 + r)] = t[yy][g8][nb][i];
+  }
+  __syncthreads();
+  // ---- warp-private z' planes: V_y^T | V_x^T, 1/lambda, V_x | V_y
+  const double* lamx = tab->lam[kx];
+  const double* lamy = tab->lam[ky];
+  const double* lamz = tab->lam[kz];
+  for (int zz = 0; zz < 2; ++zz) {
+    const int z = 2 * w + zz;
+    double o[2][2][2];
+    load_frag(&tab->Vf[ky][0][0], V, lane);
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxT(z, 4 * kc + T.k4, x)];
+      o[g8][0][0] = o[g8][0][1] = o[g8][1][0] = o[g8][1][1] = 0.0;
+      full_group(V, a, o[g8]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) T.sU[idxG(z, 8 * nb + c2 + i, 8 * g8 + r)] = o[g8][nb][i];
+    __syncwarp();
+    load_frag(&tab->Vf[kx][0][0], V, lane);
+    double Vb[2][4];
+    load_frag(&tab->Vbp[kx][0][0], Vb, lane);
+    const double lz = 0.0 + __ldg(lamz + z);
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int y = 8 * g8 + r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxG(z, y, 4 * kc + T.k4)];
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      full_group(V, a, acc);
+      const double lzy = lz + __ldg(lamy + y);
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        const int x = 8 * (kc >> 1) + c2 + (kc & 1);
+        a[kc] = acc[kc >> 1][kc & 1] / (lzy + __ldg(lamx + x));
+      }
+      o[g8][0][0] = o[g8][0][1] = o[g8][1][0] = o[g8][1][1] = 0.0;
+      full_group(Vb, a, o[g8]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+        *reinterpret_cast<double2*>(&T.sU[idxA(z, 8 * g8 + r, 8 * nb + c2)]) = make_double2(o[g8][nb][0], o[g8][nb][1]);
+    __syncwarp();
+    load_frag(&tab->Vb[ky][0][0], V, lane);
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxA(z, 4 * kc + T.k4, x)];
+      o[g8][0][0] = o[g8][0][1] = o[g8][1][0] = o[g8][1][1] = 0.0;
+      full_group(V, a, o[g8]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) T.sU[idxC(z, 8 * nb + c2 + i, 8 * g8 + r)] = o[g8][nb][i];
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- z lines: backward V_z, x_new = x_old + correction
+  load_frag(&tab->Vb[kz][0][0], V, lane);
+  for (int yy = 0; yy < 2; ++yy) {
+    const int y = 2 * w + yy;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxC(4 * kc + T.k4, y, x)];
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      full_group(V, a, acc);
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const long long o = off0 + (long long)(8 * nb + c2 + i) * T.sz + (long long)y * T.sy + x;
+          xn[o] = __ldg(xo + o) + acc[nb][i];
+        }
+    }
+  }
+}
+
+static Tables8 build_tables8(const double* opd, const double* eigd) {
+  PatchL pl = build_patch_l(opd);
+  Tables8 t;
+  auto perm = [](int kc, int c) { return 8 * (kc >> 1) + 2 * c + (kc & 1); };
+  for (int q = 0; q < 4; ++q) {
+    const double* V = eigd + q * 256;  // V[i][j], row-major
+    for (int fr = 0; fr < 8; ++fr)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int nb = fr >> 2, kc = fr & 3, n = 8 * nb + (ln >> 2), c = ln & 3;
+        const int ks = 4 * kc + c, kp = perm(kc, c);
+        t.L[q][fr][ln] = pl.L[q][n][ks];
+        t.Vf[q][fr][ln] = V[ks * 16 + n];   // (V^T)[n][k] = V[k][n]
+        t.Vfp[q][fr][ln] = V[kp * 16 + n];
+        t.Vb[q][fr][ln] = V[n * 16 + ks];
+        t.Vbp[q][fr][ln] = V[n * 16 + kp];
+      }
+    for (int i = 0; i < 16; ++i) t.lam[q][i] = eigd[4 * 256 + q * 16 + i];
+  }
+  return t;
+}
+
+// content-addressed cache of uploaded tables (setup-time cudaMalloc/cudaMemcpy)
+static std::mutex g_tab_mu;
+struct TabEntry {
+  int dev;
+  std::vector<double> key;
+  void* ptr;
+};
+static std::vector<TabEntry> g_tabs;
+
+static const Tables8* tables8(const double* opd, const double* eigd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(opd, opd + 2 * K * K + 4 * K);
+  key.insert(key.end(), eigd, eigd + 4 * 256 + 4 * 16);
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_tabs)
+    if (e.dev == dev && e.key == key) return reinterpret_cast<const Tables8*>(e.ptr);
+  Tables8 host = build_tables8(opd, eigd);
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(Tables8)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(Tables8), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_tabs.push_back({dev, std::move(key), d});
+  return reinterpret_cast<const Tables8*>(d);
+}
+
 }  // namespace dm
 
 int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
@@ -187,7 +418,7 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
   dm::PatchL pl = dm::build_patch_l(opd);
   static const int ws = [] {
     const char* e = getenv("SUMFACT_B200_DMMA_WS");
-    return (e && *e == '0') ? 0 : 1;
+    return (e && *e == '1') ? 1 : 0;  // opt-in: measured slower than two independent CTAs per SM
   }();
   if (ws && batch == 1) {
     cudaError_t err =
@@ -211,4 +442,20 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+}  // namespace sf
+
+namespace sf {
+int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
+                        cudaStream_t st) {
+  const dm::Tables8* tab = dm::tables8(opd, eigd);
+  if (!tab) return -3;
+  auto op = dm::pack_op64(opd);
+  cudaError_t err =
+      cudaFuncSetAttribute(dm::k_colour_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
+  if (err != cudaSuccess) return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  dm::k_colour_dmma8<<<tiles, dm::kThreads, dm::kSmemTile, st>>>((const double*)xo, (const double*)b, (double*)xn, g,
+                                                                  op, tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
 }  // namespace sf

@@ -42,6 +42,13 @@ __device__ __forceinline__ int idxA(int z, int y, int x) { return z * PLANE + y 
 __device__ __forceinline__ int idxC(int z, int y, int x) {
   return z * PLANE + y * 16 + (x ^ ((((y >> 1) + z) & 3) << 2));
 }
+// smoother layouts: T = C with the roles of y and z swapped, G = Gray-code swizzle
+__device__ __forceinline__ int idxT(int z, int y, int x) {
+  return z * PLANE + y * 16 + (x ^ ((((z >> 1) + y) & 3) << 2));
+}
+__device__ __forceinline__ int idxG(int z, int y, int x) {
+  return z * PLANE + y * 16 + (x ^ (((y ^ (y >> 1)) & 3) << 2));
+}
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   // not volatile: no side effects, so ptxas may interleave independent DMMAs of several groups
@@ -82,7 +89,7 @@ struct Tile {
   double* sU;   // u -> a -> c   (VOL)
   double* sB;   // b -> dd       (VOL)
   double* tr;   // 12 trace planes: (face*2 + {alpha,beta}) * TRP + p*TRW + q
-  double* sLf;  // L_smooth fragments [kind][nb*4+kc][lane]
+  const double* sLf;  // L_smooth fragments [kind][nb*4+kc][lane] (shared or global)
   int cx, cy, cz;
   long long sy, sz;
   unsigned nbm;             // bit 2*axis+hi: face neighbour present (inside the array or ghost)
@@ -142,10 +149,11 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 
 // L_smooth[kind] as per-lane fragments: 4 kinds x 8 (nb,kc) x 32 lanes (conflict-free loads)
 __device__ __forceinline__ void stage_l_frags(const Tile& T, const double* Lsrc /* [4][16][16] */) {
+  double* dst = const_cast<double*>(T.sLf);
   for (int i = threadIdx.x; i < 4 * 8 * 32; i += kThreads) {
     const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
     const int nb = fr >> 2, kc = fr & 3;
-    T.sLf[i] = Lsrc[kind * 256 + (8 * nb + (ln >> 2)) * 16 + 4 * kc + (ln & 3)];
+    dst[i] = Lsrc[kind * 256 + (8 * nb + (ln >> 2)) * 16 + 4 * kc + (ln & 3)];
   }
 }
 

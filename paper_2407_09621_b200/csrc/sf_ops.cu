@@ -588,13 +588,23 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
       return check_launch("sf_smooth_colour copy");
     return SF_OK;
   }
-  auto op = pack_op<K, MODE>(opd);
-  auto eig = pack_eig<K, MODE>(eigd);
-  size_t smem = E::smem_bytes() + sizeof(ME<MODE>) * 4 * 4 * K * K + sizeof(double) * 8 * K;
-  if ((rc = set_smem(k_colour<K, MODE>, smem))) return rc;
-  int tiles = g.ntx * g.nty * g.ntz;
-  k_colour<K, MODE><<<(tiles + TPC - 1) / TPC, kThreads, smem, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op, eig);
-  if ((rc = check_launch("sf_smooth_colour"))) return rc;
+  bool done = false;
+  if constexpr (K == 8 && MODE == MODE_FP64) {
+    if (!use_generic()) {
+      if (launch_colour_dmma8(g, opd, eigd, xo, b, xn, st)) return check_launch("sf_smooth_colour (dmma)");
+      done = true;
+    }
+  }
+  if (!done) {
+    auto op = pack_op<K, MODE>(opd);
+    auto eig = pack_eig<K, MODE>(eigd);
+    size_t smem = E::smem_bytes() + sizeof(ME<MODE>) * 4 * 4 * K * K + sizeof(double) * 8 * K;
+    if ((rc = set_smem(k_colour<K, MODE>, smem))) return rc;
+    int tiles = g.ntx * g.nty * g.ntz;
+    k_colour<K, MODE><<<(tiles + TPC - 1) / TPC, kThreads, smem, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op,
+                                                                        eig);
+    if ((rc = check_launch("sf_smooth_colour"))) return rc;
+  }
   if (shift[0] || shift[1] || shift[2]) {
     k_copy_slabs<S><<<148 * 4, 256, 0, st>>>((const S*)xo, (S*)xn, K, gr->nx, gr->ny, gr->nz, shift[0], shift[1],
                                              shift[2]);

@@ -149,3 +149,36 @@ def test_vcycle_contraction(k):
     for _ in range(3):
         x = mg.vcycle(x, b, 3)
     assert np.linalg.norm(x - x_true) <= 0.5**3 * e0
+
+
+def test_tensor_core_smoother_matches_cuda_core_smoother(tmp_path):
+    """The DMMA Q7 colour kernel and the generic CUDA-core one agree (SUMFACT_B200_GENERIC=1)."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); import paper_2407_09621_b200 as sf; "
+            "h = sf.build_hierarchy(3, 7); n = h.n_dofs(3); "
+            "x = np.random.default_rng(1).standard_normal(n); b = np.random.default_rng(2).standard_normal(n); "
+            "np.save(%r, sf.MultigridPreconditioner(h).smooth(3, x, b))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"s{flag}.npy")
+        subprocess.run([sys.executable, "-c", code % (root, path)], check=True,
+                       env=dict(os.environ, SUMFACT_B200_GENERIC=flag))
+        outs.append(np.load(path))
+    assert rel_l2(outs[0], outs[1]) <= 1e-13
+
+
+@pytest.mark.parametrize("lvl", [3, 4])
+def test_q7_smoother_matches_oracle(lvl):
+    """Q7 smoother (DMMA path) against the CPU oracle at the sizes it finishes quickly."""
+    from oracle import port
+
+    hier = sf.build_hierarchy(lvl, 7)
+    D = hier.n_dofs(lvl)
+    x, b = unit(np.random.default_rng(5), D), unit(np.random.default_rng(6), D)
+    got = sf.MultigridPreconditioner(hier).smooth(lvl, x, b)
+    ref = port.VCycle(port.Hierarchy(lvl, 7)).smooth(lvl, x, b)
+    assert rel_l2(got, ref) <= 1e-11
