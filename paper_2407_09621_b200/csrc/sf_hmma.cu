@@ -1,0 +1,719 @@
+// FP16 / FP16-EC tensor-core kernels for Q7 (K = 8): vmult and smoother colour
+// pass with mma.sync.m16n8k16 (f16 x f16 -> f32), ldmatrix/stmatrix operand
+// staging and the reference's per-contraction demotion semantics
+// (precision.py:206-230):
+//   fp16    : every contraction's input tensor and matrix are binary16 (RNE,
+//             subnormals kept); products are exact in f32; f32 accumulation.
+//   fp16_ec : main = A_h B_h, corr = A_d B_h + A_h B_d with the 2^11-scaled
+//             residual halves d; result = main + corr / 2048.
+// Intermediate tensors therefore live in shared memory as binary16 (plus the
+// residual half for EC): demotion happens exactly once, where the reference's
+// next contraction would demote them.
+//
+// Tile = 2x2x2 cells = 16^3 dofs, 4 warps, f32 vectors in HBM (fp32 storage).
+// One 16-line group is one m16 MMA tile; a 16 -> 16 line operator is two
+// m16n8k16 MMAs.  Same cell-wise schedule as the FP64 path (sf_dmma.cuh):
+//   x: a = Mx u, b = Lx u (+halo) | y: c = My a, dd = Ly a (+halo) + My b | z: v = Lz c (+halo) + Mz dd
+// The accumulator fragment of m16n8k16 is the A fragment of the next MMA, so
+// contractions along the same axis chain in registers (smoother: z fwd, x fwd/bwd).
+// Shared layout (halves): z*264 + y*16 + 8*((x>>3) ^ ((y>>2)&1)) + (x&7): every
+// ldmatrix/stmatrix 8x8 access (rows along y or z) is bank-conflict free.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "sf_common.cuh"
+#include "sf_internal.h"
+#include "sf_tile.cuh"
+
+namespace sf {
+namespace hm {
+
+constexpr int K = 8, B = 16;
+constexpr int PZ = 264;            // halves per z plane (256 + 8 pad)
+constexpr int TVOL = 16 * PZ;      // halves per tile tensor
+constexpr int kThreads = 128;      // 4 warps
+constexpr float kEc = 2048.0f;
+
+__device__ __forceinline__ int hidx(int z, int y, int x) {
+  return z * PZ + y * 16 + ((((x >> 3) ^ (y >> 2)) & 1) << 3) + (x & 7);
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void ldsm4(unsigned (&r)[4], const __half* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm4t(unsigned (&r)[4], const __half* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void stsm4(__half* p, const unsigned (&r)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(smem_u32(p)), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+__device__ __forceinline__ void stsm4t(__half* p, const unsigned (&r)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(smem_u32(p)),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+
+// D(16x8,f32) += A(16x16,f16) B(16x8,f16)
+__device__ __forceinline__ void hmma(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ unsigned pack2(float lo, float hi) {
+  __half2 h = __halves2half2(__float2half_rn(lo), __float2half_rn(hi));
+  return *reinterpret_cast<unsigned*>(&h);
+}
+__device__ __forceinline__ float2 unpack2(unsigned u) {
+  __half2 h = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(h);
+}
+
+// A 16-line x 16-output accumulator: two n8 tiles, f32; EC keeps main and corr.
+template <int MODE>
+struct Acc16 {
+  float m[2][4];
+  float c[2][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) m[nt][i] = c[nt][i] = 0.f;
+  }
+  // output value (nt, i) after the contraction: main (+ corr/2048 for EC)
+  __device__ __forceinline__ float val(int nt, int i) const {
+    if constexpr (MODE == MODE_FP16_EC) return m[nt][i] + c[nt][i] / kEc;
+    return m[nt][i];
+  }
+};
+
+// A fragment of one operand tensor: main halves (+ EC residual halves)
+template <int MODE>
+struct AFrag {
+  unsigned h[4];
+  unsigned d[4];
+};
+
+// B fragments of one 16x16 operator: [nt][reg] (+ EC residual)
+template <int MODE>
+struct BFrag {
+  unsigned h[2][2];
+  unsigned d[2][2];
+};
+
+template <int MODE>
+__device__ __forceinline__ void mma16(Acc16<MODE>& acc, const AFrag<MODE>& a, const BFrag<MODE>& b) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    hmma(acc.m[nt], a.h, b.h[nt][0], b.h[nt][1]);
+    if constexpr (MODE == MODE_FP16_EC) {
+      hmma(acc.c[nt], a.h, b.d[nt][0], b.d[nt][1]);  // c(mh, du) part: A_h B_d ...
+      hmma(acc.c[nt], a.d, b.h[nt][0], b.h[nt][1]);  // ... and A_d B_h
+    }
+  }
+}
+
+// split an f32 value into the operand halves of the mode
+template <int MODE>
+__device__ __forceinline__ void split(float x, float& h, float& d) {
+  h = __half2float(__float2half_rn(x));
+  d = (MODE == MODE_FP16_EC) ? __half2float(__float2half_rn((x - h) * kEc)) : 0.f;
+}
+
+// accumulator fragment -> A fragment of the next MMA (same axis), with demotion
+template <int MODE>
+__device__ __forceinline__ void acc_to_a(const float (&v)[2][4], AFrag<MODE>& a) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    float h0, d0, h1, d1, h2, d2, h3, d3;
+    split<MODE>(v[nt][0], h0, d0);
+    split<MODE>(v[nt][1], h1, d1);
+    split<MODE>(v[nt][2], h2, d2);
+    split<MODE>(v[nt][3], h3, d3);
+    a.h[2 * nt] = pack2(h0, h1);
+    a.h[2 * nt + 1] = pack2(h2, h3);
+    if constexpr (MODE == MODE_FP16_EC) {
+      a.d[2 * nt] = pack2(d0, d1);
+      a.d[2 * nt + 1] = pack2(d2, d3);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- tables
+// B fragment of Op (16 out x 16 in) for lane ln, n tile nt, register j:
+//   (Op[8nt + (ln>>2)][2(ln&3) + 8j], Op[...][... + 1]) as half2 (+ EC residual half2)
+struct HTables {
+  unsigned M[2][2][2][32];      // [h/d][nt][j][lane]  M_patch
+  unsigned L[4][2][2][2][32];   // [kind][h/d][nt][j][lane]  L_smooth[kind]
+  unsigned Vf[4][2][2][2][32];  // Op = V^T
+  unsigned Vb[4][2][2][2][32];  // Op = V
+  double lam[4][16];
+  float ucol[2][K], urow[2][K];  // [h/d] demoted halo vectors
+};
+
+template <int MODE>
+__device__ __forceinline__ void load_b(BFrag<MODE>& b, const unsigned* t /* [2][2][2][32] */, int lane) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      b.h[nt][j] = __ldg(t + (0 * 4 + nt * 2 + j) * 32 + lane);
+      if constexpr (MODE == MODE_FP16_EC) b.d[nt][j] = __ldg(t + (1 * 4 + nt * 2 + j) * 32 + lane);
+    }
+}
+
+// ---------------------------------------------------------------- tile
+template <int MODE>
+struct HTile {
+  __half* uh;  // tensor U (h) ; EC residual at uh + 2*TVOL
+  __half* bh;  // tensor B (h) ; EC residual at bh + 2*TVOL
+  float* tr;   // V1 trace planes (12 x 16 x 17 f32)
+  int cx, cy, cz;
+  long long sy, sz;
+  unsigned nbm;
+  int kind[3];
+  int lane, warp, g, t;
+  __device__ __forceinline__ __half* ud() const { return uh + 2 * TVOL; }
+  __device__ __forceinline__ __half* bd() const { return bh + 2 * TVOL; }
+};
+
+template <int MODE>
+constexpr size_t smem_bytes() {
+  return sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL + sizeof(float) * 12 * 16 * 17;
+}
+
+// store a value into (h, d) tensors at half index i
+template <int MODE>
+__device__ __forceinline__ void put(__half* h, __half* d, int i, float x) {
+  float hh, dd;
+  split<MODE>(x, hh, dd);
+  h[i] = __float2half_rn(hh);
+  if constexpr (MODE == MODE_FP16_EC) d[i] = __float2half_rn(dd);
+}
+
+template <int MODE>
+__device__ __forceinline__ void ld_a(AFrag<MODE>& a, const __half* h, const __half* d, int off, bool trans) {
+  if (trans) {
+    ldsm4t(a.h, h + off);
+    if constexpr (MODE == MODE_FP16_EC) ldsm4t(a.d, d + off);
+  } else {
+    ldsm4(a.h, h + off);
+    if constexpr (MODE == MODE_FP16_EC) ldsm4(a.d, d + off);
+  }
+}
+
+// store accumulator values (already final f32) via stmatrix as (h, d)
+template <int MODE>
+__device__ __forceinline__ void st_acc(__half* h, __half* d, int off, const float (&v)[2][4], bool trans) {
+  AFrag<MODE> a;
+  acc_to_a<MODE>(v, a);
+  // A fragment regs (0: rows 0-7 k 0-7, 1: rows 8-15 k 0-7, 2: rows 0-7 k 8-15, 3: rows 8-15 k 8-15)
+  // map onto stmatrix matrices in the same order as the ldmatrix addressing used here.
+  if (trans) {
+    stsm4t(h + off, a.h);
+    if constexpr (MODE == MODE_FP16_EC) stsm4t(d + off, a.d);
+  } else {
+    stsm4(h + off, a.h);
+    if constexpr (MODE == MODE_FP16_EC) stsm4(d + off, a.d);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void finals(const Acc16<MODE>& acc, float (&v)[2][4]) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[nt][i] = acc.val(nt, i);
+}
+
+// ldmatrix / stmatrix lane address for a 16x16 operand:
+//   non-trans (rows along the "line" axis a1, k along x):  line = j + 8(q&1), k0 = 8(q>>1)
+//   trans     (memory rows along the k axis):                krow = j + 8(q>>1), line0 = 8(q&1)
+__device__ __forceinline__ void lane_qj(int lane, int& q, int& j) {
+  q = lane >> 3;
+  j = lane & 7;
+}
+
+// halo update on a stiffness accumulator of 16 lines; alpha/beta per line from the trace plane
+template <int MODE>
+__device__ __forceinline__ void halo16(const HTile<MODE>& T, Acc16<MODE>& acc, const HTables* tab, int axis,
+                                       const float* tr_lo_a, const float* tr_lo_b, const float* tr_hi_a,
+                                       const float* tr_hi_b) {
+  // lines g and g+8 (rows of the accumulator), outputs n = 8nt + 2t + {0,1}
+  const int g = T.g, t2 = 2 * T.t;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int line = g + 8 * rr;
+    if ((T.nbm >> (2 * axis)) & 1) {  // lo neighbour -> cell 0 outputs (nt = 0)
+      float ah, ad;
+      split<MODE>(tr_lo_a[line], ah, ad);
+      const float bet = tr_lo_b[line];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int n = t2 + i;
+        acc.m[0][2 * rr + i] = fmaf(tab->urow[0][n], ah, acc.m[0][2 * rr + i]);
+        if constexpr (MODE == MODE_FP16_EC) {
+          acc.c[0][2 * rr + i] = fmaf(tab->urow[1][n], ah, acc.c[0][2 * rr + i]);
+          acc.c[0][2 * rr + i] = fmaf(tab->urow[0][n], ad, acc.c[0][2 * rr + i]);
+        }
+      }
+      if (t2 == 0) acc.m[0][2 * rr] += bet;
+    }
+    if ((T.nbm >> (2 * axis + 1)) & 1) {  // hi neighbour -> cell 1 outputs (nt = 1)
+      float ah, ad;
+      split<MODE>(tr_hi_a[line], ah, ad);
+      const float bet = tr_hi_b[line];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int n = t2 + i;
+        acc.m[1][2 * rr + i] = fmaf(tab->ucol[0][n], ah, acc.m[1][2 * rr + i]);
+        if constexpr (MODE == MODE_FP16_EC) {
+          acc.c[1][2 * rr + i] = fmaf(tab->ucol[1][n], ah, acc.c[1][2 * rr + i]);
+          acc.c[1][2 * rr + i] = fmaf(tab->ucol[0][n], ad, acc.c[1][2 * rr + i]);
+        }
+      }
+      if (t2 + 1 == K - 1) acc.m[1][2 * rr + 1] += bet;
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ const float* trp(const HTile<MODE>& T, int face, int plane) {
+  return T.tr + (face * 2 + plane) * (16 * 17);
+}
+
+// prologue + x/y stages; leaves c in U and dd in B (f16 tensors), trace planes ready
+template <int MODE>
+__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<K, MODE>& op,
+                                           const HTables* tab, const float* __restrict__ u) {
+  T.uh = reinterpret_cast<__half*>(smem);
+  T.bh = T.uh + TVOL;
+  T.tr = reinterpret_cast<float*>(smem + sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL);
+  if (MODE == MODE_FP16_EC) T.bh = T.uh + TVOL;  // layout: uh | bh | ud | bd
+  TileEngine<K, MODE, 1> e(smem, g);
+  e.tr = T.tr;
+  int cx, cy, cz;
+  if (!e.tile_cells(g, 0, cx, cy, cz)) return false;
+  T.cx = cx; T.cy = cy; T.cz = cz;
+  T.sy = e.sy; T.sz = e.sz;
+  T.nbm = 0;
+  const int c0[3] = {cx, cy, cz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (e.face_src(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
+    if (e.face_src(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
+    T.kind[a] = patch_kind(g, a, c0[a]);
+  }
+  T.lane = threadIdx.x & 31;
+  T.warp = threadIdx.x >> 5;
+  T.g = T.lane >> 2;
+  T.t = T.lane & 3;
+  // tile -> (h, d) tensors
+  const float* ub = u + (long long)(cz * K) * T.sz + (long long)(cy * K) * T.sy + cx * K;
+  for (int i = threadIdx.x; i < 1024; i += kThreads) {
+    const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
+    const float4 q4 = __ldg(reinterpret_cast<const float4*>(ub + z * T.sz + y * T.sy + x4));
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 0), q4.x);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 1), q4.y);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 2), q4.z);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 3), q4.w);
+  }
+  e.traces(g, op, u);
+  __syncthreads();
+  e.trace_masses(g, op);
+  __syncthreads();
+
+  int q, j;
+  lane_qj(T.lane, q, j);
+  BFrag<MODE> bm, bl;
+  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
+  // x and y stages on the warp's 4 z planes (in place)
+  for (int zz = 0; zz < 4; ++zz) {
+    const int z = 4 * T.warp + zz;
+    load_b<MODE>(bl, &tab->L[T.kind[0]][0][0][0][0], T.lane);
+    {
+      AFrag<MODE> a;
+      ld_a<MODE>(a, T.uh, T.ud(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), false);
+      Acc16<MODE> am, as;
+      am.zero();
+      as.zero();
+      mma16<MODE>(am, a, bm);
+      mma16<MODE>(as, a, bl);
+      halo16<MODE>(T, as, tab, 0, trp(T, 0, 0) + z * 17, trp(T, 0, 1) + z * 17, trp(T, 1, 0) + z * 17,
+                   trp(T, 1, 1) + z * 17);
+      float va[2][4], vb[2][4];
+      finals<MODE>(am, va);
+      finals<MODE>(as, vb);
+      __syncwarp();
+      st_acc<MODE>(T.uh, T.ud(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), va, false);
+      st_acc<MODE>(T.bh, T.bd(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), vb, false);
+    }
+    __syncwarp();
+    load_b<MODE>(bl, &tab->L[T.kind[1]][0][0][0][0], T.lane);
+    {
+      // y lines: rows = x, k = y (memory rows along y -> trans)
+      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
+      AFrag<MODE> a, b;
+      ld_a<MODE>(a, T.uh, T.ud(), off, true);
+      ld_a<MODE>(b, T.bh, T.bd(), off, true);
+      Acc16<MODE> c, d, e2;
+      c.zero();
+      d.zero();
+      e2.zero();
+      mma16<MODE>(c, a, bm);
+      mma16<MODE>(d, a, bl);
+      halo16<MODE>(T, d, tab, 1, trp(T, 2, 0) + z * 17, trp(T, 2, 1) + z * 17, trp(T, 3, 0) + z * 17,
+                   trp(T, 3, 1) + z * 17);
+      mma16<MODE>(e2, b, bm);
+      float vc[2][4], vd[2][4];
+      finals<MODE>(c, vc);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vd[nt][i] = d.val(nt, i) + e2.val(nt, i);
+      __syncwarp();
+      st_acc<MODE>(T.uh, T.ud(), off, vc, true);
+      st_acc<MODE>(T.bh, T.bd(), off, vd, true);
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// z stage for row y: v (16 lines x, 16 outputs z) as f32 values
+template <int MODE>
+__device__ __forceinline__ void z_lines(const HTile<MODE>& T, const HTables* tab, int y, const BFrag<MODE>& bm,
+                                        const BFrag<MODE>& bl, float (&v)[2][4]) {
+  int q, j;
+  lane_qj(T.lane, q, j);
+  const int off = hidx(j + 8 * (q >> 1), y, 8 * (q & 1));
+  AFrag<MODE> c, d;
+  ld_a<MODE>(c, T.uh, T.ud(), off, true);
+  ld_a<MODE>(d, T.bh, T.bd(), off, true);
+  Acc16<MODE> s, m;
+  s.zero();
+  m.zero();
+  mma16<MODE>(s, c, bl);
+  halo16<MODE>(T, s, tab, 2, trp(T, 4, 0) + y * 17, trp(T, 4, 1) + y * 17, trp(T, 5, 0) + y * 17,
+               trp(T, 5, 1) + y * 17);
+  mma16<MODE>(m, d, bm);
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[nt][i] = s.val(nt, i) + m.val(nt, i);
+}
+
+// accumulator element (nt, i): line = g + 8*(i>>1), output = 8nt + 2t + (i&1)
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restrict__ u, float* __restrict__ v, Geom g,
+                                                         LevelOp<K, MODE> op, const HTables* __restrict__ tab) {
+  extern __shared__ __align__(128) char smem[];
+  HTile<MODE> T;
+  u += (long long)blockIdx.y * g.batch_stride;
+  v += (long long)blockIdx.y * g.batch_stride;
+  if (!tile_front<MODE>(T, smem, g, op, tab, u)) return;
+  __syncthreads();
+  BFrag<MODE> bm, bl;
+  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
+  load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
+  float* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+    float o[2][4];
+    z_lines<MODE>(T, tab, y, bm, bl, o);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        vb[(long long)z * T.sz + (long long)y * T.sy + x] = o[nt][i];
+      }
+  }
+}
+
+// smoother colour pass (see sf_dmma.cu k_colour_dmma8 for the stage order)
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restrict__ xo, const float* __restrict__ b,
+                                                          float* __restrict__ xn, Geom g, LevelOp<K, MODE> op,
+                                                          const HTables* __restrict__ tab) {
+  extern __shared__ __align__(128) char smem[];
+  HTile<MODE> T;
+  if (!tile_front<MODE>(T, smem, g, op, tab, xo)) return;
+  __syncthreads();
+  const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
+  int q, j;
+  lane_qj(T.lane, q, j);
+  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  BFrag<MODE> bm, bl, bv;
+  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
+  load_b<MODE>(bl, &tab->L[kz][0][0][0][0], T.lane);
+  load_b<MODE>(bv, &tab->Vf[kz][0][0][0][0], T.lane);
+  // z lines: residual r = b - A x, forward V_z^T chained in registers; out (rows z') via stmatrix.trans
+  float keep[4][2][4];
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+    float o[2][4];
+    z_lines<MODE>(T, tab, y, bm, bl, o);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        o[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - o[nt][i];
+      }
+    AFrag<MODE> a;
+    acc_to_a<MODE>(o, a);
+    Acc16<MODE> acc;
+    acc.zero();
+    mma16<MODE>(acc, a, bv);
+    finals<MODE>(acc, keep[yy]);
+  }
+  __syncthreads();  // all z-stage reads of U/B done before U is overwritten
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+    st_acc<MODE>(T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), keep[yy], true);
+  }
+  __syncthreads();
+  // warp-private z' planes: V_y^T | V_x^T, 1/lambda, V_x | V_y
+  const double* lamx = tab->lam[kx];
+  const double* lamy = tab->lam[ky];
+  const double* lamz = tab->lam[kz];
+  for (int zz = 0; zz < 4; ++zz) {
+    const int z = 4 * T.warp + zz;
+    {
+      load_b<MODE>(bv, &tab->Vf[ky][0][0][0][0], T.lane);
+      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
+      AFrag<MODE> a;
+      ld_a<MODE>(a, T.uh, T.ud(), off, true);
+      Acc16<MODE> acc;
+      acc.zero();
+      mma16<MODE>(acc, a, bv);
+      float o[2][4];
+      finals<MODE>(acc, o);
+      __syncwarp();
+      st_acc<MODE>(T.uh, T.ud(), off, o, true);
+    }
+    __syncwarp();
+    {
+      load_b<MODE>(bv, &tab->Vf[kx][0][0][0][0], T.lane);
+      const int off = hidx(z, j + 8 * (q & 1), 8 * (q >> 1));
+      AFrag<MODE> a;
+      ld_a<MODE>(a, T.uh, T.ud(), off, false);
+      Acc16<MODE> acc;
+      acc.zero();
+      mma16<MODE>(acc, a, bv);
+      float o[2][4];
+      const double lz = 0.0 + __ldg(lamz + z);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int y = T.g + 8 * (i >> 1), x = 8 * nt + 2 * T.t + (i & 1);
+          o[nt][i] = acc.val(nt, i) / (float)((lz + __ldg(lamy + y)) + __ldg(lamx + x));
+        }
+      acc_to_a<MODE>(o, a);
+      load_b<MODE>(bv, &tab->Vb[kx][0][0][0][0], T.lane);
+      acc.zero();
+      mma16<MODE>(acc, a, bv);
+      finals<MODE>(acc, o);
+      __syncwarp();
+      st_acc<MODE>(T.uh, T.ud(), off, o, false);
+    }
+    __syncwarp();
+    {
+      load_b<MODE>(bv, &tab->Vb[ky][0][0][0][0], T.lane);
+      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
+      AFrag<MODE> a;
+      ld_a<MODE>(a, T.uh, T.ud(), off, true);
+      Acc16<MODE> acc;
+      acc.zero();
+      mma16<MODE>(acc, a, bv);
+      float o[2][4];
+      finals<MODE>(acc, o);
+      __syncwarp();
+      st_acc<MODE>(T.uh, T.ud(), off, o, true);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // z lines: backward V_z, x_new = x_old + correction
+  load_b<MODE>(bv, &tab->Vb[kz][0][0][0][0], T.lane);
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+    AFrag<MODE> a;
+    ld_a<MODE>(a, T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), true);
+    Acc16<MODE> acc;
+    acc.zero();
+    mma16<MODE>(acc, a, bv);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
+        xn[o] = __ldg(xo + o) + acc.val(nt, i);
+      }
+  }
+}
+
+// ------------------------------------------------------------- host side
+static void split_host(int mode, double x, unsigned short& h, unsigned short& d) {
+  const float x32 = (float)x;
+  const __half hh = __float2half_rn(x32);
+  h = *reinterpret_cast<const unsigned short*>(&hh);
+  const float hf = __half2float(hh);
+  const __half dd = __float2half_rn((x32 - hf) * kEc);
+  d = mode == MODE_FP16_EC ? *reinterpret_cast<const unsigned short*>(&dd) : 0;
+}
+
+static void pack_op_frags(int mode, const double* Op /* [16][16] */, unsigned* dst /* [2][2][2][32] */) {
+  for (int nt = 0; nt < 2; ++nt)
+    for (int jj = 0; jj < 2; ++jj)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int n = 8 * nt + (ln >> 2), k0 = 2 * (ln & 3) + 8 * jj;
+        unsigned short h0, d0, h1, d1;
+        split_host(mode, Op[n * 16 + k0], h0, d0);
+        split_host(mode, Op[n * 16 + k0 + 1], h1, d1);
+        dst[(0 * 4 + nt * 2 + jj) * 32 + ln] = (unsigned)h0 | ((unsigned)h1 << 16);
+        dst[(1 * 4 + nt * 2 + jj) * 32 + ln] = (unsigned)d0 | ((unsigned)d1 << 16);
+      }
+}
+
+static HTables build_tables(int mode, const double* opd, const double* eigd) {
+  HTables t;
+  std::memset(&t, 0, sizeof(t));
+  double Mp[256] = {0};
+  for (int c = 0; c < 2; ++c)
+    for (int i = 0; i < K; ++i)
+      for (int jj = 0; jj < K; ++jj) Mp[(c * K + i) * 16 + c * K + jj] = opd[i * K + jj];
+  pack_op_frags(mode, Mp, &t.M[0][0][0][0]);
+  double L[4][256];
+  build_patch_l_host(opd, &L[0][0]);
+  for (int q = 0; q < 4; ++q) pack_op_frags(mode, L[q], &t.L[q][0][0][0][0]);
+  if (eigd) {
+    for (int q = 0; q < 4; ++q) {
+      const double* V = eigd + q * 256;
+      double VT[256];
+      for (int i = 0; i < 16; ++i)
+        for (int jj = 0; jj < 16; ++jj) VT[i * 16 + jj] = V[jj * 16 + i];
+      pack_op_frags(mode, VT, &t.Vf[q][0][0][0][0]);
+      pack_op_frags(mode, V, &t.Vb[q][0][0][0][0]);
+      for (int i = 0; i < 16; ++i) t.lam[q][i] = eigd[4 * 256 + q * 16 + i];
+    }
+  }
+  const double* ucol = opd + 2 * K * K;
+  const double* urow = ucol + K;
+  for (int i = 0; i < K; ++i) {
+    unsigned short h, d;
+    split_host(mode, ucol[i], h, d);
+    t.ucol[0][i] = __half2float(*reinterpret_cast<__half*>(&h));
+    t.ucol[1][i] = __half2float(*reinterpret_cast<__half*>(&d));
+    split_host(mode, urow[i], h, d);
+    t.urow[0][i] = __half2float(*reinterpret_cast<__half*>(&h));
+    t.urow[1][i] = __half2float(*reinterpret_cast<__half*>(&d));
+  }
+  return t;
+}
+
+static std::mutex g_mu;
+struct Entry {
+  int dev, mode;
+  std::vector<double> key;
+  void* ptr;
+};
+static std::vector<Entry> g_cache;
+
+static const HTables* tables(int mode, const double* opd, const double* eigd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(opd, opd + 2 * K * K + 4 * K);
+  if (eigd) key.insert(key.end(), eigd, eigd + 4 * 256 + 4 * 16);
+  key.push_back(eigd ? 1.0 : 0.0);
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& e : g_cache)
+    if (e.dev == dev && e.mode == mode && e.key == key) return reinterpret_cast<const HTables*>(e.ptr);
+  HTables host = build_tables(mode, opd, eigd);
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(HTables)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(HTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_cache.push_back({dev, mode, std::move(key), d});
+  return reinterpret_cast<const HTables*>(d);
+}
+
+template <int MODE>
+static LevelOp<K, MODE> pack_op_h(const double* opd) {
+  LevelOp<K, MODE> op;
+  for (int i = 0; i < K; ++i)
+    for (int jj = 0; jj < K; ++jj) {
+      op.M[i][jj] = pack_me<MODE>(opd[i * K + jj]);
+      op.D[i][jj] = pack_me<MODE>(opd[K * K + i * K + jj]);
+    }
+  const double* vv = opd + 2 * K * K;
+  for (int i = 0; i < K; ++i) {
+    op.ucol[i] = pack_me<MODE>(vv[i]);
+    op.urow[i] = pack_me<MODE>(vv[K + i]);
+    op.bl[i] = pack_me<MODE>(vv[2 * K + i]);
+    op.br[i] = pack_me<MODE>(vv[3 * K + i]);
+  }
+  return op;
+}
+
+template <int MODE>
+static int vmult(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+  const HTables* tab = tables(MODE, opd, nullptr);
+  if (!tab) return -3;
+  auto op = pack_op_h<MODE>(opd);
+  if (cudaFuncSetAttribute(k_vmult_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
+      cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_vmult_h8<MODE><<<dim3(tiles, batch), kThreads, smem_bytes<MODE>(), st>>>((const float*)u, (float*)v, g, op, tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+template <int MODE>
+static int colour(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
+                  cudaStream_t st) {
+  const HTables* tab = tables(MODE, opd, eigd);
+  if (!tab) return -3;
+  auto op = pack_op_h<MODE>(opd);
+  if (cudaFuncSetAttribute(k_colour_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
+      cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_colour_h8<MODE><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)xo, (const float*)b, (float*)xn, g, op,
+                                                                 tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace hm
+
+int launch_vmult_hmma8(int mode, const Geom& g, const double* opd, const void* u, void* v, int batch,
+                       cudaStream_t st) {
+  return mode == MODE_FP16 ? hm::vmult<MODE_FP16>(g, opd, u, v, batch, st)
+                           : hm::vmult<MODE_FP16_EC>(g, opd, u, v, batch, st);
+}
+
+int launch_colour_hmma8(int mode, const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b,
+                        void* xn, cudaStream_t st) {
+  return mode == MODE_FP16 ? hm::colour<MODE_FP16>(g, opd, eigd, xo, b, xn, st)
+                           : hm::colour<MODE_FP16_EC>(g, opd, eigd, xo, b, xn, st);
+}
+
+}  // namespace sf

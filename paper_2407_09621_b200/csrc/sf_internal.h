@@ -2,12 +2,72 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cuda_fp16.h>
+
 #include "sf_common.cuh"
 
 namespace sf {
+
+// host: one matrix entry prepared under a mode (fp16: demoted; EC: (main, 2^11-scaled residual))
+template <int MODE>
+inline ME<MODE> pack_me(double x) {
+  ME<MODE> m;
+  if constexpr (MODE == MODE_FP64) {
+    m.h = x;
+  } else if constexpr (MODE == MODE_FP32) {
+    m.h = (float)x;
+  } else if constexpr (MODE == MODE_FP16) {
+    m.h = __half2float(__float2half_rn((float)x));
+  } else {
+    const float x32 = (float)x;
+    const float h = __half2float(__float2half_rn(x32));
+    m.h = h;
+    m.d = __half2float(__float2half_rn((x32 - h) * kEcScale));
+  }
+  return m;
+}
+
+// host: L_smooth[(lb,rb)] (16x16, Q7) = [[D + lb*Bl, U], [U^T, D + rb*Br]] from the cell-wise blocks
+inline void build_patch_l_host(const double* opd, double* L /* [4][16][16] */) {
+  constexpr int K = 8, B = 16;
+  const double* D = opd + K * K;
+  const double* ucol = opd + 2 * K * K;
+  const double* urow = ucol + K;
+  const double* bl = urow + K;
+  const double* br = bl + K;
+  for (int q = 0; q < 4; ++q) {
+    double* P = L + q * B * B;
+    const int lb = q >> 1, rb = q & 1;
+    for (int i = 0; i < B * B; ++i) P[i] = 0.0;
+    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < K; ++i)
+        for (int j = 0; j < K; ++j) P[(c * K + i) * B + c * K + j] = D[i * K + j];
+    for (int i = 0; i < K; ++i) {
+      P[i * B + K] = ucol[i];            // U column 0
+      P[(K - 1) * B + K + i] = urow[i];  // U row K-1
+      P[K * B + i] = ucol[i];            // U^T row 0
+      P[(K + i) * B + K - 1] = urow[i];  // U^T column K-1
+    }
+    if (lb)
+      for (int i = 0; i < K; ++i) {
+        P[i * B] += bl[i];
+        if (i > 0) P[i] += bl[i];
+      }
+    if (rb)
+      for (int i = 0; i < K; ++i) {
+        P[(K + i) * B + B - 1] += br[i];
+        if (i < K - 1) P[(B - 1) * B + K + i] += br[i];
+      }
+  }
+}
 // FP64 Q7 vmult on DMMA tensor cores (sf_dmma.cu); returns 0 or SF_ECUDA
 int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, void* v, int batch, cudaStream_t st);
 // FP64 Q7 smoother colour pass on DMMA (sf_dmma.cu)
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
+                        const void* b, void* x_new, cudaStream_t st);
+// FP16 / FP16-EC Q7 kernels on HMMA (sf_hmma.cu)
+int launch_vmult_hmma8(int mode, const Geom& g, const double* level_op, const void* u, void* v, int batch,
+                       cudaStream_t st);
+int launch_colour_hmma8(int mode, const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
                         const void* b, void* x_new, cudaStream_t st);
 }  // namespace sf

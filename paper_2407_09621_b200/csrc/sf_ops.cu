@@ -559,6 +559,12 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
       return SF_OK;
     }
   }
+  if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (!use_generic()) {
+      if (launch_vmult_hmma8(MODE, g, opd, u, v, batch, st)) return check_launch("sf_vmult (hmma)");
+      return SF_OK;
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   auto op = pack_op<K, MODE>(opd);
@@ -592,6 +598,12 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (!use_generic()) {
       if (launch_colour_dmma8(g, opd, eigd, xo, b, xn, st)) return check_launch("sf_smooth_colour (dmma)");
+      done = true;
+    }
+  }
+  if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (!use_generic()) {
+      if (launch_colour_hmma8(MODE, g, opd, eigd, xo, b, xn, st)) return check_launch("sf_smooth_colour (hmma)");
       done = true;
     }
   }

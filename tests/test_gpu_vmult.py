@@ -146,3 +146,15 @@ def test_tensor_core_path_matches_cuda_core_path(tmp_path):
         subprocess.run([sys.executable, "-c", code % (root, path)], check=True, env=env)
         outs.append(np.load(path))
     assert rel_l2(outs[0], outs[1]) <= 1e-14
+
+
+@pytest.mark.parametrize("lvl", [3, 4])
+@pytest.mark.parametrize("mode", [P.FP16, P.FP16_EC])
+def test_q7_half_precision_tensor_core_vmult_band(lvl, mode):
+    """HMMA fp16 / fp16-EC Q7 vmult: error vs fp64 within the reference's own error band."""
+    H = port.Hierarchy(lvl, 7)
+    u = np.random.default_rng(0).standard_normal(H.n_dofs(lvl))
+    ref64 = port.apply_operator(H, lvl, u, "fp64")
+    ref_err = rel_l2(port.apply_operator(H, lvl, u, mode.value), ref64)
+    err = rel_l2(sf.apply_operator(sf.build_hierarchy(lvl, 7), lvl, u, mode), ref64)
+    assert 0.25 * ref_err <= err <= 4.0 * ref_err, (err, ref_err)
