@@ -105,6 +105,20 @@ struct Acc<MODE_FP16_EC> {
 //   first/last cell : D + Bl / D + Br with Bl = (B_left - H_left)[:K,:K] (column/row 0),
 //                     Br = (B_right - H_right)[K:,K:] (column/row K-1)
 // ucol = U[:,0], urow = U[K-1,:], bl = Bl[:,0], br = Br[:,K-1].
+// Range management for the binary16 modes.  All factors are
+// powers of two, so scaling is exact and the demoted values equal 2^a times the
+// unscaled demoted values whenever those are normal binary16 numbers:
+//   matrices:  M^ = 2^aM M, L^ = 2^aL L (D, U, Nitsche blocks), V^ = 2^aV V  (static, per level)
+//   vectors :  u^ = 2^e u with a per-CTA block exponent e putting max|u^| in [2, 4)
+//   operator:  A^ = 2^aA A, aA = aL + 2 aM  ->  A u = 2^-(aA + e) (A^ u^)
+//   patch inverse: S^-1 r = 2^-(aD + 6 aV + e_r) V^(x3) (2^aD Lambda^-1) V^T(x3) r^
+// fp64/fp32 modes use all-zero exponents.
+struct Scales {
+  int aA;  // operator exponent
+  int aV;  // eigenvector exponent
+  int aD;  // division exponent: the kernels divide by (lambda_sum * 2^-aD)
+};
+
 template <int K, int MODE>
 struct LevelOp {
   ME<MODE> M[K][K];
@@ -113,7 +127,41 @@ struct LevelOp {
   ME<MODE> urow[K];
   ME<MODE> bl[K];
   ME<MODE> br[K];
+  Scales sc;
 };
+
+// 2^e as float / double (normal range only)
+__host__ __device__ __forceinline__ float pow2f(int e) {
+  union {
+    int i;
+    float f;
+  } u;
+  u.i = (e + 127) << 23;
+  return u.f;
+}
+__host__ __device__ __forceinline__ double pow2d(int e) {
+  union {
+    long long i;
+    double f;
+  } u;
+  u.i = (long long)(e + 1023) << 52;
+  return u.f;
+}
+// CTA-wide max of |x| over non-negative floats via integer atomics on a shared word
+__device__ __forceinline__ void smax(int* word, float v) {
+  v = fabsf(v);
+  if (v > 0.f) atomicMax(word, __float_as_int(v < 3.0e38f ? v : 3.0e38f));
+}
+// block exponent: e such that max|v| * 2^e lies in [2, 4) (0 for an all-zero or non-finite block)
+__device__ __forceinline__ int block_exp(float maxabs) {
+  if (!(maxabs > 0.f) || !(maxabs < 3.0e38f)) return 0;
+  const int ex = ((__float_as_int(maxabs) >> 23) & 0xff) - 127;  // maxabs in [2^ex, 2^ex+1)
+  int e = 1 - ex;
+  if (e > 100) e = 100;
+  if (e < -100) e = -100;
+  return e;
+}
+__device__ __forceinline__ int block_exp(double maxabs) { return block_exp((float)maxabs); }
 
 // Fast-diagonalisation tables for the vertex-patch smoother (multigrid.py:47-83):
 // V[kind] (2K x 2K, M-orthonormal eigenvectors of L_smooth[kind] vs M_patch) and the

@@ -182,6 +182,8 @@ struct HTile {
   __half* uh;  // tensor U (h) ; EC residual at uh + 2*TVOL
   __half* bh;  // tensor B (h) ; EC residual at bh + 2*TVOL
   float* tr;   // V1 trace planes (12 x 16 x 17 f32)
+  int* s_exp;  // block-exponent words ([0] input, [1] residual)
+  int eu;      // input block exponent: u^ = 2^eu u
   int cx, cy, cz;
   long long sy, sz;
   unsigned nbm;
@@ -193,7 +195,7 @@ struct HTile {
 
 template <int MODE>
 constexpr size_t smem_bytes() {
-  return sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL + sizeof(float) * 12 * 16 * 17;
+  return sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL + sizeof(float) * 12 * 16 * 17 + 16;
 }
 
 // store a value into (h, d) tensors at half index i
@@ -304,10 +306,14 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   T.bh = T.uh + TVOL;
   T.tr = reinterpret_cast<float*>(smem + sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL);
   if (MODE == MODE_FP16_EC) T.bh = T.uh + TVOL;  // layout: uh | bh | ud | bd
+  T.s_exp = reinterpret_cast<int*>(T.tr + 12 * 16 * 17);
   TileEngine<K, MODE, 1> e(smem, g);
   e.tr = T.tr;
+  e.s_exp = T.s_exp;
   int cx, cy, cz;
   if (!e.tile_cells(g, 0, cx, cy, cz)) return false;
+  if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
+  __syncthreads();
   T.cx = cx; T.cy = cy; T.cz = cz;
   T.sy = e.sy; T.sz = e.sz;
   T.nbm = 0;
@@ -322,15 +328,30 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   T.warp = threadIdx.x >> 5;
   T.g = T.lane >> 2;
   T.t = T.lane & 3;
-  // tile -> (h, d) tensors
+  // tile -> registers -> block exponent -> scaled (h, d) tensors
   const float* ub = u + (long long)(cz * K) * T.sz + (long long)(cy * K) * T.sy + cx * K;
-  for (int i = threadIdx.x; i < 1024; i += kThreads) {
+  float4 q4[1024 / kThreads];
+  float mx = 0.f;
+#pragma unroll
+  for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
+    const int i = threadIdx.x + k2 * kThreads;
     const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
-    const float4 q4 = __ldg(reinterpret_cast<const float4*>(ub + z * T.sz + y * T.sy + x4));
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 0), q4.x);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 1), q4.y);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 2), q4.z);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 3), q4.w);
+    q4[k2] = __ldg(reinterpret_cast<const float4*>(ub + z * T.sz + y * T.sy + x4));
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q4[k2].x), fabsf(q4[k2].y)), fmaxf(fabsf(q4[k2].z), fabsf(q4[k2].w))));
+  }
+  smax(&T.s_exp[0], mx);
+  __syncthreads();
+  T.eu = block_exp(__int_as_float(T.s_exp[0]));
+  e.eu = T.eu;
+  const float us = pow2f(T.eu);
+#pragma unroll
+  for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
+    const int i = threadIdx.x + k2 * kThreads;
+    const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 0), q4[k2].x * us);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 1), q4[k2].y * us);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 2), q4[k2].z * us);
+    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 3), q4[k2].w * us);
   }
   e.traces(g, op, u);
   __syncthreads();
@@ -431,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
   load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
   float* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  const float os = pow2f(-(op.sc.aA + T.eu));
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     float o[2][4];
@@ -440,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        vb[(long long)z * T.sz + (long long)y * T.sy + x] = o[nt][i];
+        vb[(long long)z * T.sz + (long long)y * T.sy + x] = o[nt][i] * os;
       }
   }
 }
@@ -462,32 +484,42 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   load_b<MODE>(bl, &tab->L[kz][0][0][0][0], T.lane);
   load_b<MODE>(bv, &tab->Vf[kz][0][0][0][0], T.lane);
-  // z lines: residual r = b - A x, forward V_z^T chained in registers; out (rows z') via stmatrix.trans
-  float keep[4][2][4];
+  // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
+  float rr[4][2][4];
+  const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    float o[2][4];
-    z_lines<MODE>(T, tab, y, bm, bl, o);
+    z_lines<MODE>(T, tab, y, bm, bl, rr[yy]);
+    float mx = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        o[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - o[nt][i];
+        rr[yy][nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - rr[yy][nt][i] * os;
+        mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
       }
-    AFrag<MODE> a;
-    acc_to_a<MODE>(o, a);
-    Acc16<MODE> acc;
-    acc.zero();
-    mma16<MODE>(acc, a, bv);
-    finals<MODE>(acc, keep[yy]);
+    smax(&T.s_exp[1], mx);
   }
-  __syncthreads();  // all z-stage reads of U/B done before U is overwritten
+  __syncthreads();  // all z-stage reads of U/B done, residual exponent complete
+  const int er = block_exp(__int_as_float(T.s_exp[1]));
+  const float rs = pow2f(er);
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    st_acc<MODE>(T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), keep[yy], true);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rr[yy][nt][i] *= rs;
+    AFrag<MODE> a;
+    acc_to_a<MODE>(rr[yy], a);
+    Acc16<MODE> acc;
+    acc.zero();
+    mma16<MODE>(acc, a, bv);
+    float o[2][4];
+    finals<MODE>(acc, o);
+    st_acc<MODE>(T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), o, true);
   }
   __syncthreads();
   // warp-private z' planes: V_y^T | V_x^T, 1/lambda, V_x | V_y
@@ -525,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int y = T.g + 8 * (i >> 1), x = 8 * nt + 2 * T.t + (i & 1);
-          o[nt][i] = acc.val(nt, i) / (float)((lz + __ldg(lamy + y)) + __ldg(lamx + x));
+          o[nt][i] = acc.val(nt, i) / (float)(((lz + __ldg(lamy + y)) + __ldg(lamx + x)) * pow2d(-op.sc.aD));
         }
       acc_to_a<MODE>(o, a);
       load_b<MODE>(bv, &tab->Vb[kx][0][0][0][0], T.lane);
@@ -552,8 +584,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
     __syncwarp();
   }
   __syncthreads();
-  // z lines: backward V_z, x_new = x_old + correction
+  // z lines: backward V_z, x_new = x_old + correction (back to true units)
   load_b<MODE>(bv, &tab->Vb[kz][0][0][0][0], T.lane);
+  const float cs = pow2f(-(op.sc.aD + 6 * op.sc.aV + er));
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     AFrag<MODE> a;
@@ -567,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
       for (int i = 0; i < 4; ++i) {
         const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
         const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
-        xn[o] = __ldg(xo + o) + acc.val(nt, i);
+        xn[o] = __ldg(xo + o) + acc.val(nt, i) * cs;
       }
   }
 }
@@ -648,7 +681,9 @@ static const HTables* tables(int mode, const double* opd, const double* eigd) {
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& e : g_cache)
     if (e.dev == dev && e.mode == mode && e.key == key) return reinterpret_cast<const HTables*>(e.ptr);
-  HTables host = build_tables(mode, opd, eigd);
+  double op_s[2 * K * K + 4 * K], eig_s[4 * 256 + 4 * 16];
+  level_scales(K, opd, eigd, op_s, eigd ? eig_s : nullptr);
+  HTables host = build_tables(mode, op_s, eigd ? eig_s : nullptr);
   void* d = nullptr;
   if (cudaMalloc(&d, sizeof(HTables)) != cudaSuccess) return nullptr;
   if (cudaMemcpy(d, &host, sizeof(HTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
@@ -657,8 +692,11 @@ static const HTables* tables(int mode, const double* opd, const double* eigd) {
 }
 
 template <int MODE>
-static LevelOp<K, MODE> pack_op_h(const double* opd) {
+static LevelOp<K, MODE> pack_op_h(const double* opd_raw, const double* eig_raw) {
+  Prepared<K, MODE> pr(opd_raw, eig_raw);
+  const double* opd = pr.opd;
   LevelOp<K, MODE> op;
+  op.sc = pr.sc;
   for (int i = 0; i < K; ++i)
     for (int jj = 0; jj < K; ++jj) {
       op.M[i][jj] = pack_me<MODE>(opd[i * K + jj]);
@@ -678,7 +716,7 @@ template <int MODE>
 static int vmult(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   const HTables* tab = tables(MODE, opd, nullptr);
   if (!tab) return -3;
-  auto op = pack_op_h<MODE>(opd);
+  auto op = pack_op_h<MODE>(opd, nullptr);
   if (cudaFuncSetAttribute(k_vmult_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
       cudaSuccess)
     return -3;
@@ -692,7 +730,7 @@ static int colour(const Geom& g, const double* opd, const double* eigd, const vo
                   cudaStream_t st) {
   const HTables* tab = tables(MODE, opd, eigd);
   if (!tab) return -3;
-  auto op = pack_op_h<MODE>(opd);
+  auto op = pack_op_h<MODE>(opd, eigd);
   if (cudaFuncSetAttribute(k_colour_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
       cudaSuccess)
     return -3;

@@ -4,6 +4,8 @@
 
 #include <cuda_fp16.h>
 
+#include <cmath>
+
 #include "sf_common.cuh"
 
 namespace sf {
@@ -26,6 +28,56 @@ inline ME<MODE> pack_me(double x) {
   }
   return m;
 }
+
+// host: static power-of-two range scales of one level for the binary16 modes
+// (sf_common.cuh).  Writes scaled copies of level_op (M by 2^aM,
+// the stiffness blocks by 2^aL) and of the eigenvector table (V by 2^aV).
+inline int ceil_log2(double x) {
+  int e;
+  const double m = std::frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
+  return m == 0.5 ? e - 1 : e;
+}
+inline Scales level_scales(int K, const double* opd, const double* eigd, double* op_out, double* eig_out) {
+  Scales sc{0, 0, 0};
+  if (opd) {
+    double mM = 0, mL = 0;
+    for (int i = 0; i < K * K; ++i) mM = std::fmax(mM, std::fabs(opd[i]));
+    for (int i = K * K; i < 2 * K * K + 4 * K; ++i) mL = std::fmax(mL, std::fabs(opd[i]));
+    const int aM = mM > 0 ? -ceil_log2(mM) : 0;     // max|M^| in (1/2, 1]
+    const int aL = mL > 0 ? 7 - ceil_log2(mL) : 0;  // max|L^| in (64, 128]
+    sc.aA = aL + 2 * aM;
+    for (int i = 0; i < K * K; ++i) op_out[i] = std::ldexp(opd[i], aM);
+    for (int i = K * K; i < 2 * K * K + 4 * K; ++i) op_out[i] = std::ldexp(opd[i], aL);
+  }
+  if (eigd) {
+    const int B = 2 * K;
+    double mV = 0, lmin = 1e300;
+    for (int i = 0; i < 4 * B * B; ++i) mV = std::fmax(mV, std::fabs(eigd[i]));
+    for (int i = 0; i < 4 * B; ++i) lmin = std::fmin(lmin, eigd[4 * B * B + i]);
+    sc.aV = 1 - ceil_log2(mV);          // max|V^| in (1, 2]
+    sc.aD = ceil_log2(3.0 * lmin) - 8;  // divided values <= 2^-7 of the forward transform
+    for (int i = 0; i < 4 * B * B; ++i) eig_out[i] = std::ldexp(eigd[i], sc.aV);
+    for (int i = 0; i < 4 * B; ++i) eig_out[4 * B * B + i] = eigd[4 * B * B + i];
+  }
+  return sc;
+}
+
+// host: the (possibly range-scaled) operator blocks a launch packs into kernel parameters
+template <int K, int MODE>
+struct Prepared {
+  double op[2 * K * K + 4 * K];
+  double eig[4 * 4 * K * K + 8 * K];
+  const double* opd;
+  const double* eigd;
+  Scales sc{0, 0, 0};
+  Prepared(const double* o, const double* e) : opd(o), eigd(e) {
+    if constexpr (MT<MODE>::kHalf) {
+      sc = level_scales(K, o, e, op, eig);
+      if (o) opd = op;
+      if (e) eigd = eig;
+    }
+  }
+};
 
 // host: L_smooth[(lb,rb)] (16x16, Q7) = [[D + lb*Bl, U], [U^T, D + rb*Br]] from the cell-wise blocks
 inline void build_patch_l_host(const double* opd, double* L /* [4][16][16] */) {

@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kThreads) k_vmult(const typename MT<MODE>::S* 
   v += (long long)blockIdx.y * g.batch_stride;
   E e(smem, g);
   e.apply_to_zstage(g, op, u);
+  const C os = e.out_scale(op);
   for (int i = threadIdx.x; i < TPC * E::B * E::B; i += blockDim.x) {
     int x = i % E::B;
     int y = (i / E::B) % E::B;
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_vmult(const typename MT<MODE>::S* 
     e.zline(g, op, t, y, x, cz, vv);
     typename E::S* out = v + (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + x);
 #pragma unroll
-    for (int z = 0; z < E::B; ++z) out[z * e.sz] = (typename E::S)vv[z];
+    for (int z = 0; z < E::B; ++z) out[z * e.sz] = (typename E::S)(vv[z] * os);
   }
 }
 
@@ -62,13 +63,31 @@ __device__ __forceinline__ void full_line(const ME<MODE>* A, const Op<MODE>* w, 
     for (int j = 0; j < B; ++j) acc[i].fma(TRANS ? A[j * B + i] : A[i * B + j], w[j]);
 }
 
+// divisor of the fast-diagonalisation step: (lambda sum) [* 2^-aD in binary16 modes]
+template <int MODE>
+__device__ __forceinline__ typename MT<MODE>::C lam_div(double lsum, const Scales& sc) {
+  if constexpr (MT<MODE>::kHalf) return (typename MT<MODE>::C)(lsum * pow2d(-sc.aD));
+  return (typename MT<MODE>::C)lsum;
+}
+// factor turning the scaled patch correction back into S^-1 r (binary16 modes)
+template <int MODE>
+__device__ __forceinline__ typename MT<MODE>::C corr_scale(const Scales& sc, int er) {
+  if constexpr (MT<MODE>::kHalf) return pow2f(-(sc.aD + 6 * sc.aV + er));
+  return typename MT<MODE>::C(1);
+}
+template <int MODE>
+__device__ __forceinline__ int read_exp(const int* word) {
+  if constexpr (MT<MODE>::kHalf) return block_exp(__int_as_float(*word));
+  return 0;
+}
 
 // --------------------------------------------------- smoother colour pass
 // One colour (tiling shift) of the multiplicative vertex-patch smoother,
 // multigrid.py:186-203: r = b - A x on each patch, x_new = x + P^-1 r with the
 // fast-diagonalisation inverse.  Reads x_old, writes x_new (ping-pong) so the
 // residual of every patch sees only pre-colour values, exactly as the
-// reference's full-vector residual does.
+// reference's full-vector residual does.  (TPC * B^2 <= blockDim: one line per
+// thread and stage.)
 template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S* __restrict__ xo,
                                                      const typename MT<MODE>::S* __restrict__ b,
@@ -78,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S*
   using E = TileEngine<K, MODE, TPC>;
   using C = typename E::C;
   using S = typename E::S;
-  constexpr int B = E::B, P = E::P;
+  constexpr int B = E::B, P = E::P, NL = TPC * B * B;
   extern __shared__ __align__(16) char smem[];
   E e(smem, g);
   ME<MODE>* sV = reinterpret_cast<ME<MODE>*>(smem + E::smem_bytes());
@@ -86,30 +105,41 @@ __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S*
   for (int i = threadIdx.x; i < 4 * B * B; i += blockDim.x) sV[i] = (&eig.V[0][0][0])[i];
   for (int i = threadIdx.x; i < 4 * B; i += blockDim.x) sLam[i] = (&eig.lam[0][0])[i];
   e.apply_to_zstage(g, op, xo);
-
-  // z lines: residual, forward V_z^T
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int x = i % B, y = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
-    C vv[B];
-    e.zline(g, op, t, y, x, cz, vv);
-    const S* bp = b + (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + x);
-    Op<MODE> w[B];
+  const int i = threadIdx.x;
+  int cx = 0, cy = 0, cz = 0;
+  const bool act = i < NL && e.tile_cells(g, i / (B * B), cx, cy, cz);
+  const int t = i / (B * B);
+  {  // z lines: residual (true units), block exponent, forward V_z^T
+    const int x = i % B, y = (i / B) % B;
+    C r[B];
+    if (act) {
+      C vv[B];
+      e.zline(g, op, t, y, x, cz, vv);
+      const C os = e.out_scale(op);
+      const S* bp = b + (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + x);
 #pragma unroll
-    for (int z = 0; z < B; ++z) w[z] = prep<MODE>((C)bp[z * e.sz] - vv[z]);
-    Acc<MODE> acc[B];
-    full_line<B, MODE, true>(sV + patch_kind(g, 2, cz) * B * B, w, acc);
-    C* col = e.su + t * E::VOL + E::idx(0, y, x);
+      for (int z = 0; z < B; ++z) {
+        r[z] = (C)bp[z * e.sz] - vv[z] * os;
+        if constexpr (E::kHalf) smax(&e.s_exp[1], (float)r[z]);
+      }
+    }
+    __syncthreads();
+    const C rs = E::kHalf ? (C)pow2f(read_exp<MODE>(&e.s_exp[1])) : C(1);
+    if (act) {
+      Op<MODE> w[B];
 #pragma unroll
-    for (int z = 0; z < B; ++z) col[z * B * P] = acc[z].result();
+      for (int z = 0; z < B; ++z) w[z] = prep<MODE>(r[z] * rs);
+      Acc<MODE> acc[B];
+      full_line<B, MODE, true>(sV + patch_kind(g, 2, cz) * B * B, w, acc);
+      C* col = e.su + t * E::VOL + E::idx(0, y, x);
+#pragma unroll
+      for (int z = 0; z < B; ++z) col[z * B * P] = acc[z].result();
+    }
   }
   __syncthreads();
-  // y lines: forward V_y^T
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int x = i % B, z = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
+  const int er = read_exp<MODE>(&e.s_exp[1]);
+  if (act) {  // y lines: forward V_y^T
+    const int x = i % B, z = (i / B) % B;
     C* col = e.su + t * E::VOL + E::idx(z, 0, x);
     Op<MODE> w[B];
 #pragma unroll
@@ -120,32 +150,26 @@ __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S*
     for (int y = 0; y < B; ++y) col[y * P] = acc[y].result();
   }
   __syncthreads();
-  // x lines: forward V_x^T, divide by eigenvalue sums, backward V_x
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int y = i % B, z = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
-    int kx = patch_kind(g, 0, cx), ky = patch_kind(g, 1, cy), kz = patch_kind(g, 2, cz);
+  if (act) {  // x lines: forward V_x^T, divide by eigenvalue sums, backward V_x
+    const int y = i % B, z = (i / B) % B;
+    const int kx = patch_kind(g, 0, cx), ky = patch_kind(g, 1, cy), kz = patch_kind(g, 2, cz);
     C* row = e.su + t * E::VOL + E::idx(z, y, 0);
     Op<MODE> w[B];
 #pragma unroll
     for (int x = 0; x < B; ++x) w[x] = prep<MODE>(row[x]);
     Acc<MODE> acc[B];
     full_line<B, MODE, true>(sV + kx * B * B, w, acc);
-    double lzy = (0.0 + sLam[kz * B + z]) + sLam[ky * B + y];
+    const double lzy = (0.0 + sLam[kz * B + z]) + sLam[ky * B + y];
 #pragma unroll
-    for (int x = 0; x < B; ++x) w[x] = prep<MODE>(acc[x].result() / (C)(lzy + sLam[kx * B + x]));
+    for (int x = 0; x < B; ++x) w[x] = prep<MODE>(acc[x].result() / lam_div<MODE>(lzy + sLam[kx * B + x], op.sc));
     Acc<MODE> acc2[B];
     full_line<B, MODE, false>(sV + kx * B * B, w, acc2);
 #pragma unroll
     for (int x = 0; x < B; ++x) row[x] = acc2[x].result();
   }
   __syncthreads();
-  // y lines: backward V_y
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int x = i % B, z = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
+  if (act) {  // y lines: backward V_y
+    const int x = i % B, z = (i / B) % B;
     C* col = e.su + t * E::VOL + E::idx(z, 0, x);
     Op<MODE> w[B];
 #pragma unroll
@@ -156,20 +180,18 @@ __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S*
     for (int y = 0; y < B; ++y) col[y * P] = acc[y].result();
   }
   __syncthreads();
-  // z lines: backward V_z, x_new = x_old + correction
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int x = i % B, y = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
+  if (act) {  // z lines: backward V_z, x_new = x_old + correction
+    const int x = i % B, y = (i / B) % B;
     const C* col = e.su + t * E::VOL + E::idx(0, y, x);
     Op<MODE> w[B];
 #pragma unroll
     for (int z = 0; z < B; ++z) w[z] = prep<MODE>(col[z * B * P]);
     Acc<MODE> acc[B];
     full_line<B, MODE, false>(sV + patch_kind(g, 2, cz) * B * B, w, acc);
+    const C cs = corr_scale<MODE>(op.sc, er);
     long long off = (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + x);
 #pragma unroll
-    for (int z = 0; z < B; ++z) xn[off + z * e.sz] = (S)((C)xo[off + z * e.sz] + acc[z].result());
+    for (int z = 0; z < B; ++z) xn[off + z * e.sz] = (S)((C)xo[off + z * e.sz] + acc[z].result() * cs);
   }
 }
 
@@ -211,38 +233,58 @@ __global__ void __launch_bounds__(kThreads) k_resid_restrict(const typename MT<M
   using E = TileEngine<K, MODE, TPC>;
   using C = typename E::C;
   using S = typename E::S;
-  constexpr int B = E::B, P = E::P;
+  constexpr int B = E::B, P = E::P, NL = TPC * B * B;
   extern __shared__ __align__(16) char smem[];
   E e(smem, g);
-  if (with_op) e.apply_to_zstage(g, op, x);
+  if (with_op) {
+    e.apply_to_zstage(g, op, x);
+  } else {
+    e.init_exp();
+    __syncthreads();
+  }
   long long syc = (long long)(g.nx / 2) * K, szc = syc * (long long)(g.ny / 2) * K;
-  // z lines: residual, restrict along z (B -> K)
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int xx = i % B, y = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
-    C vv[B];
-    if (with_op) e.zline(g, op, t, y, xx, cz, vv);
-    const S* bp = b + (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + xx);
-    Op<MODE> w[B];
+  const int i = threadIdx.x;
+  int cx = 0, cy = 0, cz = 0;
+  const bool act = i < NL && e.tile_cells(g, i / (B * B), cx, cy, cz);
+  const int t = i / (B * B);
+  {  // z lines: residual, block exponent, restrict along z (B -> K)
+    const int xx = i % B, y = (i / B) % B;
+    C r[B];
+    if (act) {
+      C vv[B];
+      if (with_op) e.zline(g, op, t, y, xx, cz, vv);
+      const C os = e.out_scale(op);
+      const S* bp = b + (long long)(cz * K) * e.sz + (long long)(cy * K + y) * e.sy + (cx * K + xx);
 #pragma unroll
-    for (int z = 0; z < B; ++z) w[z] = prep<MODE>(with_op ? (C)bp[z * e.sz] - vv[z] : (C)bp[z * e.sz]);
-    C* col = e.sb + t * E::VOL + E::idx(0, y, xx);
+      for (int z = 0; z < B; ++z) {
+        r[z] = with_op ? (C)bp[z * e.sz] - vv[z] * os : (C)bp[z * e.sz];
+        if constexpr (E::kHalf) smax(&e.s_exp[1], (float)r[z]);
+      }
+    }
+    __syncthreads();
+    const C rs = E::kHalf ? (C)pow2f(read_exp<MODE>(&e.s_exp[1])) : C(1);
+    if (act) {
+      Op<MODE> w[B];
 #pragma unroll
-    for (int kc = 0; kc < K; ++kc) {
-      Acc<MODE> a;
+      for (int z = 0; z < B; ++z) w[z] = prep<MODE>(r[z] * rs);
+      C* col = e.sb + t * E::VOL + E::idx(0, y, xx);
 #pragma unroll
-      for (int j = 0; j < B; ++j) a.fma(emb.P[j][kc], w[j]);
-      col[kc * B * P] = a.result();
+      for (int kc = 0; kc < K; ++kc) {
+        Acc<MODE> a;
+#pragma unroll
+        for (int j = 0; j < B; ++j) a.fma(emb.P[j][kc], w[j]);
+        col[kc * B * P] = a.result();
+      }
     }
   }
   __syncthreads();
+  const C back = E::kHalf ? (C)pow2f(-read_exp<MODE>(&e.s_exp[1])) : C(1);
   // y lines: (zc < K, x < B)
-  for (int i = threadIdx.x; i < TPC * K * B; i += blockDim.x) {
-    int xx = i % B, zc = (i / B) % K, t = i / (K * B);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
-    C* col = e.sb + t * E::VOL + E::idx(zc, 0, xx);
+  for (int j2 = threadIdx.x; j2 < TPC * K * B; j2 += blockDim.x) {
+    int xx = j2 % B, zc = (j2 / B) % K, tt = j2 / (K * B);
+    int ax, ay, az;
+    if (!e.tile_cells(g, tt, ax, ay, az)) continue;
+    C* col = e.sb + tt * E::VOL + E::idx(zc, 0, xx);
     Op<MODE> w[B];
 #pragma unroll
     for (int y = 0; y < B; ++y) w[y] = prep<MODE>(col[y * P]);
@@ -259,21 +301,21 @@ __global__ void __launch_bounds__(kThreads) k_resid_restrict(const typename MT<M
   }
   __syncthreads();
   // x lines: (zc, yc) -> K coarse values
-  for (int i = threadIdx.x; i < TPC * K * K; i += blockDim.x) {
-    int yc = i % K, zc = (i / K) % K, t = i / (K * K);
-    int cx, cy, cz;
-    if (!e.tile_cells(g, t, cx, cy, cz)) continue;
-    const C* row = e.sb + t * E::VOL + E::idx(zc, yc, 0);
+  for (int j2 = threadIdx.x; j2 < TPC * K * K; j2 += blockDim.x) {
+    int yc = j2 % K, zc = (j2 / K) % K, tt = j2 / (K * K);
+    int ax, ay, az;
+    if (!e.tile_cells(g, tt, ax, ay, az)) continue;
+    const C* row = e.sb + tt * E::VOL + E::idx(zc, yc, 0);
     Op<MODE> w[B];
 #pragma unroll
     for (int xx = 0; xx < B; ++xx) w[xx] = prep<MODE>(row[xx]);
-    S* out = coarse + (long long)((cz / 2) * K + zc) * szc + (long long)((cy / 2) * K + yc) * syc + (cx / 2) * K;
+    S* out = coarse + (long long)((az / 2) * K + zc) * szc + (long long)((ay / 2) * K + yc) * syc + (ax / 2) * K;
 #pragma unroll
     for (int kc = 0; kc < K; ++kc) {
       Acc<MODE> a;
 #pragma unroll
       for (int j = 0; j < B; ++j) a.fma(emb.P[j][kc], w[j]);
-      out[kc] = (S)a.result();
+      out[kc] = (S)(a.result() * back);
     }
   }
 }
@@ -286,10 +328,12 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
                                                           int ncz, Embed<K, MODE> emb) {
   constexpr int TPC = Tpc<K>::value;
   constexpr int B = 2 * K, P = B + 1, VOL = B * B * P;
+  constexpr bool kHalf = MT<MODE>::kHalf;
   using C = typename MT<MODE>::C;
   using S = typename MT<MODE>::S;
   extern __shared__ __align__(16) char smem[];
   C* s = reinterpret_cast<C*>(smem);
+  int* s_exp = reinterpret_cast<int*>(s + TPC * VOL);
   long long syc = (long long)ncx * K, szc = syc * (long long)ncy * K;
   long long syf = 2 * syc, szf = syf * 2LL * ncy * K;
   int ncell = ncx * ncy * ncz;
@@ -299,16 +343,30 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
     x = id % ncx; y = (id / ncx) % ncy; z = id / (ncx * ncy);
     return true;
   };
-  // x lines straight from global: (t, zc, yc) -> B values along fine x
-  for (int i = threadIdx.x; i < TPC * K * K; i += blockDim.x) {
-    int yc = i % K, zc = (i / K) % K, t = i / (K * K);
-    int cx, cy, cz;
-    if (!cell(t, cx, cy, cz)) continue;
-    const S* in = ec + (long long)(cz * K + zc) * szc + (long long)(cy * K + yc) * syc + cx * K;
+  if (threadIdx.x == 0) s_exp[0] = 0;
+  __syncthreads();
+  // x lines straight from global: (t, zc, yc) -> B values along fine x (one line per thread)
+  const int i = threadIdx.x;
+  const int yc = i % K, zc = (i / K) % K, t0 = i / (K * K);
+  int cx = 0, cy = 0, cz = 0;
+  const bool act = i < TPC * K * K && cell(t0, cx, cy, cz);
+  C in[K];
+  if (act) {
+    const S* src = ec + (long long)(cz * K + zc) * szc + (long long)(cy * K + yc) * syc + cx * K;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      in[j] = (C)src[j];
+      if constexpr (kHalf) smax(&s_exp[0], (float)in[j]);
+    }
+  }
+  __syncthreads();
+  const int ee = kHalf ? block_exp(__int_as_float(s_exp[0])) : 0;
+  if (act) {
+    const C sc = kHalf ? (C)pow2f(ee) : C(1);
     Op<MODE> w[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) w[j] = prep<MODE>((C)in[j]);
-    C* row = s + t * VOL + (zc * B + yc) * P;
+    for (int j = 0; j < K; ++j) w[j] = prep<MODE>(in[j] * sc);
+    C* row = s + t0 * VOL + (zc * B + yc) * P;
 #pragma unroll
     for (int o = 0; o < B; ++o) {
       Acc<MODE> a;
@@ -319,11 +377,11 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
   }
   __syncthreads();
   // y lines: (t, zc, x) K -> B
-  for (int i = threadIdx.x; i < TPC * K * B; i += blockDim.x) {
-    int xf = i % B, zc = (i / B) % K, t = i / (K * B);
-    int cx, cy, cz;
-    if (!cell(t, cx, cy, cz)) continue;
-    C* col = s + t * VOL + (zc * B) * P + xf;
+  for (int j2 = threadIdx.x; j2 < TPC * K * B; j2 += blockDim.x) {
+    int xf = j2 % B, zz = (j2 / B) % K, t = j2 / (K * B);
+    int ax, ay, az;
+    if (!cell(t, ax, ay, az)) continue;
+    C* col = s + t * VOL + (zz * B) * P + xf;
     Op<MODE> w[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) w[j] = prep<MODE>(col[j * P]);
@@ -336,26 +394,26 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
     }
   }
   __syncthreads();
+  const C back = kHalf ? (C)pow2f(-ee) : C(1);
   // z lines: (t, y, x) K -> B, added into the fine vector
-  for (int i = threadIdx.x; i < TPC * B * B; i += blockDim.x) {
-    int xf = i % B, yf = (i / B) % B, t = i / (B * B);
-    int cx, cy, cz;
-    if (!cell(t, cx, cy, cz)) continue;
+  for (int j2 = threadIdx.x; j2 < TPC * B * B; j2 += blockDim.x) {
+    int xf = j2 % B, yf = (j2 / B) % B, t = j2 / (B * B);
+    int ax, ay, az;
+    if (!cell(t, ax, ay, az)) continue;
     const C* col = s + t * VOL + yf * P + xf;
     Op<MODE> w[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) w[j] = prep<MODE>(col[j * B * P]);
-    S* out = fine + (long long)(2 * cz * K) * szf + (long long)(2 * cy * K + yf) * syf + (2 * cx * K + xf);
+    S* out = fine + (long long)(2 * az * K) * szf + (long long)(2 * ay * K + yf) * syf + (2 * ax * K + xf);
 #pragma unroll
     for (int o = 0; o < B; ++o) {
       Acc<MODE> a;
 #pragma unroll
       for (int j = 0; j < K; ++j) a.fma(emb.P[o][j], w[j]);
-      out[o * szf] = (S)((C)out[o * szf] + a.result());
+      out[o * szf] = (S)((C)out[o * szf] + a.result() * back);
     }
   }
 }
-
 
 // ------------------------------------------- standalone patch inverse (batch)
 // out = (V_z (x) V_y (x) V_x) diag(1/(lam_z+lam_y+lam_x)) (V_z^T (x) V_y^T (x) V_x^T) in
@@ -364,20 +422,28 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
 template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads) k_patch_apply(const typename MT<MODE>::S* __restrict__ in,
                                                           typename MT<MODE>::S* __restrict__ out, int count, int kx,
-                                                          int ky, int kz, PatchEig<K, MODE> eig) {
+                                                          int ky, int kz, PatchEig<K, MODE> eig, Scales sc) {
   constexpr int TPC = Tpc<K>::value;
   constexpr int B = 2 * K, P = B + 1, VOL = B * B * P;
+  constexpr bool kHalf = MT<MODE>::kHalf;
   using C = typename MT<MODE>::C;
   using S = typename MT<MODE>::S;
   extern __shared__ __align__(16) char smem[];
   C* s = reinterpret_cast<C*>(smem);
+  int* s_exp = reinterpret_cast<int*>(s + TPC * VOL);
   const long long pvol = (long long)B * B * B;
+  if (threadIdx.x == 0) s_exp[0] = 0;
+  __syncthreads();
   for (int i = threadIdx.x; i < TPC * B * B * B; i += blockDim.x) {
     int t = i / (B * B * B), r = i % (B * B * B);
     int id = blockIdx.x * TPC + t;
-    s[t * VOL + (r / B) * P + r % B] = id < count ? (C)in[id * pvol + r] : C(0);
+    const C v = id < count ? (C)in[id * pvol + r] : C(0);
+    s[t * VOL + (r / B) * P + r % B] = v;
+    if constexpr (kHalf) smax(&s_exp[0], (float)v);
   }
   __syncthreads();
+  const int ee = kHalf ? block_exp(__int_as_float(s_exp[0])) : 0;
+  const C s_in = kHalf ? (C)pow2f(ee) : C(1);
   const ME<MODE>* Vx = &eig.V[kx][0][0];
   const ME<MODE>* Vy = &eig.V[ky][0][0];
   const ME<MODE>* Vz = &eig.V[kz][0][0];
@@ -388,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) k_patch_apply(const typename MT<MODE
       C* row = s + t * VOL + (z * B + y) * P;
       Op<MODE> w[B];
 #pragma unroll
-      for (int x = 0; x < B; ++x) w[x] = prep<MODE>(row[x]);
+      for (int x = 0; x < B; ++x) w[x] = prep<MODE>(pass == 0 ? row[x] * s_in : row[x]);
       Acc<MODE> acc[B];
       if (pass == 0) full_line<B, MODE, true>(Vx, w, acc); else full_line<B, MODE, false>(Vx, w, acc);
 #pragma unroll
@@ -419,7 +485,8 @@ __global__ void __launch_bounds__(kThreads) k_patch_apply(const typename MT<MODE
         // lambda_sum over block axes (z, y, x) in fp64, cast, then divide (multigrid.py:60-69, 79-80)
 #pragma unroll
         for (int z = 0; z < B; ++z)
-          col[z * B * P] = acc[z].result() / (C)(((0.0 + eig.lam[kz][z]) + eig.lam[ky][y]) + eig.lam[kx][x]);
+          col[z * B * P] =
+              acc[z].result() / lam_div<MODE>(((0.0 + eig.lam[kz][z]) + eig.lam[ky][y]) + eig.lam[kx][x], sc);
       } else {
 #pragma unroll
         for (int z = 0; z < B; ++z) col[z * B * P] = acc[z].result();
@@ -427,10 +494,11 @@ __global__ void __launch_bounds__(kThreads) k_patch_apply(const typename MT<MODE
     }
     __syncthreads();
   }
+  const C cs = corr_scale<MODE>(sc, ee);
   for (int i = threadIdx.x; i < TPC * B * B * B; i += blockDim.x) {
     int t = i / (B * B * B), r = i % (B * B * B);
     int id = blockIdx.x * TPC + t;
-    if (id < count) out[id * pvol + r] = (S)s[t * VOL + (r / B) * P + r % B];
+    if (id < count) out[id * pvol + r] = (S)(s[t * VOL + (r / B) * P + r % B] * cs);
   }
 }
 
@@ -567,7 +635,9 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
   }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
-  auto op = pack_op<K, MODE>(opd);
+  Prepared<K, MODE> pr(opd, nullptr);
+  auto op = pack_op<K, MODE>(pr.opd);
+  op.sc = pr.sc;
   size_t smem = E::smem_bytes();
   if ((rc = set_smem(k_vmult<K, MODE>, smem))) return rc;
   int tiles = g.ntx * g.nty * g.ntz;
@@ -608,8 +678,10 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
     }
   }
   if (!done) {
-    auto op = pack_op<K, MODE>(opd);
-    auto eig = pack_eig<K, MODE>(eigd);
+    Prepared<K, MODE> pr(opd, eigd);
+    auto op = pack_op<K, MODE>(pr.opd);
+    op.sc = pr.sc;
+    auto eig = pack_eig<K, MODE>(pr.eigd);
     size_t smem = E::smem_bytes() + sizeof(ME<MODE>) * 4 * 4 * K * K + sizeof(double) * 8 * K;
     if ((rc = set_smem(k_colour<K, MODE>, smem))) return rc;
     int tiles = g.ntx * g.nty * g.ntz;
@@ -637,7 +709,9 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   using S = typename MT<MODE>::S;
-  auto op = pack_op<K, MODE>(opd);
+  Prepared<K, MODE> pr(opd, nullptr);
+  auto op = pack_op<K, MODE>(pr.opd);
+  op.sc = pr.sc;
   auto emb = pack_emb<K, MODE>(embd);
   size_t smem = E::smem_bytes();
   if ((rc = set_smem(k_resid_restrict<K, MODE>, smem))) return rc;
@@ -655,7 +729,7 @@ static int launch_prolong_add(const sf_grid* coarse, const double* embd, const v
   using S = typename MT<MODE>::S;
   using C = typename MT<MODE>::C;
   auto emb = pack_emb<K, MODE>(embd);
-  size_t smem = sizeof(C) * TPC * B * B * (B + 1);
+  size_t smem = sizeof(C) * TPC * B * B * (B + 1) + 16;
   int rc;
   if ((rc = set_smem(k_prolong_add<K, MODE>, smem))) return rc;
   int cells = coarse->nx * coarse->ny * coarse->nz;
@@ -671,12 +745,13 @@ static int launch_patch_apply(int count, const int* kinds, const double* eigd, c
   constexpr int B = 2 * K;
   using S = typename MT<MODE>::S;
   using C = typename MT<MODE>::C;
-  auto eig = pack_eig<K, MODE>(eigd);
-  size_t smem = sizeof(C) * TPC * B * B * (B + 1);
+  Prepared<K, MODE> pr(nullptr, eigd);
+  auto eig = pack_eig<K, MODE>(pr.eigd);
+  size_t smem = sizeof(C) * TPC * B * B * (B + 1) + 16;
   int rc;
   if ((rc = set_smem(k_patch_apply<K, MODE>, smem))) return rc;
   k_patch_apply<K, MODE><<<(count + TPC - 1) / TPC, kThreads, smem, st>>>((const S*)in, (S*)out, count, kinds[0],
-                                                                            kinds[1], kinds[2], eig);
+                                                                            kinds[1], kinds[2], eig, pr.sc);
   return check_launch("sf_patch_apply");
 }
 

@@ -104,11 +104,14 @@ struct TileEngine {
   using C = typename MT<MODE>::C;
   using S = typename MT<MODE>::S;
 
-  static constexpr size_t smem_bytes() { return sizeof(C) * TPC * (2 * VOL + 12 * PL); }
+  static constexpr size_t smem_bytes() { return sizeof(C) * TPC * (2 * VOL + 12 * PL) + 16; }
+  static constexpr bool kHalf = MT<MODE>::kHalf;
 
   C* su;  // [TPC][VOL]
   C* sb;  // [TPC][VOL]
   C* tr;  // [TPC][6][2][PL]
+  int* s_exp;  // [0]: max|u| bits, [1]: max|r| bits (binary16 block exponents)
+  int eu = 0;  // block exponent of the input tile (binary16 modes), u^ = 2^eu u
   int ntiles_total;
   int tile0;
   long long sy, sz;
@@ -117,6 +120,7 @@ struct TileEngine {
     su = reinterpret_cast<C*>(smem);
     sb = su + TPC * VOL;
     tr = sb + TPC * VOL;
+    s_exp = reinterpret_cast<int*>(tr + TPC * 12 * PL);
     ntiles_total = g.ntx * g.nty * g.ntz;
     tile0 = blockIdx.x * TPC;
     sy = (long long)g.nx * K;
@@ -162,7 +166,17 @@ struct TileEngine {
       if (tile_cells(g, t, cx, cy, cz))
         val = (C)u[(long long)(cz * K + z) * sz + (long long)(cy * K + y) * sy + (cx * K + x)];
       su[t * VOL + idx(z, y, x)] = val;
+      if constexpr (kHalf) smax(&s_exp[0], (float)val);
     }
+  }
+
+  __device__ __forceinline__ void init_exp() {
+    if (threadIdx.x == 0) s_exp[0] = s_exp[1] = 0;
+  }
+  // input scale 2^eu (binary16 modes: max |u^| in [2, 4))
+  __device__ __forceinline__ C uscale() const {
+    if constexpr (kHalf) return pow2f(eu);
+    return C(1);
   }
 
   // ---------------------------------------------------------------- stage 1
@@ -193,8 +207,9 @@ struct TileEngine {
         base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
       }
       C w[K];
+      const C us = uscale();
 #pragma unroll
-      for (int j = 0; j < K; ++j) w[j] = (C)base[j * step];
+      for (int j = 0; j < K; ++j) w[j] = (C)base[j * step] * us;
       Acc<MODE> beta;
       C alpha;
       if (hi) {  // neighbour above: alpha = w[0], beta = sum_{j>=1} urow[j] w[j]
@@ -275,8 +290,9 @@ struct TileEngine {
       if (!tile_cells(g, t, cx, cy, cz)) continue;
       C* row = su + t * VOL + idx(z, y, 0);
       Op<MODE> w[B];
+      const C us = uscale();
 #pragma unroll
-      for (int x = 0; x < B; ++x) w[x] = prep<MODE>(row[x]);
+      for (int x = 0; x < B; ++x) w[x] = prep<MODE>(row[x] * us);
       bool lb, hb;
       Op<MODE> al, ah;
       C bl_, bh_;
@@ -351,9 +367,21 @@ struct TileEngine {
     for (int z = 0; z < B; ++z) v[z] = s[z].result() + m[z].result();
   }
 
+  // factor turning zline() output (scaled units) into A u
+  __device__ __forceinline__ C out_scale(const LevelOp<K, MODE>& op) const {
+    if constexpr (kHalf) return pow2f(-(op.sc.aA + eu));
+    return C(1);
+  }
+
   // full A u on the tile up to (and excluding) stage 4; caller runs zline per thread
   __device__ __forceinline__ void apply_to_zstage(const Geom& g, const LevelOp<K, MODE>& op, const S* __restrict__ u) {
+    init_exp();
+    __syncthreads();
     load(g, u);
+    if constexpr (kHalf) {
+      __syncthreads();
+      eu = block_exp(__int_as_float(s_exp[0]));
+    }
     traces(g, op, u);
     __syncthreads();
     trace_masses(g, op);

@@ -111,3 +111,22 @@ def test_solve_matches_reference(gold, k, lvl, mode):
         assert abs(out.l2 - ref_l2) <= 0.02 * ref_l2, (out.l2, ref_l2)
     else:
         assert out.l2 <= 1.5 * max(ref_l2, ref64_l2), (out.l2, ref_l2, ref64_l2)
+
+
+def test_device_rhs_and_l2_error_match_host():
+    import math
+
+    import torch
+
+    from paper_2407_09621_b200.discretization import assemble_rhs_separable, l2_error_separable
+
+    hier = sf.build_hierarchy(3, 3)
+    prob = sf.sine_product_problem(3)
+    sine = lambda x: np.sin(np.pi * x)
+    b_dev = assemble_rhs_separable(hier, 3, sine, 3.0 * math.pi**2)
+    b_host = sf.assemble_rhs(hier, 3, prob.rhs)
+    assert np.linalg.norm(b_dev.cpu().numpy() - b_host) <= 1e-13 * np.linalg.norm(b_host)
+    u = torch.randn(hier.n_dofs(3), dtype=torch.float64, device="cuda")
+    e_dev = l2_error_separable(hier, 3, u, sine)
+    e_host = sf.l2_error(hier, 3, u.cpu().numpy(), prob.exact)
+    assert abs(e_dev - e_host) <= 1e-12 * e_host

@@ -182,3 +182,65 @@ def test_q7_smoother_matches_oracle(lvl):
     got = sf.MultigridPreconditioner(hier).smooth(lvl, x, b)
     ref = port.VCycle(port.Hierarchy(lvl, 7)).smooth(lvl, x, b)
     assert rel_l2(got, ref) <= 1e-11
+
+
+@pytest.mark.parametrize("mode", [P.FP16, P.FP16_EC, P.FP32])
+def test_q7_low_precision_smoother_band_l3(mode):
+    """Tensor-core fp16/EC colour kernel on a level with interior tiles and shifted colours."""
+    from oracle import port
+
+    lvl = 3
+    H = port.Hierarchy(lvl, 7)
+    D = H.n_dofs(lvl)
+    x, b = unit(np.random.default_rng(5), D), unit(np.random.default_rng(6), D)
+    mg_ref = port.VCycle(H)
+    ref64 = mg_ref.smooth(lvl, x, b, "fp64")
+    ref_err = rel_l2(port.VCycle(H, mode=mode.value).smooth(lvl, x, b, mode.value), ref64)
+    got = sf.MultigridPreconditioner(sf.build_hierarchy(lvl, 7), sf.VCycleConfig(mode=mode)).smooth(lvl, x, b, mode)
+    err = rel_l2(got, ref64)
+    assert err <= 4.0 * ref_err + 1e-6, (err, ref_err)
+
+
+@pytest.mark.parametrize("mode", [P.FP16, P.FP16_EC])
+def test_q7_low_precision_vcycle_band_l3(mode):
+    from oracle import port
+
+    lvl = 3
+    H = port.Hierarchy(lvl, 7)
+    b = unit(np.random.default_rng(4), H.n_dofs(lvl))
+    ref64 = port.VCycle(H).apply(b, lvl)
+    ref_err = rel_l2(port.VCycle(H, mode=mode.value).apply(b, lvl), ref64)
+    got = sf.MultigridPreconditioner(sf.build_hierarchy(lvl, 7), sf.VCycleConfig(mode=mode)).apply(b, lvl)
+    assert rel_l2(got, ref64) <= 4.0 * ref_err + 1e-6, (rel_l2(got, ref64), ref_err)
+
+
+@pytest.mark.parametrize("mode", [P.FP64, P.FP16, P.FP16_EC])
+def test_q7_solve_l4_iterations(mode):
+    """Mixed-precision solves reach the fp64 discretisation error in a comparable iteration count."""
+    out = sf.run_solve(7, 4, mode=mode, maxit=30)
+    # reference: fp16 needs 8 its at Q7 L3 and (paper) 14 at 16.8 MDoF; EC stays at the fp64 count
+    assert out.report.converged and out.report.iterations <= (3 if mode is not P.FP16 else 16)
+    ref = sf.run_solve(7, 4, mode=P.FP64, maxit=30)
+    # Q7 L4's discretisation error (2e-14) is below the algebraic error at tol 1e-8
+    assert out.l2 <= 1.5 * ref.l2 + 1e-12
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 5), (3, 6)])
+def test_ec_solve_keeps_fp64_iteration_count_at_scale(k, lvl):
+    """Range-managed fp16_ec V-cycle at 3e7/1.7e7 DoF: FP64 iteration count (+1), FP64 L2 error.
+    (The unscaled binary16 arithmetic overflows here: NaN at Q7 L5.)"""
+    import math
+
+    from paper_2407_09621_b200.discretization import assemble_rhs_separable, l2_error_separable
+    from paper_2407_09621_b200.experiments import make_operator
+
+    hier = sf.build_hierarchy(lvl, k, max_dofs=2**31)
+    sine = lambda x: np.sin(np.pi * x)
+    b = assemble_rhs_separable(hier, lvl, sine, 3 * math.pi**2)
+    res = {}
+    for mode in (P.FP64, P.FP16_EC):
+        mg = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode))
+        x, rep = sf.fgmres(make_operator(hier, lvl), lambda v: mg.apply(v, lvl), b, tol=1e-8, maxit=20)
+        res[mode] = (rep.iterations, l2_error_separable(hier, lvl, x, sine), rep.converged)
+    assert res[P.FP16_EC][2] and res[P.FP16_EC][0] <= res[P.FP64][0] + 1
+    assert res[P.FP16_EC][1] <= 1.5 * res[P.FP64][1] + 1e-12
