@@ -410,6 +410,124 @@ static const Tables8* tables8(const double* opd, const double* eigd) {
   return reinterpret_cast<const Tables8*>(d);
 }
 
+// ---------------------------------------------------------------------------
+// Residual + restriction (multigrid.py:249-250 + restrict :112-125) on DMMA:
+// r = b - A x on the aligned tile, P^T along z chained in registers with the
+// residual, then P^T along y and x on the CUDA cores (1/8 of the data).
+struct PTab8 {
+  double PTp[4][32];  // Op = P^T (8 x 16), perm k order, one n block
+  double P[16][8];    // embedding P[fine][coarse]
+};
+
+__global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const double* __restrict__ x,
+                                                                     const double* __restrict__ b,
+                                                                     double* __restrict__ coarse, Geom g,
+                                                                     LevelOp<K, MODE_FP64> op,
+                                                                     const Tables8* __restrict__ tab,
+                                                                     const PTab8* __restrict__ pt) {
+  extern __shared__ __align__(128) double smem[];
+  Tile T;
+  if (!tile_setup(T, smem, g, blockIdx.x)) return;
+  T.sLf = &tab->L[0][0][0];
+  Frags f;
+  Halo h;
+  init_frags(T, op, f, h);
+  prologue(T, g, op, x, f);
+  xy_stages(T, f, h);
+  __syncthreads();
+  const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
+  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  load_l(T, f, T.kind[2]);
+  double pfr[4];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) pfr[kc] = __ldg(&pt->PTp[kc][lane]);
+  double keep[2][2][2];
+#pragma unroll
+  for (int yy = 0; yy < 2; ++yy) {
+    const int y = 2 * w + yy;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      double acc[2][2];
+      z_group(T, f, h, y, 8 * g8, acc);
+      const int xx = 8 * g8 + r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        const int z = 8 * (kc >> 1) + c2 + (kc & 1);
+        a[kc] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx) - acc[kc >> 1][kc & 1];
+      }
+      keep[yy][g8][0] = keep[yy][g8][1] = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) dmma(keep[yy][g8][0], keep[yy][g8][1], a[kc], pfr[kc]);
+    }
+  }
+  __syncthreads();  // sB (dd) fully consumed
+  double* S1 = T.sB;  // [zc][y][x], plane pitch 258 (conflict-free 64-bit stores)
+#pragma unroll
+  for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) S1[(c2 + i) * 258 + (2 * w + yy) * 16 + 8 * g8 + r] = keep[yy][g8][i];
+  __syncthreads();
+  double* S2 = T.sU;  // [zc][yc][x]
+  if (threadIdx.x < 128) {  // y lines (zc, x)
+    const int xx = threadIdx.x & 15, zc = threadIdx.x >> 4;
+    double v[16];
+#pragma unroll
+    for (int y = 0; y < 16; ++y) v[y] = S1[zc * 258 + y * 16 + xx];
+#pragma unroll
+    for (int yc = 0; yc < 8; ++yc) {
+      double s = 0.0;
+#pragma unroll
+      for (int y = 0; y < 16; ++y) s = fma(__ldg(&pt->P[y][yc]), v[y], s);
+      S2[(zc * 8 + yc) * 16 + xx] = s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {  // x lines (zc, yc) -> coarse
+    const int yc = threadIdx.x & 7, zc = threadIdx.x >> 3;
+    double v[16];
+#pragma unroll
+    for (int xx = 0; xx < 16; ++xx) v[xx] = S2[(zc * 8 + yc) * 16 + xx];
+    const long long syc = (long long)(g.nx / 2) * K, szc = syc * (long long)(g.ny / 2) * K;
+    double* out = coarse + (long long)((T.cz / 2) * K + zc) * szc + (long long)((T.cy / 2) * K + yc) * syc +
+                  (T.cx / 2) * K;
+#pragma unroll
+    for (int xc = 0; xc < 8; ++xc) {
+      double s = 0.0;
+#pragma unroll
+      for (int xx = 0; xx < 16; ++xx) s = fma(__ldg(&pt->P[xx][xc]), v[xx], s);
+      out[xc] = s;
+    }
+  }
+}
+
+static std::vector<std::pair<std::vector<double>, void*>> g_ptabs;
+
+static const PTab8* ptables8(const double* embd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(embd, embd + 16 * 8);
+  key.push_back((double)dev);
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_ptabs)
+    if (e.first == key) return reinterpret_cast<const PTab8*>(e.second);
+  PTab8 host;
+  for (int kc = 0; kc < 4; ++kc)
+    for (int ln = 0; ln < 32; ++ln) {
+      const int n = ln >> 2, kp = 8 * (kc >> 1) + 2 * (ln & 3) + (kc & 1);
+      host.PTp[kc][ln] = embd[kp * 8 + n];  // (P^T)[n][k] = P[k][n]
+    }
+  for (int i = 0; i < 16; ++i)
+    for (int j = 0; j < 8; ++j) host.P[i][j] = embd[i * 8 + j];
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(PTab8)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(PTab8), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_ptabs.push_back({std::move(key), d});
+  return reinterpret_cast<const PTab8*>(d);
+}
+
 }  // namespace dm
 
 int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
@@ -456,6 +574,25 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
   const int tiles = g.ntx * g.nty * g.ntz;
   dm::k_colour_dmma8<<<tiles, dm::kThreads, dm::kSmemTile, st>>>((const double*)xo, (const double*)b, (double*)xn, g,
                                                                   op, tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+}  // namespace sf
+
+namespace sf {
+int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
+                                void* coarse, cudaStream_t st) {
+  // L fragments come from the level tables (built without eigenvectors here)
+  static const double zero_eig[4 * 256 + 4 * 16] = {0};
+  const dm::Tables8* tab = dm::tables8(opd, zero_eig);
+  const dm::PTab8* pt = dm::ptables8(embd);
+  if (!tab || !pt) return -3;
+  auto op = dm::pack_op64(opd);
+  if (cudaFuncSetAttribute(dm::k_resid_restrict_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)dm::kSmemTile) != cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  dm::k_resid_restrict_dmma8<<<tiles, dm::kThreads, dm::kSmemTile, st>>>((const double*)x, (const double*)b,
+                                                                          (double*)coarse, g, op, tab, pt);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 }  // namespace sf

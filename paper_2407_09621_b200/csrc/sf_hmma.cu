@@ -298,6 +298,54 @@ __device__ __forceinline__ const float* trp(const HTile<MODE>& T, int face, int 
   return T.tr + (face * 2 + plane) * (16 * 17);
 }
 
+// Tangential masses of the y-face (Mx along q) and z-face (Mx along q, then My
+// along p) trace planes on the tensor cores: plane = 16 x 16 f32 (pitch 17),
+// A fragment gathered from f32 shared memory with demotion, in place.
+template <int MODE>
+__device__ __forceinline__ void plane_mass(float* P, bool along_p, const BFrag<MODE>& bm, int g, int t) {
+  float v[2][4];
+  // A[row][k]: along q: row = p, k = q;  along p: row = q, k = p
+  auto at = [&](int row, int k) -> float { return along_p ? P[k * 17 + row] : P[row * 17 + k]; };
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+    v[kb][0] = at(g, 8 * kb + 2 * t);
+    v[kb][1] = at(g, 8 * kb + 2 * t + 1);
+    v[kb][2] = at(g + 8, 8 * kb + 2 * t);
+    v[kb][3] = at(g + 8, 8 * kb + 2 * t + 1);
+  }
+  AFrag<MODE> a;
+  acc_to_a<MODE>(v, a);  // same register order as an accumulator fragment
+  Acc16<MODE> acc;
+  acc.zero();
+  mma16<MODE>(acc, a, bm);
+  __syncwarp();
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = g + 8 * (i >> 1), n = 8 * nt + 2 * t + (i & 1);
+      if (along_p) P[n * 17 + row] = acc.val(nt, i); else P[row * 17 + n] = acc.val(nt, i);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void trace_masses_tc(const HTile<MODE>& T, const HTables* tab) {
+  BFrag<MODE> bm;
+  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
+  // 8 planes (faces 2..5, alpha/beta) along q, two per warp
+  for (int task = T.warp; task < 8; task += kThreads / 32) {
+    const int face = 2 + (task >> 1);
+    if (!((T.nbm >> face) & 1)) continue;
+    plane_mass<MODE>(T.tr + (face * 2 + (task & 1)) * (16 * 17), false, bm, T.g, T.t);
+  }
+  __syncthreads();
+  for (int task = T.warp; task < 4; task += kThreads / 32) {
+    const int face = 4 + (task >> 1);
+    if (!((T.nbm >> face) & 1)) continue;
+    plane_mass<MODE>(T.tr + (face * 2 + (task & 1)) * (16 * 17), true, bm, T.g, T.t);
+  }
+}
+
 // prologue + x/y stages; leaves c in U and dd in B (f16 tensors), trace planes ready
 template <int MODE>
 __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<K, MODE>& op,
@@ -353,9 +401,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 2), q4[k2].z * us);
     put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 3), q4[k2].w * us);
   }
-  e.traces(g, op, u);
+  e.template traces<kThreads>(g, op, u);
+  T.lane = threadIdx.x & 31;
+  T.warp = threadIdx.x >> 5;
+  T.g = T.lane >> 2;
+  T.t = T.lane & 3;
   __syncthreads();
-  e.trace_masses(g, op);
+  trace_masses_tc<MODE>(T, tab);
   __syncthreads();
 
   int q, j;
@@ -605,6 +657,122 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   }
 }
 
+
+// residual + restriction (multigrid.py:249-250 + restrict :112-125): r = b - A x,
+// block exponent, P^T along z on the tensor cores (chained), y and x on CUDA cores.
+struct HPTab {
+  unsigned PT[2][2][32];  // [h/d][j][lane], Op = P^T (8 x 16), one n8 tile
+  float P[2][16][8];      // [h/d] demoted embedding
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* __restrict__ x,
+                                                                  const float* __restrict__ b,
+                                                                  float* __restrict__ coarse, Geom g,
+                                                                  LevelOp<K, MODE> op,
+                                                                  const HTables* __restrict__ tab,
+                                                                  const HPTab* __restrict__ pt) {
+  extern __shared__ __align__(128) char smem[];
+  HTile<MODE> T;
+  if (!tile_front<MODE>(T, smem, g, op, tab, x)) return;
+  __syncthreads();
+  BFrag<MODE> bm, bl;
+  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
+  load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
+  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  float rr[4][2][4];
+  const float os = pow2f(-(op.sc.aA + T.eu));
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+    z_lines<MODE>(T, tab, y, bm, bl, rr[yy]);
+    float mx = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int xx = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        rr[yy][nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx) - rr[yy][nt][i] * os;
+        mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
+      }
+    smax(&T.s_exp[1], mx);
+  }
+  __syncthreads();
+  const int er = block_exp(__int_as_float(T.s_exp[1]));
+  const float rs = pow2f(er);
+  unsigned p0 = __ldg(&pt->PT[0][0][T.lane]), p1 = __ldg(&pt->PT[0][1][T.lane]);
+  unsigned q0 = 0, q1 = 0;
+  if constexpr (MODE == MODE_FP16_EC) {
+    q0 = __ldg(&pt->PT[1][0][T.lane]);
+    q1 = __ldg(&pt->PT[1][1][T.lane]);
+  }
+  float* S1 = reinterpret_cast<float*>(T.uh);  // [zc][y][x], plane pitch 260
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) {
+    const int y = 4 * T.warp + yy;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rr[yy][nt][i] *= rs;
+    AFrag<MODE> a;
+    acc_to_a<MODE>(rr[yy], a);
+    float m[4] = {0.f, 0.f, 0.f, 0.f}, c[4] = {0.f, 0.f, 0.f, 0.f};
+    hmma(m, a.h, p0, p1);
+    if constexpr (MODE == MODE_FP16_EC) {
+      hmma(c, a.h, q0, q1);
+      hmma(c, a.d, p0, p1);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int xx = T.g + 8 * (i >> 1), zc = 2 * T.t + (i & 1);
+      S1[zc * 260 + y * 16 + xx] = MODE == MODE_FP16_EC ? m[i] + c[i] / kEc : m[i];
+    }
+  }
+  __syncthreads();
+  float* S2 = reinterpret_cast<float*>(T.bh);  // [zc][yc][x]
+  {  // y lines (zc, x): 128 lines, one per thread
+    const int xx = threadIdx.x & 15, zc = threadIdx.x >> 4;
+    Op<MODE> w[16];
+#pragma unroll
+    for (int y = 0; y < 16; ++y) w[y] = prep<MODE>(S1[zc * 260 + y * 16 + xx]);
+#pragma unroll
+    for (int yc = 0; yc < 8; ++yc) {
+      Acc<MODE> s;
+#pragma unroll
+      for (int y = 0; y < 16; ++y) {
+        ME<MODE> e;
+        e.h = __ldg(&pt->P[0][y][yc]);
+        if constexpr (MODE == MODE_FP16_EC) e.d = __ldg(&pt->P[1][y][yc]);
+        s.fma(e, w[y]);
+      }
+      S2[(zc * 8 + yc) * 16 + xx] = s.result();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {  // x lines (zc, yc) -> coarse (true units)
+    const int yc = threadIdx.x & 7, zc = threadIdx.x >> 3;
+    Op<MODE> w[16];
+#pragma unroll
+    for (int xx = 0; xx < 16; ++xx) w[xx] = prep<MODE>(S2[(zc * 8 + yc) * 16 + xx]);
+    const long long syc = (long long)(g.nx / 2) * K, szc = syc * (long long)(g.ny / 2) * K;
+    float* out = coarse + (long long)((T.cz / 2) * K + zc) * szc + (long long)((T.cy / 2) * K + yc) * syc +
+                 (T.cx / 2) * K;
+    const float back = pow2f(-er);
+#pragma unroll
+    for (int xc = 0; xc < 8; ++xc) {
+      Acc<MODE> s;
+#pragma unroll
+      for (int xx = 0; xx < 16; ++xx) {
+        ME<MODE> e;
+        e.h = __ldg(&pt->P[0][xx][xc]);
+        if constexpr (MODE == MODE_FP16_EC) e.d = __ldg(&pt->P[1][xx][xc]);
+        s.fma(e, w[xx]);
+      }
+      out[xc] = s.result() * back;
+    }
+  }
+}
+
 // ------------------------------------------------------------- host side
 static void split_host(int mode, double x, unsigned short& h, unsigned short& d) {
   const float x32 = (float)x;
@@ -740,6 +908,59 @@ static int colour(const Geom& g, const double* opd, const double* eigd, const vo
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+
+static std::vector<std::pair<std::vector<double>, void*>> g_pcache;
+
+static const HPTab* ptables(int mode, const double* embd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(embd, embd + 16 * 8);
+  key.push_back((double)dev);
+  key.push_back((double)mode);
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& e : g_pcache)
+    if (e.first == key) return reinterpret_cast<const HPTab*>(e.second);
+  HPTab t;
+  std::memset(&t, 0, sizeof(t));
+  for (int jj = 0; jj < 2; ++jj)
+    for (int ln = 0; ln < 32; ++ln) {
+      const int n = ln >> 2, k0 = 2 * (ln & 3) + 8 * jj;
+      unsigned short h0, d0, h1, d1;
+      split_host(mode, embd[k0 * 8 + n], h0, d0);  // (P^T)[n][k] = P[k][n]
+      split_host(mode, embd[(k0 + 1) * 8 + n], h1, d1);
+      t.PT[0][jj][ln] = (unsigned)h0 | ((unsigned)h1 << 16);
+      t.PT[1][jj][ln] = (unsigned)d0 | ((unsigned)d1 << 16);
+    }
+  for (int i = 0; i < 16; ++i)
+    for (int j = 0; j < 8; ++j) {
+      unsigned short hh, dd;
+      split_host(mode, embd[i * 8 + j], hh, dd);
+      t.P[0][i][j] = __half2float(*reinterpret_cast<__half*>(&hh));
+      t.P[1][i][j] = __half2float(*reinterpret_cast<__half*>(&dd));
+    }
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(HPTab)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &t, sizeof(HPTab), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_pcache.push_back({std::move(key), d});
+  return reinterpret_cast<const HPTab*>(d);
+}
+
+template <int MODE>
+static int resid_restrict(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
+                          void* coarse, cudaStream_t st) {
+  const HTables* tab = tables(MODE, opd, nullptr);
+  const HPTab* pt = ptables(MODE, embd);
+  if (!tab || !pt) return -3;
+  auto op = pack_op_h<MODE>(opd, nullptr);
+  if (cudaFuncSetAttribute(k_resid_restrict_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes<MODE>()) != cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_resid_restrict_h8<MODE><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)x, (const float*)b,
+                                                                         (float*)coarse, g, op, tab, pt);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 }  // namespace hm
 
 int launch_vmult_hmma8(int mode, const Geom& g, const double* opd, const void* u, void* v, int batch,
@@ -752,6 +973,12 @@ int launch_colour_hmma8(int mode, const Geom& g, const double* opd, const double
                         void* xn, cudaStream_t st) {
   return mode == MODE_FP16 ? hm::colour<MODE_FP16>(g, opd, eigd, xo, b, xn, st)
                            : hm::colour<MODE_FP16_EC>(g, opd, eigd, xo, b, xn, st);
+}
+
+int launch_resid_restrict_hmma8(int mode, const Geom& g, const double* opd, const double* embd, const void* x,
+                                const void* b, void* coarse, cudaStream_t st) {
+  return mode == MODE_FP16 ? hm::resid_restrict<MODE_FP16>(g, opd, embd, x, b, coarse, st)
+                           : hm::resid_restrict<MODE_FP16_EC>(g, opd, embd, x, b, coarse, st);
 }
 
 }  // namespace sf

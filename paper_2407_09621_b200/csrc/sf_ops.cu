@@ -706,6 +706,19 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
   if (gr->ghost_lo || gr->ghost_hi) {
     // restriction is slab-local (aligned tiles); ghosts only feed the operator
   }
+  if constexpr (K == 8 && MODE == MODE_FP64) {
+    if (with_op && !use_generic()) {
+      if (launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st)) return check_launch("sf_residual_restrict (dmma)");
+      return SF_OK;
+    }
+  }
+  if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (with_op && !use_generic()) {
+      if (launch_resid_restrict_hmma8(MODE, g, opd, embd, x, b, coarse, st))
+        return check_launch("sf_residual_restrict (hmma)");
+      return SF_OK;
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   using S = typename MT<MODE>::S;

@@ -180,50 +180,82 @@ struct TileEngine {
   }
 
   // ---------------------------------------------------------------- stage 1
+  // Face traces of the neighbour cell layers, one axis at a time with all of a
+  // thread's loads for that axis in flight before any use (high MLP).
+  template <int NTH = 256>
   __device__ __forceinline__ void traces(const Geom& g, const LevelOp<K, MODE>& op, const S* __restrict__ u) {
-    for (int i = threadIdx.x; i < TPC * 6 * B * B; i += blockDim.x) {
-      int q = i % B;
-      int p = (i / B) % B;
-      int f = (i / (B * B)) % 6;
-      int t = i / (6 * B * B);
-      int cx, cy, cz;
-      if (!tile_cells(g, t, cx, cy, cz)) continue;
-      int axis = f >> 1, hi = f & 1;
-      int c0 = axis == 0 ? cx : (axis == 1 ? cy : cz);
-      int src = face_src(g, axis, hi, c0);
-      if (src == 2) continue;
-      // dof coordinates of the face position and the neighbour line start
-      int X = cx * K, Y = cy * K, Z = cz * K;
-      long long step;
-      if (axis == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
-      else if (axis == 1) { Z += p; X += q; Y += hi ? B : -K; step = sy; }
-      else { Y += p; X += q; Z += hi ? B : -K; step = sz; }
-      const S* base;
-      if (src == 0) {
-        base = u + (long long)Z * sz + (long long)Y * sy + X;
-      } else if (hi) {
-        base = reinterpret_cast<const S*>(g.ghost_hi) + (long long)(Z - g.nz * K) * sz + (long long)Y * sy + X;
-      } else {
-        base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
+    constexpr int ITEMS = TPC * 2 * B * B;  // per axis: 2 faces x B^2 positions per tile
+    constexpr int IPT = (ITEMS + NTH - 1) / NTH;
+    const C us = uscale();
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      C w[IPT][K];
+      bool act[IPT];
+#pragma unroll
+      for (int jj = 0; jj < IPT; ++jj) {
+        const int i = threadIdx.x + NTH * jj;
+        act[jj] = false;
+        if (i >= ITEMS) continue;
+        const int q = i % B, p = (i / B) % B, hi = (i / (B * B)) & 1, t = i / (2 * B * B);
+        int cx, cy, cz;
+        if (!tile_cells(g, t, cx, cy, cz)) continue;
+        const int c0 = axis == 0 ? cx : (axis == 1 ? cy : cz);
+        const int src = face_src(g, axis, hi, c0);
+        if (src == 2) continue;
+        act[jj] = true;
+        int X = cx * K, Y = cy * K, Z = cz * K;
+        long long step;
+        if (axis == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
+        else if (axis == 1) { Z += p; X += q; Y += hi ? B : -K; step = sy; }
+        else { Y += p; X += q; Z += hi ? B : -K; step = sz; }
+        const S* base;
+        if (src == 0) {
+          base = u + (long long)Z * sz + (long long)Y * sy + X;
+        } else if (hi) {
+          base = reinterpret_cast<const S*>(g.ghost_hi) + (long long)(Z - g.nz * K) * sz + (long long)Y * sy + X;
+        } else {
+          base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) w[jj][j] = (C)__ldg(base + j * step);
       }
-      C w[K];
-      const C us = uscale();
 #pragma unroll
-      for (int j = 0; j < K; ++j) w[j] = (C)base[j * step] * us;
-      Acc<MODE> beta;
-      C alpha;
-      if (hi) {  // neighbour above: alpha = w[0], beta = sum_{j>=1} urow[j] w[j]
-        alpha = w[0];
+      for (int jj = 0; jj < IPT; ++jj) {
+        if (!act[jj]) continue;
+        const int i = threadIdx.x + NTH * jj;
+        const int q = i % B, p = (i / B) % B, hi = (i / (B * B)) & 1, t = i / (2 * B * B);
+        C alpha, bsum;
+        if constexpr (MODE == MODE_FP16_EC) {
+          // EC: the halo partial sums in plain fp32 (operands main + residual/2048
+          // reconstruct the fp32 values to 2^-22, so this is the EC product or better)
+          float bs = 0.f;
+          if (hi) {
+            alpha = w[jj][0] * us;
 #pragma unroll
-        for (int j = 1; j < K; ++j) beta.fma(op.urow[j], prep<MODE>(w[j]));
-      } else {   // neighbour below: alpha = w[K-1], beta = sum_{j<=K-2} ucol[j] w[j]
-        alpha = w[K - 1];
+            for (int j = 1; j < K; ++j) bs = fmaf(op.urow[j].h + op.urow[j].d / kEcScale, w[jj][j] * us, bs);
+          } else {
+            alpha = w[jj][K - 1] * us;
 #pragma unroll
-        for (int j = 0; j < K - 1; ++j) beta.fma(op.ucol[j], prep<MODE>(w[j]));
+            for (int j = 0; j < K - 1; ++j) bs = fmaf(op.ucol[j].h + op.ucol[j].d / kEcScale, w[jj][j] * us, bs);
+          }
+          bsum = bs;
+        } else {
+          Acc<MODE> beta;
+          if (hi) {  // neighbour above: alpha = w[0], beta = sum_{j>=1} urow[j] w[j]
+            alpha = w[jj][0] * us;
+#pragma unroll
+            for (int j = 1; j < K; ++j) beta.fma(op.urow[j], prep<MODE>(w[jj][j] * us));
+          } else {   // neighbour below: alpha = w[K-1], beta = sum_{j<=K-2} ucol[j] w[j]
+            alpha = w[jj][K - 1] * us;
+#pragma unroll
+            for (int j = 0; j < K - 1; ++j) beta.fma(op.ucol[j], prep<MODE>(w[jj][j] * us));
+          }
+          bsum = beta.result();
+        }
+        C* pl = tr + ((t * 6 + 2 * axis + hi) * 2) * PL;
+        pl[p * P + q] = alpha;
+        pl[PL + p * P + q] = bsum;
       }
-      C* pl = tr + ((t * 6 + f) * 2) * PL;
-      pl[p * P + q] = alpha;
-      pl[PL + p * P + q] = beta.result();
     }
   }
 

@@ -221,8 +221,9 @@ def test_q7_solve_l4_iterations(mode):
     # reference: fp16 needs 8 its at Q7 L3 and (paper) 14 at 16.8 MDoF; EC stays at the fp64 count
     assert out.report.converged and out.report.iterations <= (3 if mode is not P.FP16 else 16)
     ref = sf.run_solve(7, 4, mode=P.FP64, maxit=30)
-    # Q7 L4's discretisation error (2e-14) is below the algebraic error at tol 1e-8
-    assert out.l2 <= 1.5 * ref.l2 + 1e-12
+    # Q7 L4's discretisation error (2e-14) is below the algebraic error at tol 1e-8; plain fp16
+    # stops at a larger algebraic error, as the reference's does (Q7 L3: 2.1e-11 vs 2.5e-13)
+    assert out.l2 <= (1.5 * ref.l2 + 1e-12 if mode is not P.FP16 else 1e-9)
 
 
 @pytest.mark.parametrize("k,lvl", [(7, 5), (3, 6)])
@@ -244,3 +245,27 @@ def test_ec_solve_keeps_fp64_iteration_count_at_scale(k, lvl):
         res[mode] = (rep.iterations, l2_error_separable(hier, lvl, x, sine), rep.converged)
     assert res[P.FP16_EC][2] and res[P.FP16_EC][0] <= res[P.FP64][0] + 1
     assert res[P.FP16_EC][1] <= 1.5 * res[P.FP64][1] + 1e-12
+
+
+@pytest.mark.parametrize("mode", [P.FP64, P.FP16, P.FP16_EC])
+def test_fused_residual_restriction_q7(mode):
+    """sf_residual_restrict with x (tensor-core fused kernel) == restrict(b - A x)."""
+    import torch
+
+    from oracle import port
+    from paper_2407_09621_b200.multigrid import restrict_device
+
+    lvl = 3
+    H = port.Hierarchy(lvl, 7)
+    rng = np.random.default_rng(17)
+    x = unit(rng, H.n_dofs(lvl))
+    b = unit(rng, H.n_dofs(lvl))
+    r = b - port.apply_operator(H, lvl, x)
+    ref = port.restrict(H, lvl, r)
+    hier = sf.build_hierarchy(lvl, 7)
+    xt = torch.from_numpy(x).to("cuda", mode.torch_dtype)
+    bt = torch.from_numpy(b).to("cuda", mode.torch_dtype)
+    out = torch.empty(hier.n_dofs(lvl - 1), dtype=mode.torch_dtype, device="cuda")
+    restrict_device(hier, lvl, bt, out, mode, x=xt)
+    err = rel_l2(out.cpu().numpy(), ref)
+    assert err <= (1e-12 if mode is P.FP64 else 5e-3 if mode is P.FP16 else 1e-5), err
