@@ -52,11 +52,13 @@ def ref_flops_per_dof(k, level):
 
 
 def kernel_flops_per_dof(k):
-    """Flops the cell-wise tile kernel executes per DoF (interior tiles):
-    line stages 7K + 9 - 3/K MACs, face traces 3(K-1)/K, trace-plane masses 6, plus 2 adds."""
-    K = k + 1
-    macs = 7 * K + 9 - 3.0 / K + 3.0 * (K - 1) / K + 6.0
-    return 2 * macs + 2
+    """Tensor-pipe flops the FP64 Q7 vmult kernel executes per DoF: one 2x2x2-cell tile
+    (4096 DoF) issues 1376 DMMA.8x8x4 (512 flop each): x stage 384, y stage 512, z stage 384, trace-plane
+    masses 96.  This is the figure ncu's DMMA-pipe utilisation measures, so frac and the pipe % agree."""
+    if k != 7:
+        K = k + 1  # CUDA-core tile engine: line stages 7K + 9 - 3/K MACs + traces/masses (DESIGN.md §4.4)
+        return 2 * (7 * K + 9 - 3.0 / K + 3.0 * (K - 1) / K + 6.0) + 2
+    return 1376 * 512 / 4096
 
 
 class ClockSampler:

@@ -43,8 +43,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
         return LIB
     objs = []
 
+    headers = [d for d in deps if not d.endswith(".cu")]
+
     def compile_one(src):
         obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        if not force and not _stale(obj, [os.path.join(CSRC, src), *headers]):
+            return obj
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

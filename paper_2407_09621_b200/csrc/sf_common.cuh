@@ -191,4 +191,24 @@ struct Geom {
   long long batch_stride;  // elements between batched vectors (blockIdx.y)
 };
 
+// Tile id -> tile coordinates in an L2-aware order: y is cut into bands of
+// kBandTiles/ntx rows; inside a band the order is x fastest, then y, then z.
+// A tile's z neighbours are then ~kBandTiles launches away (instead of
+// ntx*nty), so the neighbour cell layers its face traces read are still in
+// L2 (profiles/r01_vmult_fp64.md).
+constexpr int kBandTiles = 512;
+__device__ __forceinline__ void tile_coords(const Geom& g, int id, int& tx, int& ty, int& tz) {
+  int by = kBandTiles / g.ntx;
+  by = by < 1 ? 1 : (by > g.nty ? g.nty : by);
+  const int per_band = g.ntx * by * g.ntz;
+  const int band = id / per_band;
+  const int off = id - band * per_band;
+  const int rem = g.nty - band * by;
+  const int bh = rem < by ? rem : by;
+  tx = off % g.ntx;
+  const int r = off / g.ntx;
+  ty = band * by + r % bh;
+  tz = r / bh;
+}
+
 }  // namespace sf

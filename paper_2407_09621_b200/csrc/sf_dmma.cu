@@ -68,8 +68,24 @@ static LevelOp<K, MODE_FP64> pack_op64(const double* opd) {
   return op;
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident operator fragment tables of one level (fp64, K = 8).
+// Fragment slot fr = 4*nb + kc of lane ln holds B[k][n] = Op[8nb + (ln>>2)][k-index]:
+//   std : k-index = 4kc + (ln&3)             (A fragment loaded from shared memory)
+//   perm: k-index = 8(kc>>1) + 2(ln&3) + (kc&1)  (A fragment = the previous C fragment,
+//         so two contractions along the same axis chain in registers)
+struct Tables8 {
+  double L[4][8][32];    // L_smooth[kind], std
+  double Vf[4][8][32];   // Op = V^T (forward transform), std
+  double Vfp[4][8][32];  // Op = V^T, perm
+  double Vb[4][8][32];   // Op = V (backward transform), std
+  double Vbp[4][8][32];  // Op = V, perm
+  double lam[4][16];     // generalised eigenvalues per kind
+};
+
 __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __restrict__ u, double* __restrict__ v,
-                                                            Geom g, LevelOp<K, MODE_FP64> op, PatchL pl) {
+                                                            Geom g, LevelOp<K, MODE_FP64> op,
+                                                            const Tables8* __restrict__ tab) {
   extern __shared__ __align__(128) double smem[];
   u += (long long)blockIdx.y * g.batch_stride;
   v += (long long)blockIdx.y * g.batch_stride;
@@ -78,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  stage_l_frags(T, &pl.L[0][0][0]);
+  T.sLf = &tab->L[0][0][0];  // per-lane fragments from the L1-cached device table (coalesced)
   prologue(T, g, op, u, f);
   xy_stages(T, f, h);
   __syncthreads();
@@ -111,7 +127,8 @@ enum { BAR_FULL0 = 1, BAR_EMPTY0 = 3, BAR_CONS = 5, BAR_PROD = 6 };
 
 __global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* __restrict__ u,
                                                                  double* __restrict__ v, Geom g,
-                                                                 LevelOp<K, MODE_FP64> op, PatchL pl) {
+                                                                 LevelOp<K, MODE_FP64> op,
+                                                                 const Tables8* __restrict__ tab) {
   extern __shared__ __align__(128) double smem[];
   double* sUbuf[2] = {smem, smem + VOL};
   double* trbuf[2] = {smem + 2 * VOL, smem + 2 * VOL + 12 * TRP};
@@ -125,7 +142,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* 
   tile_geom(T, g, 0);  // lane/warp fields
   for (int i = tid; i < 4 * 8 * 32; i += kWsThreads) {
     const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
-    sLf[i] = pl.L[kind][8 * (fr >> 2) + (ln >> 2)][4 * (fr & 3) + (ln & 3)];
+    sLf[i] = (&tab->L[0][0][0])[i];
   }
   Frags f;
   Halo h;
@@ -181,20 +198,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Device-resident operator fragment tables of one level (fp64, K = 8).
-// Fragment slot fr = 4*nb + kc of lane ln holds B[k][n] = Op[8nb + (ln>>2)][k-index]:
-//   std : k-index = 4kc + (ln&3)             (A fragment loaded from shared memory)
-//   perm: k-index = 8(kc>>1) + 2(ln&3) + (kc&1)  (A fragment = the previous C fragment,
-//         so two contractions along the same axis chain in registers)
-struct Tables8 {
-  double L[4][8][32];    // L_smooth[kind], std
-  double Vf[4][8][32];   // Op = V^T (forward transform), std
-  double Vfp[4][8][32];  // Op = V^T, perm
-  double Vb[4][8][32];   // Op = V (backward transform), std
-  double Vbp[4][8][32];  // Op = V, perm
-  double lam[4][16];     // generalised eigenvalues per kind
-};
 
 __device__ __forceinline__ void load_frag(const double* tab /* [8][32] */, double (*l)[4], int lane) {
 #pragma unroll
@@ -533,7 +536,9 @@ static const PTab8* ptables8(const double* embd) {
 int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   static_assert(dm::kSmemTile <= 113 * 1024, "two CTAs per SM");
   auto op = dm::pack_op64(opd);
-  dm::PatchL pl = dm::build_patch_l(opd);
+  static const double zero_eig[4 * 256 + 4 * 16] = {0};
+  const dm::Tables8* tab = dm::tables8(opd, zero_eig);
+  if (!tab) return -3;
   static const int ws = [] {
     const char* e = getenv("SUMFACT_B200_DMMA_WS");
     return (e && *e == '1') ? 1 : 0;  // opt-in: measured slower than two independent CTAs per SM
@@ -548,7 +553,7 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = g.ntx * g.nty * g.ntz;
     const int grid = tiles < sms ? tiles : sms;
-    dm::k_vmult_dmma8_ws<<<grid, dm::kWsThreads, dm::kSmemWs, st>>>((const double*)u, (double*)v, g, op, pl);
+    dm::k_vmult_dmma8_ws<<<grid, dm::kWsThreads, dm::kSmemWs, st>>>((const double*)u, (double*)v, g, op, tab);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   }
   cudaError_t err =
@@ -556,7 +561,7 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
   if (err != cudaSuccess) return -3;
   const int tiles = g.ntx * g.nty * g.ntz;
   dm::k_vmult_dmma8<<<dim3(tiles, batch), dm::kThreads, dm::kSmemTile, st>>>((const double*)u, (double*)v, g, op,
-                                                                              pl);
+                                                                              tab);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

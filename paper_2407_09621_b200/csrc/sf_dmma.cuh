@@ -108,10 +108,11 @@ __device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0)
 
 __device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
   if (tile_id >= g.ntx * g.nty * g.ntz) return false;
-  const int tx = tile_id % g.ntx, rr = tile_id / g.ntx;
+  int tx, ty, tz;
+  tile_coords(g, tile_id, tx, ty, tz);
   T.cx = g.tx0 + 2 * tx;
-  T.cy = g.ty0 + 2 * (rr % g.nty);
-  T.cz = g.tz0 + 2 * (rr / g.nty);
+  T.cy = g.ty0 + 2 * ty;
+  T.cz = g.tz0 + 2 * tz;
   T.sy = (long long)g.nx * K;
   T.sz = T.sy * (long long)g.ny * K;
   const int c0[3] = {T.cx, T.cy, T.cz};

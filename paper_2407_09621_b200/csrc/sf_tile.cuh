@@ -133,10 +133,8 @@ struct TileEngine {
   __device__ __forceinline__ bool tile_cells(const Geom& g, int t, int& cx, int& cy, int& cz) const {
     int id = tile0 + t;
     if (id >= ntiles_total) return false;
-    int tx = id % g.ntx;
-    int r = id / g.ntx;
-    int ty = r % g.nty;
-    int tz = r / g.nty;
+    int tx, ty, tz;
+    tile_coords(g, id, tx, ty, tz);
     cx = g.tx0 + 2 * tx;
     cy = g.ty0 + 2 * ty;
     cz = g.tz0 + 2 * tz;

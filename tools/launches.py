@@ -15,7 +15,8 @@ def load(path):
             v = float(r[i_val].replace(",", ""))
         except ValueError:
             continue
-        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[i_unit], 1.0)
+        scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+                 "second": 1e3, "s": 1e3}[r[i_unit]]
         out.append((r[i_name], v * scale))
     return out
 
