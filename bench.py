@@ -189,31 +189,18 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     u = torch.randn(D, dtype=torch.float64, device="cuda", generator=gen)
     v = torch.empty_like(u)
-    plane = A * A
     if world > 1:
-        glo = torch.empty(K * plane, dtype=torch.float64, device="cuda")
-        ghi = torch.empty(K * plane, dtype=torch.float64, device="cuda")
-        grid = _native.SfGrid(n, n, n, glo.data_ptr() if rank > 0 else None,
-                              ghi.data_ptr() if rank < world - 1 else None)
+        from paper_2407_09621_b200 import slab
+
+        op = slab.DistributedOperator.weak(hier, lvl, slab.SlabComm())  # NCCL K-plane halo + ghosted vmult
+
+        def step():
+            op.apply(u, v, P.FP64)
     else:
         grid = hier.grid(lvl)
 
-    def exchange():
-        ops = []
-        if rank > 0:
-            ops.append(dist.P2POp(dist.isend, u[:K * plane], rank - 1))
-            ops.append(dist.P2POp(dist.irecv, glo, rank - 1))
-        if rank < world - 1:
-            ops.append(dist.P2POp(dist.isend, u[D - K * plane:], rank + 1))
-            ops.append(dist.P2POp(dist.irecv, ghi, rank + 1))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-
-    def step():
-        if world > 1:
-            exchange()
-        vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
+        def step():
+            vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
 
     for _ in range(max(args.warmup, 3)):
         step()

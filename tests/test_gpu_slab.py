@@ -1,0 +1,32 @@
+"""z-slab decomposition with the CUDA kernels: 2 and 4 ranks sharing cuda:0 (gloo, host-staged halos --
+the NCCL path moves the same tensors), checked against the single-GPU path (SURVEY.md §8e:
+"compare an N-GPU slab run to the 1-GPU run")."""
+import pytest
+
+from slab_launch import run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,k,lvl", [(2, 7, 3), (4, 3, 4), (2, 2, 3)])
+def test_distributed_vmult_and_vcycle_fp64(world, k, lvl):
+    res = run(world, "--case", "gpu", "--degree", k, "--level", lvl, "--mode", "fp64")
+    for r in res:
+        assert r["vmult_rel_err"] <= 1e-14, r
+        assert r["weak_vmult_rel_err"] <= 1e-14, r
+        assert r["vcycle_rel_err"] <= 1e-12, r
+
+
+@pytest.mark.parametrize("mode", ["fp16", "fp16_ec", "fp32"])
+def test_distributed_vcycle_low_precision(mode):
+    res = run(2, "--case", "gpu", "--degree", 7, "--level", 3, "--mode", mode)
+    for r in res:
+        assert r["vcycle_rel_err"] <= 1e-5, r
+
+
+@pytest.mark.parametrize("world,k,lvl,mode", [(2, 7, 4, "fp64"), (2, 7, 4, "fp16_ec"), (4, 3, 5, "fp64")])
+def test_distributed_fgmres_solve_matches_single_gpu(world, k, lvl, mode):
+    res = run(world, "--case", "gpu", "--degree", k, "--level", lvl, "--mode", mode, "--solve")
+    for r in res:
+        assert r["its_dist"] == r["its_single"], r
+        assert r["solve_rel_err"] <= 1e-8, r
