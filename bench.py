@@ -325,6 +325,18 @@ def extras(sf, hier, lvl, k, u, v):
         b = torch.randn(D6, dtype=mode.torch_dtype, device="cuda")
         ms = timeit(lambda: mg._smooth_device(6, x, b, mode), reps=2)
         res[f"smooth_step_q{k}_l6_{mode.value}_ms"] = ms
+    del x, b, mg
+    # time-to-solution (BASELINE configs[3]): FGMRES(fp64) + V-cycle(fp64 | fp16_ec), Q7 level 6,
+    # 1.34e8 DoF, setup excluded (tools/bench_solve.py)
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from bench_solve import solve_once
+
+        for mode in (P.FP64, P.FP16_EC):
+            r = solve_once(h6, 6, mode, reps=1)
+            res[f"solve_q{k}_l6_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
+    except Exception as exc:  # secondary measurement only
+        res["solve_error"] = repr(exc)[:200]
     return res
 
 

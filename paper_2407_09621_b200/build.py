@@ -29,6 +29,19 @@ def _deps():
     return files
 
 
+def _includes(path, seen=None):
+    """path plus every local header it #includes (transitively)."""
+    import re
+
+    seen = seen if seen is not None else set()
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for inc in re.findall(r'#include\s+"([^"]+)"', open(path).read()):
+        _includes(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return seen
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -43,11 +56,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         return LIB
     objs = []
 
-    headers = [d for d in deps if not d.endswith(".cu")]
-
     def compile_one(src):
         obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
-        if not force and not _stale(obj, [os.path.join(CSRC, src), *headers]):
+        if not force and not _stale(obj, _includes(os.path.join(CSRC, src))):
             return obj
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:

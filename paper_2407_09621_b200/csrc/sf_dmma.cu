@@ -85,17 +85,18 @@ struct Tables8 {
 
 __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __restrict__ u, double* __restrict__ v,
                                                             Geom g, LevelOp<K, MODE_FP64> op,
-                                                            const Tables8* __restrict__ tab) {
+                                                            const Tables8* __restrict__ tab, int prefetch) {
   extern __shared__ __align__(128) double smem[];
   u += (long long)blockIdx.y * g.batch_stride;
   v += (long long)blockIdx.y * g.batch_stride;
   Tile T;
   if (!tile_setup(T, smem, g, blockIdx.x)) return;
+  if (prefetch) prefetch_tile_l2(g, u, blockIdx.x + prefetch);
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
   T.sLf = &tab->L[0][0][0];  // per-lane fragments from the L1-cached device table (coalesced)
-  prologue(T, g, op, u, f);
+  prologue_xs(T, g, op, u, f);
   xy_stages(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
     }
   }
 }
+
 
 
 // Persistent warp-specialised variant: 8 consumer warps run the x/y/z stages of
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __re
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue(T, g, op, xo, f);
+  prologue_xs(T, g, op, xo, f);
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue(T, g, op, x, f);
+  prologue_xs(T, g, op, x, f);
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -556,12 +558,17 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
     dm::k_vmult_dmma8_ws<<<grid, dm::kWsThreads, dm::kSmemWs, st>>>((const double*)u, (double*)v, g, op, tab);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   }
-  cudaError_t err =
-      cudaFuncSetAttribute(dm::k_vmult_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
+  auto kern = dm::k_vmult_dmma8;
+  static const int pf = [] {
+    const char* e = getenv("SUMFACT_B200_PREFETCH");
+    return e ? atoi(e) : 148;  // one CTA per SM ahead: +2.5% (profiles/r01_vmult_fp64.md)
+  }();
+
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
   if (err != cudaSuccess) return -3;
   const int tiles = g.ntx * g.nty * g.ntz;
-  dm::k_vmult_dmma8<<<dim3(tiles, batch), dm::kThreads, dm::kSmemTile, st>>>((const double*)u, (double*)v, g, op,
-                                                                              tab);
+  kern<<<dim3(tiles, batch), dm::kThreads, dm::kSmemTile, st>>>((const double*)u, (double*)v, g, op,
+                                                                              tab, pf);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

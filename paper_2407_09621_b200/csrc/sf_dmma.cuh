@@ -142,6 +142,19 @@ __device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g,
   return tile_geom(T, g, tile_id);
 }
 
+// L2 prefetch of the u rows of tile `tile_id` (one 128-byte row per thread, 256 rows): issued
+// ~one wave of CTAs ahead so the tile's own cp.async (and its neighbours' trace loads) hit L2.
+__device__ __forceinline__ void prefetch_tile_l2(const Geom& g, const double* __restrict__ u, int tile_id) {
+  if (tile_id >= g.ntx * g.nty * g.ntz || threadIdx.x >= 256) return;
+  int tx, ty, tz;
+  tile_coords(g, tile_id, tx, ty, tz);
+  const long long sy = (long long)g.nx * K, sz = sy * (long long)g.ny * K;
+  const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
+  const double* p = u + (long long)((g.tz0 + 2 * tz) * K + z) * sz + (long long)((g.ty0 + 2 * ty) * K + y) * sy +
+                    (g.tx0 + 2 * tx) * K;
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 // named barriers (id 0 is __syncthreads)
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
@@ -389,6 +402,300 @@ __device__ __forceinline__ void init_frags(const Tile& T, const OpT& op, Frags& 
   h.ur[1] = op.urow[T.c2 + 1].h;
   h.uc[0] = op.ucol[T.c2].h;
   h.uc[1] = op.ucol[T.c2 + 1].h;
+}
+
+
+// ---------------------------------------------------------------------------
+// Software-pipelined front end (vmult / colour / residual-restriction kernels):
+// the neighbour-trace loads of axis a+1 are issued into registers before the
+// DMMA stage of axis a and consumed after it, so two thirds of the L2/HBM trace
+// latency hides behind tensor-core work (profiles/r01_vmult_fp64.md).
+constexpr int kTIPT = 512 / kThreads;  // trace items per thread and axis (2 faces x 256 points / CTA)
+
+template <int AXIS>
+__device__ __forceinline__ void trace_load(const Tile& T, const Geom& g, const double* __restrict__ u,
+                                           double (&w)[kTIPT][K]) {
+#pragma unroll
+  for (int j = 0; j < kTIPT; ++j) {
+    const int it = threadIdx.x + kThreads * j;
+    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
+    if (!((T.nbm >> (2 * AXIS + hi)) & 1)) continue;
+    int X = T.cx * K, Y = T.cy * K, Z = T.cz * K;
+    long long step;
+    if (AXIS == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
+    else if (AXIS == 1) { Z += p; X += q; Y += hi ? B : -K; step = T.sy; }
+    else { Y += p; X += q; Z += hi ? B : -K; step = T.sz; }
+    const double* base;
+    if (AXIS == 2 && (Z < 0 || Z >= g.nz * K)) {
+      base = hi ? reinterpret_cast<const double*>(g.ghost_hi) + (long long)(Z - g.nz * K) * T.sz
+                : reinterpret_cast<const double*>(g.ghost_lo) + (long long)(Z + K) * T.sz;
+      base += (long long)Y * T.sy + X;
+    } else {
+      base = u + (long long)Z * T.sz + (long long)Y * T.sy + X;
+    }
+    if (AXIS == 0) {
+#pragma unroll
+      for (int c = 0; c < K / 2; ++c) {
+        const double2 v2 = __ldg(reinterpret_cast<const double2*>(base + 2 * c));
+        w[j][2 * c] = v2.x;
+        w[j][2 * c + 1] = v2.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) w[j][c] = __ldg(base + c * step);
+    }
+  }
+}
+
+template <int AXIS, class OpT>
+__device__ __forceinline__ void trace_store(const Tile& T, const OpT& op, const double (&w)[kTIPT][K]) {
+#pragma unroll
+  for (int j = 0; j < kTIPT; ++j) {
+    const int it = threadIdx.x + kThreads * j;
+    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
+    if (!((T.nbm >> (2 * AXIS + hi)) & 1)) continue;
+    double alpha, beta = 0.0;
+    if (hi) {
+      alpha = w[j][0];
+#pragma unroll
+      for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[j][c], beta);
+    } else {
+      alpha = w[j][K - 1];
+#pragma unroll
+      for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[j][c], beta);
+    }
+    double* pl = T.tr + (2 * AXIS + hi) * 2 * TRP;
+    pl[p * TRW + q] = alpha;
+    pl[TRP + p * TRW + q] = beta;
+  }
+}
+
+// tangential mass along q (Mx) on trace planes [first, first + 4): one 8-row group per warp task
+__device__ __forceinline__ void plane_mass_rows(const Tile& T, const Frags& f, int first) {
+  for (int task = T.warp; task < 8; task += kThreads / 32) {
+    const int plane = first + (task >> 1);
+    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
+    double* P = T.tr + plane * TRP + (task & 1) * 8 * TRW;
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = P[T.r * TRW + 4 * kc + T.k4];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    mass_group(f, a, acc);
+    __syncwarp();
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      P[T.r * TRW + 8 * nb + T.c2] = acc[nb][0];
+      P[T.r * TRW + 8 * nb + T.c2 + 1] = acc[nb][1];
+    }
+  }
+}
+// tangential mass along p (My) on the z-face planes 8..11
+__device__ __forceinline__ void plane_mass_cols(const Tile& T, const Frags& f) {
+  for (int task = T.warp; task < 8; task += kThreads / 32) {
+    const int plane = 8 + (task >> 1);
+    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
+    double* P = T.tr + plane * TRP + (task & 1) * 8;
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = P[(4 * kc + T.k4) * TRW + T.r];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    mass_group(f, a, acc);
+    __syncwarp();
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      P[(8 * nb + T.c2) * TRW + T.r] = acc[nb][0];
+      P[(8 * nb + T.c2 + 1) * TRW + T.r] = acc[nb][1];
+    }
+  }
+}
+
+// x stage on the warp's two z planes: a = Mx u -> U, b = Lx u (+ x halo) -> B (rows stay in their row)
+__device__ __forceinline__ void x_stage(const Tile& T, Frags& f, const Halo& h) {
+  load_l(T, f, T.kind[0]);
+#pragma unroll 1
+  for (int zz = 0; zz < 2; ++zz) {
+    const int z = 2 * T.warp + zz;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int y = 8 * g8 + T.r;
+      double a[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU(z, y, 4 * kc + T.k4)];
+      double ra[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, rb[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      mass_group(f, a, ra);
+      stiff_group(f, a, rb);
+      h.apply(T, rb, 0, z * TRW + y);
+      __syncwarp();  // lines y of this group live in rows y only: in-place per group is safe
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int i = idxA(z, y, 8 * nb + T.c2);
+        *reinterpret_cast<double2*>(&T.sU[i]) = make_double2(ra[nb][0], ra[nb][1]);
+        *reinterpret_cast<double2*>(&T.sB[i]) = make_double2(rb[nb][0], rb[nb][1]);
+      }
+    }
+  }
+}
+
+// y stage on the warp's two z planes: c = My a -> U, dd = Ly a (+ y halo) + My b -> B
+__device__ __forceinline__ void y_stage(const Tile& T, Frags& f, const Halo& h) {
+  load_l(T, f, T.kind[1]);
+#pragma unroll 1
+  for (int zz = 0; zz < 2; ++zz) {
+    const int z = 2 * T.warp + zz;
+    double ra[2][2][2], rb[2][2][2];
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + T.r;
+      double a[4], b[4];
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        a[kc] = T.sU[idxA(z, 4 * kc + T.k4, x)];
+        b[kc] = T.sB[idxA(z, 4 * kc + T.k4, x)];
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
+      mass_group(f, a, ra[g8]);
+      stiff_group(f, a, rb[g8]);
+      h.apply(T, rb[g8], 1, z * TRW + x);
+      mass_group(f, b, rb[g8]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int x = 8 * g8 + T.r;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int j = idxC(z, 8 * nb + T.c2 + i, x);
+          T.sU[j] = ra[g8][nb][i];
+          T.sB[j] = rb[g8][nb][i];
+        }
+    }
+    __syncwarp();
+  }
+}
+
+// Prologue with all three axes' trace loads in flight at once (one L2/HBM round trip
+// instead of three): 48 doubles of loads per thread, issued before any is consumed.
+template <class OpT>
+__device__ __forceinline__ void prologue_wide(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                              const Frags& f) {
+  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
+    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
+    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
+  }
+  double w0[kTIPT][K], w1[kTIPT][K], w2[kTIPT][K];
+  trace_load<0>(T, g, u, w0);
+  trace_load<1>(T, g, u, w1);
+  trace_load<2>(T, g, u, w2);
+  trace_store<0>(T, op, w0);
+  trace_store<1>(T, op, w1);
+  trace_store<2>(T, op, w2);
+  cp_async_wait_all();
+  __syncthreads();
+  plane_mass_rows(T, f, 4);
+  plane_mass_rows(T, f, 8);
+  __syncthreads();
+  plane_mass_cols(T, f);
+  __syncthreads();
+}
+
+// Prologue with the x-face neighbour layers staged through shared memory: the two x
+// neighbour cell layers (2 x 16 x 16 rows of 8 doubles, 32 KB) go to the still-unused B
+// buffer by cp.async -- 64-byte row segments, coalesced, no registers -- instead of per-lane
+// 64-byte LDGs that touch 32 cache lines per warp instruction.  Chunk c of staged row i
+// sits at chunk c ^ ((i >> 1) & 3): the 8 lanes of an LDS.128 quarter-warp hit 8 distinct
+// bank groups.  y/z faces keep the register path (their loads are row-coalesced).
+__device__ __forceinline__ int xs_idx(int row, int c) { return row * 8 + 2 * (c ^ ((row >> 1) & 3)); }
+
+template <class OpT>
+__device__ __forceinline__ void prologue_xs(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                            const Frags& f) {
+  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
+    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
+    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
+  }
+  // staged row = (hi * 16 + z) * 16 + y ; 4 chunks of 16 B per row
+  for (int c = threadIdx.x; c < 2 * 256 * 4; c += kThreads) {
+    const int ch = c & 3, row = c >> 2, hi = row >> 8, z = (row >> 4) & 15, y = row & 15;
+    if (!((T.nbm >> hi) & 1)) continue;
+    const double* src = ubase + z * T.sz + y * T.sy + (hi ? B : -K) + 2 * ch;
+    cp_async16(&T.sB[xs_idx(row, ch)], src);
+  }
+  double w1[kTIPT][K], w2[kTIPT][K];
+  trace_load<1>(T, g, u, w1);
+  trace_load<2>(T, g, u, w2);
+  trace_store<1>(T, op, w1);
+  trace_store<2>(T, op, w2);
+  cp_async_wait_all();
+  __syncthreads();
+  // x traces from the staged layers: item = (hi, p = z, q = y) -> one staged row
+#pragma unroll
+  for (int j = 0; j < kTIPT; ++j) {
+    const int it = threadIdx.x + kThreads * j;
+    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
+    if (!((T.nbm >> hi) & 1)) continue;
+    const int row = (hi * 16 + p) * 16 + q;
+    double w[K];
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx(row, ch)]);
+      w[2 * ch] = v2.x;
+      w[2 * ch + 1] = v2.y;
+    }
+    double alpha, beta = 0.0;
+    if (hi) {
+      alpha = w[0];
+#pragma unroll
+      for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[c], beta);
+    } else {
+      alpha = w[K - 1];
+#pragma unroll
+      for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
+    }
+    double* pl = T.tr + hi * 2 * TRP;
+    pl[p * TRW + q] = alpha;
+    pl[TRP + p * TRW + q] = beta;
+  }
+  plane_mass_rows(T, f, 4);
+  plane_mass_rows(T, f, 8);
+  __syncthreads();  // also: staged layers consumed before the x stage writes B
+  plane_mass_cols(T, f);
+  __syncthreads();
+}
+
+// Everything before the z stage, pipelined.  On return (after a __syncthreads) U holds c,
+// B holds dd and the z-face planes carry their (My Mx) tangential masses.
+template <class OpT>
+__device__ __forceinline__ void front_stages(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                             Frags& f, const Halo& h) {
+  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
+    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
+    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
+  }
+  double w[kTIPT][K];
+  trace_load<0>(T, g, u, w);
+  trace_store<0>(T, op, w);
+  trace_load<1>(T, g, u, w);  // in flight across the x stage
+  cp_async_wait_all();
+  __syncthreads();
+  x_stage(T, f, h);
+  trace_store<1>(T, op, w);
+  trace_load<2>(T, g, u, w);  // in flight across the y-plane masses and the y stage
+  __syncthreads();
+  plane_mass_rows(T, f, 4);   // y faces: Mx along q
+  __syncthreads();
+  y_stage(T, f, h);
+  trace_store<2>(T, op, w);
+  __syncthreads();
+  plane_mass_rows(T, f, 8);   // z faces: Mx along q
+  __syncthreads();
+  plane_mass_cols(T, f);      // z faces: My along p
+  __syncthreads();
 }
 
 }  // namespace dm

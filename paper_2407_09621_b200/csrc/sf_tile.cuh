@@ -214,8 +214,24 @@ struct TileEngine {
         } else {
           base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
         }
+        constexpr int V = 16 / sizeof(S);  // elements per 16-byte vector
+        if (axis == 0 && V == 4 && K % V == 0) {  // (fp64: scalar loads keep the generic kernels at 3 CTAs/SM)
+          // x faces: the neighbour's K nodes are contiguous -- 16-byte loads (4x / 2x fewer
+          // L1 wavefronts than scalar loads that each touch a different row)
 #pragma unroll
-        for (int j = 0; j < K; ++j) w[jj][j] = (C)__ldg(base + j * step);
+          for (int c = 0; c < K / V; ++c) {
+            if constexpr (V == 4) {
+              const float4 q4 = __ldg(reinterpret_cast<const float4*>(base) + c);
+              w[jj][4 * c] = (C)q4.x; w[jj][4 * c + 1] = (C)q4.y; w[jj][4 * c + 2] = (C)q4.z; w[jj][4 * c + 3] = (C)q4.w;
+            } else {
+              const double2 d2 = __ldg(reinterpret_cast<const double2*>(base) + c);
+              w[jj][2 * c] = (C)d2.x; w[jj][2 * c + 1] = (C)d2.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) w[jj][j] = (C)__ldg(base + j * step);
+        }
       }
 #pragma unroll
       for (int jj = 0; jj < IPT; ++jj) {

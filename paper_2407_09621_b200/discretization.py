@@ -152,6 +152,8 @@ def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = Pre
     numpy in -> numpy out (storage dtype of ``mode``); CUDA tensor in -> CUDA
     tensor out.  ``out`` (optional) receives the result: a host tensor (e.g.
     pinned, for streaming host buffers through the GPU) or a CUDA tensor.
+    Host inputs of at least ``STREAM_MIN_DOFS`` entries are streamed through the
+    GPU in z-slabs (copy-in, vmult and copy-out of consecutive slabs overlap).
     Raises ValueError on a length mismatch, like the reference.
     """
     n = hier.n_dofs(level)
@@ -159,6 +161,18 @@ def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = Pre
     if size != n:
         raise ValueError(f"expected {n} entries, got {size}")
     device.require_cuda()
+    on_host = not (isinstance(u, torch.Tensor) and u.is_cuda)
+    if on_host and n >= STREAM_MIN_DOFS and (out is None or not out.is_cuda):
+        src = u if isinstance(u, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(u).reshape(-1)))
+        if src.dtype != mode.torch_dtype:
+            src = src.to(mode.torch_dtype)
+        src = src.reshape(-1).contiguous()
+        if out is None:
+            dst_np = np.empty(n, dtype=mode.storage_dtype)
+            _stream_vmult(hier, level, src, torch.from_numpy(dst_np), mode)
+            return dst_np if not isinstance(u, torch.Tensor) else torch.from_numpy(dst_np)
+        _stream_vmult(hier, level, src, out.reshape(-1), mode)
+        return out
     if isinstance(u, torch.Tensor) and not u.is_cuda:
         t = u.reshape(-1).to(device="cuda", dtype=mode.torch_dtype, non_blocking=True)
         host = True
@@ -174,6 +188,79 @@ def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = Pre
         torch.cuda.current_stream().synchronize()
         return out
     return device.to_host(v, mode.storage_dtype) if host else v
+
+
+STREAM_MIN_DOFS = 1 << 24
+_STREAM_BUFS: dict = {}
+
+
+def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Tensor, mode: PrecisionMode,
+                  slab_cells: int | None = None):
+    """v = A u for HOST u, v: z-slabs of the vector flow host -> HBM -> host on three streams.
+
+    Slab i's copy-in (with the K ghost planes on each side it needs), its vmult (sf_vmult with
+    ghost_lo/ghost_hi pointing at those planes -- the same mechanism as the multi-GPU halo) and its
+    copy-out run on separate streams, so the host-link transfers in both directions overlap each
+    other and the kernel.  Two device buffers per direction (double buffering).
+    """
+    n, K = hier.n_cells(level), hier.degree + 1
+    layer = K * (n * K) ** 2  # one cell layer of dofs
+    if slab_cells is None:
+        slab_cells = max(2, (n // 16) & ~1)
+    slab_cells = min(slab_cells, n)
+    dt = mode.torch_dtype
+    key = (torch.cuda.current_device(), dt, slab_cells, layer)
+    bufs = _STREAM_BUFS.get(key)
+    if bufs is None:
+        _STREAM_BUFS.clear()
+        bufs = {"in": [torch.empty((slab_cells + 2) * layer, dtype=dt, device="cuda") for _ in range(2)],
+                "out": [torch.empty(slab_cells * layer, dtype=dt, device="cuda") for _ in range(2)],
+                "streams": [torch.cuda.Stream() for _ in range(3)]}
+        _STREAM_BUFS[key] = bufs
+    s_in, s_run, s_out = bufs["streams"]
+    main = torch.cuda.current_stream()
+    for s in (s_in, s_run, s_out):
+        s.wait_stream(main)
+    in_free = [None, None]   # vmult finished reading in[b]
+    out_free = [None, None]  # copy-out finished reading out[b]
+    lm = hier.matrices(level)
+    L = _native.lib()
+    es = u.element_size()
+    for i, z0 in enumerate(range(0, n, slab_cells)):
+        b = i & 1
+        z1 = min(n, z0 + slab_cells)
+        lo, hi = int(z0 > 0), int(z1 < n)
+        dbuf, obuf = bufs["in"][b], bufs["out"][b]
+        with torch.cuda.stream(s_in):
+            if in_free[b] is not None:
+                s_in.wait_event(in_free[b])
+            a0, a1 = (z0 - lo) * layer, (z1 + hi) * layer
+            dbuf[: a1 - a0].copy_(u[a0:a1], non_blocking=True)
+            loaded = torch.cuda.Event()
+            loaded.record(s_in)
+        s_run.wait_event(loaded)
+        if out_free[b] is not None:
+            s_run.wait_event(out_free[b])
+        base = dbuf.data_ptr()
+        loc = base + lo * layer * es                       # first dof of the slab itself
+        ghost_lo = base if lo else None                    # the K planes just below: dbuf's first layer
+        ghost_hi = loc + (z1 - z0) * layer * es if hi else None                 # K planes just above
+        grid = _native.SfGrid(n, n, z1 - z0, ghost_lo, ghost_hi)
+        rc = L.sf_vmult(mode.code, hier.degree, grid, _native.host_ptr(lm.cell_op), loc, obuf.data_ptr(), 1,
+                        s_run.cuda_stream)
+        _native.check(rc, "sf_vmult (streamed)")
+        done = torch.cuda.Event()
+        done.record(s_run)
+        in_free[b] = done
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done)
+            v[z0 * layer:z1 * layer].copy_(obuf[: (z1 - z0) * layer], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(s_out)
+            out_free[b] = copied
+    main.wait_stream(s_out)
+    s_out.synchronize()
+    return v
 
 
 def materialize_device(hier: MeshHierarchy, level: int, mode: PrecisionMode = PrecisionMode.FP64,

@@ -158,3 +158,30 @@ def test_q7_half_precision_tensor_core_vmult_band(lvl, mode):
     ref_err = rel_l2(port.apply_operator(H, lvl, u, mode.value), ref64)
     err = rel_l2(sf.apply_operator(sf.build_hierarchy(lvl, 7), lvl, u, mode), ref64)
     assert 0.25 * ref_err <= err <= 4.0 * ref_err, (err, ref_err)
+
+
+@pytest.mark.parametrize("mode", [P.FP64, P.FP16_EC])
+@pytest.mark.parametrize("slab_cells", [2, 4, 6])
+def test_streamed_host_vmult_matches_device(mode, slab_cells):
+    """apply_operator on host buffers streams z-slabs with ghost planes through the GPU."""
+    from paper_2407_09621_b200 import discretization as dz
+
+    k, lvl = 3, 4
+    hier = sf.build_hierarchy(lvl, k)
+    n = hier.n_dofs(lvl)
+    u = torch.randn(n, dtype=mode.torch_dtype).pin_memory()
+    v = torch.empty_like(u).pin_memory()
+    dz._stream_vmult(hier, lvl, u, v, mode, slab_cells=slab_cells)
+    ref = torch.empty(n, dtype=mode.torch_dtype, device="cuda")
+    dz.vmult_device(hier, lvl, u.cuda(), ref, mode)
+    assert torch.equal(v, ref.cpu()) or mode is not P.FP64
+    assert float((v - ref.cpu()).norm() / ref.norm().cpu()) <= (1e-15 if mode is P.FP64 else 1e-6)
+    # the public API takes this path for large host inputs
+    old = dz.STREAM_MIN_DOFS
+    dz.STREAM_MIN_DOFS = 1
+    try:
+        w = sf.apply_operator(hier, lvl, u.numpy(), mode)
+    finally:
+        dz.STREAM_MIN_DOFS = old
+    assert isinstance(w, np.ndarray) and w.dtype == mode.storage_dtype
+    assert np.abs(w - ref.cpu().numpy()).max() <= 1e-12 * float(ref.abs().max()) or mode is not P.FP64
