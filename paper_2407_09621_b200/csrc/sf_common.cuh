@@ -191,14 +191,18 @@ struct Geom {
   long long batch_stride;  // elements between batched vectors (blockIdx.y)
 };
 
-// Tile id -> tile coordinates in an L2-aware order: y is cut into bands of
-// kBandTiles/ntx rows; inside a band the order is x fastest, then y, then z.
-// A tile's z neighbours are then ~kBandTiles launches away (instead of
-// ntx*nty), so the neighbour cell layers its face traces read are still in
-// L2 (profiles/r01_vmult_fp64.md).
-constexpr int kBandTiles = 512;
+// Tile id -> tile coordinates in an L2-aware order: y is cut into bands of BAND/ntx tile
+// rows; inside a band the order is x fastest, then y, then z.  A tile's z neighbours are then
+// ~BAND launches away (instead of ntx*nty), so the neighbour cell layers its face traces read
+// are still in L2 (profiles/r01_vmult_fp64.md).  BAND = tiles in ~16 MiB of
+// fp64 data: 512 for Q7 (32 KiB tiles), 4096 for Q3.
+template <int K>
+constexpr int band_tiles() {
+  return (1 << 24) / (8 * K * K * K * 8) > 1 ? (1 << 24) / (8 * K * K * K * 8) : 1;
+}
+template <int K>
 __device__ __forceinline__ void tile_coords(const Geom& g, int id, int& tx, int& ty, int& tz) {
-  int by = kBandTiles / g.ntx;
+  int by = band_tiles<K>() / g.ntx;
   by = by < 1 ? 1 : (by > g.nty ? g.nty : by);
   const int per_band = g.ntx * by * g.ntz;
   const int band = id / per_band;

@@ -109,7 +109,7 @@ __device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0)
 __device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
   if (tile_id >= g.ntx * g.nty * g.ntz) return false;
   int tx, ty, tz;
-  tile_coords(g, tile_id, tx, ty, tz);
+  tile_coords<K>(g, tile_id, tx, ty, tz);
   T.cx = g.tx0 + 2 * tx;
   T.cy = g.ty0 + 2 * ty;
   T.cz = g.tz0 + 2 * tz;
@@ -147,7 +147,7 @@ __device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g,
 __device__ __forceinline__ void prefetch_tile_l2(const Geom& g, const double* __restrict__ u, int tile_id) {
   if (tile_id >= g.ntx * g.nty * g.ntz || threadIdx.x >= 256) return;
   int tx, ty, tz;
-  tile_coords(g, tile_id, tx, ty, tz);
+  tile_coords<K>(g, tile_id, tx, ty, tz);
   const long long sy = (long long)g.nx * K, sz = sy * (long long)g.ny * K;
   const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
   const double* p = u + (long long)((g.tz0 + 2 * tz) * K + z) * sz + (long long)((g.ty0 + 2 * ty) * K + y) * sy +

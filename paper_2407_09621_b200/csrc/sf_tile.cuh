@@ -134,7 +134,7 @@ struct TileEngine {
     int id = tile0 + t;
     if (id >= ntiles_total) return false;
     int tx, ty, tz;
-    tile_coords(g, id, tx, ty, tz);
+    tile_coords<K>(g, id, tx, ty, tz);
     cx = g.tx0 + 2 * tx;
     cy = g.ty0 + 2 * ty;
     cz = g.tz0 + 2 * tz;

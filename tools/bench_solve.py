@@ -50,7 +50,8 @@ if __name__ == "__main__":
     ap.add_argument("--degree", type=int, default=7)
     ap.add_argument("--level", type=int, default=6)
     ap.add_argument("--modes", default="fp64,fp16_ec,fp16")
+    ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
     hier = sf.build_hierarchy(a.level, a.degree, max_dofs=2**34)
     for m in a.modes.split(","):
-        print(json.dumps(solve_once(hier, a.level, sf.PrecisionMode.parse(m))), flush=True)
+        print(json.dumps(solve_once(hier, a.level, sf.PrecisionMode.parse(m), reps=a.reps)), flush=True)
