@@ -12,4 +12,4 @@ from .discretization import (MeshHierarchy, build_hierarchy, apply_operator, mat
 from .multigrid import (MultigridPreconditioner, VCycleConfig, PatchSolver, default_ordering,  # noqa: F401
                         restrict, prolongate, patch_inverse_apply)
 from .krylov import fgmres, gmres, SolveReport  # noqa: F401
-from .experiments import run_solve  # noqa: F401
+from .experiments import run_solve, convergence_study, error_profile  # noqa: F401

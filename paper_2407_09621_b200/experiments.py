@@ -55,3 +55,44 @@ def run_solve(degree: int, level: int, mode: PrecisionMode = PrecisionMode.FP64,
     report.h1_error = h1_seminorm_error(hier, level, x, prob.gradient)
     return SolveOutcome(degree=degree, level=level, mode=mode, solver=solver, dofs=hier.n_dofs(level),
                         report=report, l2=report.l2_error, h1=report.h1_error, x=x if keep_solution else None)
+
+
+def convergence_study(degree: int, max_level: int, solver: str = "fgmres", tol: float = 1e-8,
+                      maxit: int = 100) -> list[dict]:
+    """Per-level errors and observed orders for the manufactured problem (experiments.py:106-127)."""
+    import numpy as np
+
+    hier = build_hierarchy(max_level, degree)
+    rows = []
+    prev_l2 = None
+    for level in hier.levels():
+        out = run_solve(degree, level, solver=solver, tol=tol, maxit=maxit, hier=hier)
+        rate = float(np.log2(prev_l2 / out.l2)) if prev_l2 else None
+        rows.append({"level": level, "h": hier.h(level), "dofs": out.dofs, "l2_error": out.l2,
+                     "h1_error": out.h1, "rate": rate, "iterations": out.report.iterations})
+        prev_l2 = out.l2
+    return rows
+
+
+def error_profile(degree: int, max_level: int, modes, seed: int = 0) -> list[dict]:
+    """Relative error of one operator apply against fp64, per size and mode (experiments.py:130-148).
+
+    Same seeded inputs as the reference (one standard-normal draw per level, in level order);
+    every apply runs on the device.
+    """
+    import numpy as np
+
+    from .discretization import apply_operator
+    from .precision import relative_error
+
+    hier = build_hierarchy(max_level, degree)
+    rng = np.random.default_rng(seed)
+    rows = []
+    for level in hier.levels():
+        u = rng.standard_normal(hier.n_dofs(level))
+        ref = apply_operator(hier, level, u, PrecisionMode.FP64)
+        for mode in modes:
+            out = apply_operator(hier, level, u, mode)
+            rows.append({"dofs": hier.n_dofs(level), "level": level, "mode": mode.value,
+                         "relative_error": relative_error(out, ref)})
+    return rows

@@ -139,6 +139,24 @@ def half():
     save("half", x=x, demoted=demote16(x))
 
 
+def error_profiles():
+    """Reference experiments.error_profile(7, 4, (fp32, fp16, fp16_ec), seed=0) -> JSON rows
+    (acceptance criterion 9 inputs, tests/test_gpu_acceptance.py)."""
+    import json
+
+    from sumfact.experiments import error_profile
+
+    rows = error_profile(7, 4, (PrecisionMode.FP32, PrecisionMode.FP16, PrecisionMode.FP16_EC), seed=0)
+    path = os.path.join(OUT, "error_profile_k7_l4.json")
+    with open(path, "w") as fh:
+        json.dump(rows, fh, indent=0)
+    print(f"wrote {path}", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    globals()[sys.argv[1]]()
+    sys.exit(0)
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     print("reference sumfact", sumfact.__version__, "compiled core:", sumfact.HAVE_COMPILED)
