@@ -85,18 +85,19 @@ struct Tables8 {
 
 __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __restrict__ u, double* __restrict__ v,
                                                             Geom g, LevelOp<K, MODE_FP64> op,
-                                                            const Tables8* __restrict__ tab, int prefetch) {
+                                                            const Tables8* __restrict__ tab, Band bd, int prefetch) {
   extern __shared__ __align__(128) double smem[];
-  u += (long long)blockIdx.y * g.batch_stride;
-  v += (long long)blockIdx.y * g.batch_stride;
   Tile T;
-  if (!tile_setup(T, smem, g, blockIdx.x)) return;
-  if (prefetch) prefetch_tile_l2(g, u, blockIdx.x + prefetch);
+  int batch;
+  if (!tile_setup_band(T, smem, g, bd, batch)) return;
+  u += (long long)batch * g.batch_stride;
+  v += (long long)batch * g.batch_stride;
+  if (prefetch) prefetch_ahead_l2(g, bd, T, u);
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
   T.sLf = &tab->L[0][0][0];  // per-lane fragments from the L1-cached device table (coalesced)
-  prologue_xs(T, g, op, u, f);
+  prologue_fast(T, g, op, u, f);
   xy_stages(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
@@ -223,15 +224,16 @@ __device__ __forceinline__ void full_group(const double (*l)[4], const double* a
 __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __restrict__ xo,
                                                              const double* __restrict__ b, double* __restrict__ xn,
                                                              Geom g, LevelOp<K, MODE_FP64> op,
-                                                             const Tables8* __restrict__ tab) {
+                                                             const Tables8* __restrict__ tab, Band bd) {
   extern __shared__ __align__(128) double smem[];
   Tile T;
-  if (!tile_setup(T, smem, g, blockIdx.x)) return;
+  int batch;
+  if (!tile_setup_band(T, smem, g, bd, batch)) return;
   T.sLf = &tab->L[0][0][0];
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue_xs(T, g, op, xo, f);
+  prologue_fast(T, g, op, xo, f);
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -429,15 +431,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
                                                                      double* __restrict__ coarse, Geom g,
                                                                      LevelOp<K, MODE_FP64> op,
                                                                      const Tables8* __restrict__ tab,
-                                                                     const PTab8* __restrict__ pt) {
+                                                                     const PTab8* __restrict__ pt, Band bd) {
   extern __shared__ __align__(128) double smem[];
   Tile T;
-  if (!tile_setup(T, smem, g, blockIdx.x)) return;
+  int batch;
+  if (!tile_setup_band(T, smem, g, bd, batch)) return;
   T.sLf = &tab->L[0][0][0];
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue_xs(T, g, op, x, f);
+  prologue_fast(T, g, op, x, f);
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -566,9 +569,15 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
 
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
   if (err != cudaSuccess) return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  kern<<<dim3(tiles, batch), dm::kThreads, dm::kSmemTile, st>>>((const double*)u, (double*)v, g, op,
-                                                                              tab, pf);
+  const dm::Band bd = dm::make_band(g);
+  // grid z = (z, band) x batch; split very large batches across launches (gridDim.z <= 65535)
+  const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
+  for (int b0 = 0; b0 < batch; b0 += per) {
+    const int nb = batch - b0 < per ? batch - b0 : per;
+    const double* ub = (const double*)u + (long long)b0 * g.batch_stride;
+    double* vb = (double*)v + (long long)b0 * g.batch_stride;
+    kern<<<dim3(g.ntx, bd.by, bd.zb * nb), dm::kThreads, dm::kSmemTile, st>>>(ub, vb, g, op, tab, bd, pf);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -583,9 +592,9 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
   cudaError_t err =
       cudaFuncSetAttribute(dm::k_colour_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
   if (err != cudaSuccess) return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  dm::k_colour_dmma8<<<tiles, dm::kThreads, dm::kSmemTile, st>>>((const double*)xo, (const double*)b, (double*)xn, g,
-                                                                  op, tab);
+  const dm::Band bd = dm::make_band(g);
+  dm::k_colour_dmma8<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
+      (const double*)xo, (const double*)b, (double*)xn, g, op, tab, bd);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 }  // namespace sf
@@ -602,9 +611,9 @@ int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* 
   if (cudaFuncSetAttribute(dm::k_resid_restrict_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)dm::kSmemTile) != cudaSuccess)
     return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  dm::k_resid_restrict_dmma8<<<tiles, dm::kThreads, dm::kSmemTile, st>>>((const double*)x, (const double*)b,
-                                                                          (double*)coarse, g, op, tab, pt);
+  const dm::Band bd = dm::make_band(g);
+  dm::k_resid_restrict_dmma8<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
+      (const double*)x, (const double*)b, (double*)coarse, g, op, tab, pt, bd);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 }  // namespace sf

@@ -95,6 +95,7 @@ struct Tile {
   unsigned nbm;             // bit 2*axis+hi: face neighbour present (inside the array or ghost)
   int kind[3];
   int r, k4, c2, lane, warp;
+  int b0;  // banded launch: first tile row of the band
 };
 
 // 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary
@@ -106,10 +107,44 @@ __device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0)
   return 1;
 }
 
+// Banded 3-D launch (replaces per-thread integer divisions of a linear tile id): grid =
+// (ntx, band rows `by`, ntz * nbands [* batch]); launch order x, y-in-band, z, band -- the
+// L2-aware order of tile_coords<K>.  Returns false for the idle CTAs of a partial last band.
+struct Band {
+  int by, zb;  // tile rows per band; ntz * nbands (z extent of one batch vector)
+};
+__host__ __forceinline__ Band make_band(const Geom& g) {
+  int by = band_tiles<K>() / g.ntx;
+  by = by < 1 ? 1 : (by > g.nty ? g.nty : by);
+  const int nb = (g.nty + by - 1) / by;
+  return Band{by, g.ntz * nb};
+}
+__device__ __forceinline__ bool band_tile(const Geom& g, const Band& bd, int& tx, int& ty, int& tz, int& batch) {
+  int zz = blockIdx.z;
+  batch = 0;
+  if (gridDim.z > (unsigned)bd.zb) {
+    batch = zz / bd.zb;
+    zz -= batch * bd.zb;
+  }
+  const int band = zz / g.ntz;
+  tz = zz - band * g.ntz;
+  ty = band * bd.by + blockIdx.y;
+  tx = blockIdx.x;
+  return ty < g.nty;
+}
+
+__device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id);
+__device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz);
+
 __device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
   if (tile_id >= g.ntx * g.nty * g.ntz) return false;
   int tx, ty, tz;
   tile_coords<K>(g, tile_id, tx, ty, tz);
+  tile_fields(T, g, tx, ty, tz);
+  return true;
+}
+
+__device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz) {
   T.cx = g.tx0 + 2 * tx;
   T.cy = g.ty0 + 2 * ty;
   T.cz = g.tz0 + 2 * tz;
@@ -131,7 +166,37 @@ __device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
   T.r = T.lane >> 2;
   T.k4 = T.lane & 3;
   T.c2 = 2 * T.k4;
+}
+
+// banded-grid variant of tile_setup; `batch` = vector index of a batched launch
+__device__ __forceinline__ bool tile_setup_band(Tile& T, double* smem, const Geom& g, const Band& bd, int& batch) {
+  T.sU = smem;
+  T.sB = smem + VOL;
+  T.tr = T.sB + VOL;
+  T.sLf = T.tr + 12 * TRP;
+  int tx, ty, tz;
+  if (!band_tile(g, bd, tx, ty, tz, batch)) return false;
+  tile_fields(T, g, tx, ty, tz);
+  T.b0 = ty - blockIdx.y;  // first tile row of this band
   return true;
+}
+
+// L2 prefetch of the u rows of the tile two rows ahead in launch order (~2 ntx CTAs later):
+// (tx, ty + 2) inside the band, else the wrapped row of the next z layer.
+__device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd, const Tile& T,
+                                                  const double* __restrict__ u) {
+  const int ty = (T.cy - g.ty0) >> 1, tz = (T.cz - g.tz0) >> 1;
+  const int b0 = T.b0;
+  const int bh = min(bd.by, g.nty - b0);
+  int ny = ty + 2, nz = tz;
+  if (ny >= b0 + bh) {
+    ny -= bh;
+    if (++nz >= g.ntz) return;
+  }
+  if (ny < b0 || threadIdx.x >= 256) return;
+  const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
+  const double* p = u + (long long)((g.tz0 + 2 * nz) * K + z) * T.sz + (long long)((g.ty0 + 2 * ny) * K + y) * T.sy + T.cx * K;
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 __device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g, int tile_id) {
@@ -659,6 +724,110 @@ __device__ __forceinline__ void prologue_xs(Tile& T, const Geom& g, const OpT& o
     double* pl = T.tr + hi * 2 * TRP;
     pl[p * TRW + q] = alpha;
     pl[TRP + p * TRW + q] = beta;
+  }
+  plane_mass_rows(T, f, 4);
+  plane_mass_rows(T, f, 8);
+  __syncthreads();  // also: staged layers consumed before the x stage writes B
+  plane_mass_cols(T, f);
+  __syncthreads();
+}
+
+// prologue_xs with the address arithmetic strength-reduced: every thread's cp.async chunks and
+// trace items share one (x, y) position and step only in z (or along the face normal), so each
+// source/destination is one pointer plus a constant stride instead of a fresh 64-bit
+// index computation per element (the prologue was half of the kernel's instructions).
+template <class OpT>
+__device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+                                              const Frags& f) {
+  const int tid = threadIdx.x;
+  const long long sy = T.sy, sz = T.sz;
+  const long long txy = (long long)(T.cy * K) * sy + T.cx * K;  // tile origin within a z plane
+  const double* ub = u + (long long)(T.cz * K) * sz + txy;
+  {  // tile: chunk (x2 = tid & 7, y = (tid >> 3) & 15, z = (tid >> 7) + 2i)
+    const int x2 = tid & 7, y = (tid >> 3) & 15, z0 = tid >> 7;
+    const double* src = ub + z0 * sz + y * sy + 2 * x2;
+    double* dst = &T.sU[idxU(z0, y, 2 * x2)];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cp_async16(dst + i * 512, src + 2 * i * sz);
+  }
+  {  // x-neighbour layers: chunk ch = tid & 3 of row (hi, z = (tid >> 6) + 4k, y = (tid >> 2) & 15)
+    const int ch = tid & 3, y = (tid >> 2) & 15, zb = tid >> 6;
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      if (!((T.nbm >> hi) & 1)) continue;
+      const double* src = ub + zb * sz + y * sy + (hi ? B : -K) + 2 * ch;
+      double* dst = &T.sB[xs_idx((hi * 16 + zb) * 16 + y, ch)];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cp_async16(dst + k * 512, src + 4 * k * sz);
+    }
+  }
+  // y and z faces: item (hi = j, p = (tid >> 4) & 15, q = tid & 15); K values along the normal
+  const int p = (tid >> 4) & 15, q = tid & 15;
+  double w1[2][K], w2[2][K];
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+    if ((T.nbm >> (2 + hi)) & 1) {  // y faces: Z = p, X = q, Y = hi ? 16 : -8
+      const double* b1 = ub + p * sz + q + (hi ? B : -K) * sy;
+#pragma unroll
+      for (int c = 0; c < K; ++c) w1[hi][c] = __ldg(b1 + c * sy);
+    }
+    if ((T.nbm >> (4 + hi)) & 1) {  // z faces: Y = p, X = q, Z = hi ? 16 : -8 (ghost planes past the slab)
+      const double* b2;
+      const bool inside = hi ? (T.cz + 2 < g.nz) : (T.cz > 0);
+      if (inside) b2 = ub + (hi ? B : -K) * sz + p * sy + q;
+      else b2 = reinterpret_cast<const double*>(hi ? g.ghost_hi : g.ghost_lo) + txy + p * sy + q;
+#pragma unroll
+      for (int c = 0; c < K; ++c) w2[hi][c] = __ldg(b2 + c * sz);
+    }
+  }
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+#pragma unroll
+    for (int axis = 1; axis < 3; ++axis) {
+      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
+      const double* w = axis == 1 ? w1[hi] : w2[hi];
+      double alpha, beta = 0.0;
+      if (hi) {
+        alpha = w[0];
+#pragma unroll
+        for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[c], beta);
+      } else {
+        alpha = w[K - 1];
+#pragma unroll
+        for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
+      }
+      double* pl = T.tr + (2 * axis + hi) * 2 * TRP + p * TRW + q;
+      pl[0] = alpha;
+      pl[TRP] = beta;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // x traces from the staged layers: item (hi, p = z, q = y) -> one staged row
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+    if (!((T.nbm >> hi) & 1)) continue;
+    const int row = (hi * 16 + p) * 16 + q;
+    double w[K];
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx(row, ch)]);
+      w[2 * ch] = v2.x;
+      w[2 * ch + 1] = v2.y;
+    }
+    double alpha, beta = 0.0;
+    if (hi) {
+      alpha = w[0];
+#pragma unroll
+      for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[c], beta);
+    } else {
+      alpha = w[K - 1];
+#pragma unroll
+      for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
+    }
+    double* pl = T.tr + hi * 2 * TRP + p * TRW + q;
+    pl[0] = alpha;
+    pl[TRP] = beta;
   }
   plane_mass_rows(T, f, 4);
   plane_mass_rows(T, f, 8);
