@@ -11,6 +11,10 @@
 
 namespace sf {
 namespace dm {
+// prologue_fast addresses with 32-bit element offsets: 24 planes of the local array must fit
+static bool offsets32(const Geom& g) {
+  return 24LL * g.nx * g.ny * K * K < 2147483647LL;
+}
 
 struct PatchL {
   double L[4][B][B];  // L_smooth[kind], kind = 2*left_bnd + right_bnd
@@ -539,6 +543,7 @@ static const PTab8* ptables8(const double* embd) {
 }  // namespace dm
 
 int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+  if (!dm::offsets32(g)) return kUseGeneric;
   static_assert(dm::kSmemTile <= 113 * 1024, "two CTAs per SM");
   auto op = dm::pack_op64(opd);
   static const double zero_eig[4 * 256 + 4 * 16] = {0};
@@ -586,6 +591,7 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
 namespace sf {
 int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
                         cudaStream_t st) {
+  if (!dm::offsets32(g)) return kUseGeneric;
   const dm::Tables8* tab = dm::tables8(opd, eigd);
   if (!tab) return -3;
   auto op = dm::pack_op64(opd);
@@ -602,6 +608,7 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
 namespace sf {
 int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
                                 void* coarse, cudaStream_t st) {
+  if (!dm::offsets32(g)) return kUseGeneric;
   // L fragments come from the level tables (built without eigenvectors here)
   static const double zero_eig[4 * 256 + 4 * 16] = {0};
   const dm::Tables8* tab = dm::tables8(opd, zero_eig);

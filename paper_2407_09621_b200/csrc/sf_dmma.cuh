@@ -740,7 +740,8 @@ template <class OpT>
 __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
                                               const Frags& f) {
   const int tid = threadIdx.x;
-  const long long sy = T.sy, sz = T.sz;
+  // 32-bit element strides (host guarantees 24 * sz < 2^31): one IMAD.WIDE per address
+  const int sy = (int)T.sy, sz = (int)T.sz;
   const long long txy = (long long)(T.cy * K) * sy + T.cx * K;  // tile origin within a z plane
   const double* ub = u + (long long)(T.cz * K) * sz + txy;
   {  // tile: chunk (x2 = tid & 7, y = (tid >> 3) & 15, z = (tid >> 7) + 2i)

@@ -623,8 +623,11 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
   if (rc) return rc;
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (!use_generic()) {
-      if (launch_vmult_dmma8(g, opd, u, v, batch, st)) return check_launch("sf_vmult (dmma)");
-      return SF_OK;
+      const int r = launch_vmult_dmma8(g, opd, u, v, batch, st);
+      if (r != kUseGeneric) {  // (declined: local array too large for 32-bit tile offsets)
+        if (r) return check_launch("sf_vmult (dmma)");
+        return SF_OK;
+      }
     }
   }
   if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
@@ -667,8 +670,11 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
   bool done = false;
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (!use_generic()) {
-      if (launch_colour_dmma8(g, opd, eigd, xo, b, xn, st)) return check_launch("sf_smooth_colour (dmma)");
-      done = true;
+      const int r = launch_colour_dmma8(g, opd, eigd, xo, b, xn, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_smooth_colour (dmma)");
+        done = true;
+      }
     }
   }
   if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
@@ -708,8 +714,11 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
   }
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (with_op && !use_generic()) {
-      if (launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st)) return check_launch("sf_residual_restrict (dmma)");
-      return SF_OK;
+      const int r = launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_residual_restrict (dmma)");
+        return SF_OK;
+      }
     }
   }
   if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
