@@ -88,6 +88,15 @@ int sf_prolongate_add(int mode, int k, const sf_grid* coarse_grid, const double*
 int sf_patch_apply(int mode, int k, long long count, const int* kinds, const double* patch_eig, const void* in,
                    void* out, void* stream);
 
+/* out[o, i, r] = sum_k m[i, k] u[o, k, r] on device arrays u (outer, n, inner), m (rows, n),
+ * out (outer, rows, inner): double for mode 0, float otherwise; ascending k with one rounded
+ * multiply and add per term (bitwise contract_f8 / contract_f4), modes applied per operand as
+ * contract_mode does.
+ * Replaces contract_batch -> _impl.contract_f8 / contract_f4   _core/__init__.py:27-59,
+ *          contract_mode                                      precision.py:206-230. */
+int sf_contract(int mode, long long outer, int n, long long inner, int rows, const void* m, const void* u, void* out,
+                void* stream);
+
 /* ---- vector kernels for FGMRES and the V-cycle boundary (krylov.py:49-137, multigrid.py:262-266) ---- */
 
 /* out = (dtype_out) in, dtype 0 = double, 1 = float.  Replaces np.asarray(x, dtype=...). */

@@ -7,6 +7,7 @@ run_solve).  All compute runs in libsumfact_b200.so; there is no CPU fallback.
 __version__ = "0.1.0"
 
 from .precision import PrecisionMode, relative_error  # noqa: F401
+from .core import contract_batch, contract_mode  # noqa: F401
 from .discretization import (MeshHierarchy, build_hierarchy, apply_operator, materialize_operator,  # noqa: F401
                              assemble_rhs, interpolate, l2_error, h1_seminorm_error, sine_product_problem)
 from .multigrid import (MultigridPreconditioner, VCycleConfig, PatchSolver, default_ordering,  # noqa: F401

@@ -57,6 +57,8 @@ def lib():
             "sf_axpy_dev": ([c_ll, c_d, c_p, c_p, c_p, c_p], c_i),
             "sf_axpby": ([c_ll, c_d, c_p, c_d, c_p, c_p], c_i),
             "sf_axpby_f32": ([c_ll, c_f, c_p, c_f, c_p, c_p], c_i),
+            "sf_contract": ([c_i, c_ll, c_i, c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
+            "sf_contract_last_error": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -69,14 +71,16 @@ def lib():
 
 
 EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_smooth_colour", "sf_residual_restrict",
-            "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32")
+            "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
+            "sf_contract")
 
 
 def check(rc: int, what: str):
     if rc == SF_OK:
         return
     L = lib()
-    msg = (L.sf_last_error() or b"").decode() or (L.sf_vec_last_error() or b"").decode()
+    msg = ((L.sf_last_error() or b"").decode() or (L.sf_vec_last_error() or b"").decode()
+           or (L.sf_contract_last_error() or b"").decode())
     if rc == SF_EINVAL:
         raise ValueError(f"{what}: {msg}")
     if rc == SF_EUNSUPPORTED:
