@@ -393,9 +393,9 @@ __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h
       for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU(z, y, 4 * kc + T.k4)];
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
+      h.apply(T, rb[g8], 0, z * TRW + y);  // halo first: the DFMAs need no DMMA result
       mass_group(f, a, ra[g8]);
       stiff_group(f, a, rb[g8]);
-      h.apply(T, rb[g8], 0, z * TRW + y);
     }
     __syncwarp();
 #pragma unroll
@@ -421,9 +421,9 @@ __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h
       }
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
+      h.apply(T, rb[g8], 1, z * TRW + x);  // (y halo)
       mass_group(f, a, ra[g8]);   // c = My a
       stiff_group(f, a, rb[g8]);  // d = Ly a
-      h.apply(T, rb[g8], 1, z * TRW + x);
       mass_group(f, b, rb[g8]);   // dd = d + My b
     }
     __syncwarp();
@@ -454,8 +454,8 @@ __device__ __forceinline__ void z_group(const Tile& T, const Frags& f, const Hal
     dd[kc] = T.sB[idxC(4 * kc + T.k4, y, x)];
   }
   acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+  h.apply(T, acc, 2, y * TRW + x);  // (z halo)
   stiff_group(f, cc, acc);
-  h.apply(T, acc, 2, y * TRW + x);
   mass_group(f, dd, acc);
 }
 
