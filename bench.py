@@ -176,9 +176,16 @@ def main():
     from paper_2407_09621_b200.discretization import vmult_device
 
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # SUMFACT_B200_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the N>1 path on a 1-GPU box)
+    shared = os.environ.get("SUMFACT_B200_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     k, lvl = args.degree, args.level
     K = k + 1
     hier = sf.build_hierarchy(lvl, k, max_dofs=2**34, min_level=lvl)
@@ -189,17 +196,29 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     u = torch.randn(D, dtype=torch.float64, device="cuda", generator=gen)
     v = torch.empty_like(u)
+    kernel_events = []  # (start, end) CUDA events around the vmult kernel of every timed step
     if world > 1:
         from paper_2407_09621_b200 import slab
 
-        op = slab.DistributedOperator.weak(hier, lvl, slab.SlabComm())  # NCCL K-plane halo + ghosted vmult
+        comm = slab.SlabComm()
+        op = slab.DistributedOperator.weak(hier, lvl, comm)  # NCCL K-plane halo + ghosted vmult
+        glo, ghi = op.ghosts(torch.float64)
+        grid = _native.SfGrid(n, n, n, glo.data_ptr() if comm.lo is not None else None,
+                              ghi.data_ptr() if comm.hi is not None else None)
 
-        def step():
-            op.apply(u, v, P.FP64)
+        def step(timed=False):
+            slab.exchange_face_planes(comm, op.slab, u, glo, ghi)
+            if timed:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
+            if timed:
+                ev[1].record()
+                kernel_events.append(ev)
     else:
         grid = hier.grid(lvl)
 
-        def step():
+        def step(timed=False):
             vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
 
     for _ in range(max(args.warmup, 3)):
@@ -215,7 +234,7 @@ def main():
         dist.barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        step(timed=True)
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -224,21 +243,33 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if shared:
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * D / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant (only) kernel in the step: executed-flop model vs measured FP64 peak
+    # roofline of the dominant kernel (the vmult; the only one of ours in the step): executed DMMA-schedule
+    # flops per launch over its average launch time (CUDA events on its stream; max over ranks)
+    kms = ms
+    if kernel_events:
+        kms = sum(a.elapsed_time(b) for a, b in kernel_events) / len(kernel_events)
+        t = torch.tensor([kms], dtype=torch.float64)
+        if not shared:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kms = float(t.item())
     kflops = kernel_flops_per_dof(k) * D
-    achieved_tf = kflops / (ms * 1e-3) / 1e12 if world == 1 else None
+    achieved_tf = kflops / (kms * 1e-3) / 1e12
     hbm, hbm_src = peaks()
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None, "traffic": None,
-                "kernel": "k_vmult<8,0>" if k == 7 else f"k_vmult<{K},0>",
+                "kernel": "sf::dm::k_vmult_dmma8" if k == 7 else f"sf::k_vmult<{K},0>",
+                "kernel_ms": kms,
                 "flops_per_dof": kernel_flops_per_dof(k),
                 "peak_source": "measured DMMA microbenchmark (profiles/r01_microbench_fp64.md)",
-                "hbm": {"achieved": 16 * D / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                        "frac": 16 * D / (ms * 1e-3) / 1e9 / hbm, "peak_source": hbm_src}}
+                "hbm": {"achieved": 16 * D / (kms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": 16 * D / (kms * 1e-3) / 1e9 / hbm, "peak_source": hbm_src}}
     traffic = os.path.join(ROOT, "profiles", "vmult_traffic.json")
     if os.path.exists(traffic):
         try:
@@ -253,28 +284,48 @@ def main():
                                   f"({world * D} DoF; {D} per GPU)",
                       "degree": k, "level": lvl, "dofs_per_gpu": D,
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                      "l2_flush": "not needed: u, v = 2 x 8.6 GB >> 126 MB L2"},
+                      "l2_flush": f"not needed: u, v = 2 x {8 * D / 1e9:.2f} GB per GPU >> 126 MB L2"},
            "tflops_reference_equivalent": value * 1e9 * ref_flops_per_dof(k, lvl) / 1e12,
            "roofline": roofline, "clocks": clk, "gpu_launches": args.steps}
 
-    if rank == 0 and world == 1:
-        # e2e: public API with pinned host buffers, H2D + D2H per step
-        try:
-            uh = torch.empty(D, dtype=torch.float64, pin_memory=True)
-            uh.copy_(u)
-            vh = torch.empty(D, dtype=torch.float64, pin_memory=True)
-            sf.apply_operator(hier, lvl, uh, out=vh)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for _ in range(args.e2e_steps):
+    # e2e: the public API with pinned HOST buffers, H2D + D2H inside the timed region, every step
+    try:
+        uh = torch.empty(D, dtype=torch.float64, pin_memory=True)
+        uh.copy_(u)
+        vh = torch.empty(D, dtype=torch.float64, pin_memory=True)
+        if world == 1:
+            api = "paper_2407_09621_b200.apply_operator(pinned host; z-slabs streamed)"
+
+            def e2e_step():
                 sf.apply_operator(hier, lvl, uh, out=vh)
-            torch.cuda.synchronize()
-            dt = (time.perf_counter() - t0) / args.e2e_steps
-            out["e2e"] = {"value": D / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * D,
-                          "d2h_bytes_per_step": 8 * D, "api": "paper_2407_09621_b200.apply_operator(pinned host)"}
-            del uh, vh
-        except Exception as exc:  # pinned allocation can fail on small hosts
-            out["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
+        else:
+            api = "slab.DistributedOperator.apply (per-rank pinned host slab -> HBM -> halo + vmult -> host)"
+
+            def e2e_step():
+                u.copy_(uh, non_blocking=True)
+                op.apply(u, v, P.FP64)
+                vh.copy_(v, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64)
+            if not shared:
+                t = t.cuda()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        out["e2e"] = {"value": world * D / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * D * world,
+                      "d2h_bytes_per_step": 8 * D * world, "api": api}
+        del uh, vh
+    except Exception as exc:  # pinned allocation can fail on small hosts
+        out["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
+    if rank == 0 and world == 1:
         if not args.no_cpu:
             out["cpu_baseline"] = {kk: vv for kk, vv in cpu_baseline().items() if kk != "seconds_per_vmult"}
         if not args.no_extras:
