@@ -454,29 +454,66 @@ def assemble_rhs_separable(hier: MeshHierarchy, level: int, f1, scale: float = 1
     return (scale * b1[:, None, None] * b1[None, :, None] * b1[None, None, :]).reshape(-1).contiguous()
 
 
-def l2_error_separable(hier: MeshHierarchy, level: int, u_h: torch.Tensor, e1, scale: float = 1.0,
-                       slab_cells: int = 8) -> float:
-    """L2 distance between u_h (device) and scale * e1(x) e1(y) e1(z), k+3-point Gauss quadrature."""
-    from .basis import gauss_rule, lagrange_values
+def _separable_error_sq(hier, level, u_h, mats, factors, slab_cells=8):
+    """sum_q w_q (I u_h - scale * f_z f_y f_x)^2 over k+3-point Gauss points, slab by slab on the device.
+
+    mats[a]: (q, K) evaluation matrix along tensor axis a (values or derivatives);
+    factors[a]: the exact 1-D factor along axis a at the n*q points (scale folded into axis 0).
+    """
+    from .basis import gauss_rule
 
     n, h, K = hier.n_cells(level), hier.h(level), hier.degree + 1
     rule = gauss_rule(hier.degree + 3)
     q = len(rule.points)
-    S = torch.from_numpy(lagrange_values(hier.basis.nodes, rule.points)).cuda()  # (q, K)
-    pts = (np.arange(n)[:, None] + rule.points[None, :]) * h
-    w1 = torch.from_numpy(np.tile(rule.weights, n) * h).cuda()  # (n*q,)
-    ex = torch.from_numpy(e1(pts).reshape(-1)).cuda()            # (n*q,)
+    Sx, Sy, Sz = (torch.from_numpy(np.ascontiguousarray(m)).cuda() for m in mats)
+    fx, fy, fz = (torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).cuda() for f in factors)
+    w1 = torch.from_numpy(np.tile(rule.weights, n) * h).cuda()
     U = u_h.reshape(n, K, n, K, n, K)
     total = torch.zeros((), dtype=torch.float64, device="cuda")
     for z0 in range(0, n, slab_cells):
         blk = U[z0:z0 + slab_cells]
-        t = torch.einsum("qk,zkylxm->zqylxm", S, blk)
-        t = torch.einsum("qk,zaykxm->zayqxm", S, t)
-        t = torch.einsum("qk,zaybxk->zaybxq", S, t)
+        t = torch.einsum("qk,zkylxm->zqylxm", Sz, blk)
+        t = torch.einsum("qk,zaykxm->zayqxm", Sy, t)
+        t = torch.einsum("qk,zaybxk->zaybxq", Sx, t)
         nz = blk.shape[0]
         t = t.reshape(nz * q, n * q, n * q)
         zi = slice(z0 * q, (z0 + nz) * q)
-        exact = scale * ex[zi][:, None, None] * ex[None, :, None] * ex[None, None, :]
+        exact = fz[zi][:, None, None] * fy[None, :, None] * fx[None, None, :]
         W = w1[zi][:, None, None] * w1[None, :, None] * w1[None, None, :]
         total += (W * (t - exact) ** 2).sum()
+    return total
+
+
+def l2_error_separable(hier: MeshHierarchy, level: int, u_h: torch.Tensor, e1, scale: float = 1.0,
+                       slab_cells: int = 8) -> float:
+    """L2 distance between u_h (device) and scale * e1(x) e1(y) e1(z), k+3-point Gauss quadrature
+    (the reference's l2_error, discretization.py:431-441, for separable exact solutions)."""
+    from .basis import gauss_rule, lagrange_values
+
+    n, h = hier.n_cells(level), hier.h(level)
+    rule = gauss_rule(hier.degree + 3)
+    S = lagrange_values(hier.basis.nodes, rule.points)
+    pts = (np.arange(n)[:, None] + rule.points[None, :]) * h
+    f = e1(pts)
+    total = _separable_error_sq(hier, level, u_h, (S, S, S), (f, f, scale * f), slab_cells)
+    return float(torch.sqrt(total))
+
+
+def h1_seminorm_error_separable(hier: MeshHierarchy, level: int, u_h: torch.Tensor, e1, de1, scale: float = 1.0,
+                                slab_cells: int = 8) -> float:
+    """H1-seminorm distance to scale * e1 e1 e1 with d/dx e1 = de1 (discretization.py:444-459), on the device."""
+    from .basis import gauss_rule, lagrange_derivatives, lagrange_values
+
+    n, h = hier.n_cells(level), hier.h(level)
+    rule = gauss_rule(hier.degree + 3)
+    S = lagrange_values(hier.basis.nodes, rule.points)
+    Dm = lagrange_derivatives(hier.basis.nodes, rule.points) / h
+    pts = (np.arange(n)[:, None] + rule.points[None, :]) * h
+    f, df = e1(pts), de1(pts)
+    total = torch.zeros((), dtype=torch.float64, device="cuda")
+    for a in range(3):
+        mats = tuple(Dm if b == a else S for b in range(3))
+        facs = [df if b == a else f for b in range(3)]
+        facs[2] = scale * facs[2]
+        total += _separable_error_sq(hier, level, u_h, mats, facs, slab_cells)
     return float(torch.sqrt(total))

@@ -44,15 +44,24 @@ def run_solve(degree: int, level: int, mode: PrecisionMode = PrecisionMode.FP64,
     """
     if solver not in ("fgmres", "gmres"):
         raise ValueError(f"unknown solver {solver!r}")
+    import math
+
+    import numpy as np
+
+    from .discretization import assemble_rhs_separable, h1_seminorm_error_separable, l2_error_separable
+
     hier = hier or build_hierarchy(level, degree)
-    prob = sine_product_problem(hier.dim)
-    b = torch.from_numpy(assemble_rhs(hier, level, prob.rhs)).cuda()
+    sine_product_problem(hier.dim)  # the manufactured problem of the reference (discretization.py:504-531)
+    # its data are separable products of sin(pi x): load vector and error norms stay on the device
+    sine = lambda x: np.sin(np.pi * x)
+    dsine = lambda x: np.pi * np.cos(np.pi * x)
+    b = assemble_rhs_separable(hier, level, sine, 3.0 * math.pi**2)
     mg = MultigridPreconditioner(hier, VCycleConfig(pre_smooth_steps=pre_smooth, post_smooth_steps=post_smooth,
                                                     coarse_level=coarse_level, mode=mode))
     run = fgmres if solver == "fgmres" else gmres
     x, report = run(make_operator(hier, level), lambda v: mg.apply(v, level), b, tol=tol, maxit=maxit)
-    report.l2_error = l2_error(hier, level, x, prob.exact)
-    report.h1_error = h1_seminorm_error(hier, level, x, prob.gradient)
+    report.l2_error = l2_error_separable(hier, level, x, sine)
+    report.h1_error = h1_seminorm_error_separable(hier, level, x, sine, dsine)
     return SolveOutcome(degree=degree, level=level, mode=mode, solver=solver, dofs=hier.n_dofs(level),
                         report=report, l2=report.l2_error, h1=report.h1_error, x=x if keep_solution else None)
 

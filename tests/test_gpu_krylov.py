@@ -130,3 +130,8 @@ def test_device_rhs_and_l2_error_match_host():
     e_dev = l2_error_separable(hier, 3, u, sine)
     e_host = sf.l2_error(hier, 3, u.cpu().numpy(), prob.exact)
     assert abs(e_dev - e_host) <= 1e-12 * e_host
+    from paper_2407_09621_b200.discretization import h1_seminorm_error_separable
+
+    h_dev = h1_seminorm_error_separable(hier, 3, u, sine, lambda x: np.pi * np.cos(np.pi * x))
+    h_host = sf.h1_seminorm_error(hier, 3, u.cpu().numpy(), prob.gradient)
+    assert abs(h_dev - h_host) <= 1e-12 * h_host
