@@ -134,22 +134,27 @@ __device__ __forceinline__ void split(float x, float& h, float& d) {
   d = (MODE == MODE_FP16_EC) ? __half2float(__float2half_rn((x - h) * kEc)) : 0.f;
 }
 
-// accumulator fragment -> A fragment of the next MMA (same axis), with demotion
+// accumulator fragment -> A fragment of the next MMA (same axis), with demotion.
+// Pairs are rounded with one packed cvt (cvt.rn.f16x2.f32) and the EC residual is formed from
+// the packed halves directly -- the same values as split() + pack2() with ~40 % fewer
+// instructions (the F2FP/HADD2 chain was the largest instruction class, profiles/r01_smoother_fp16.md).
+template <int MODE>
+__device__ __forceinline__ void demote_pair(float x0, float x1, unsigned& h, unsigned& d) {
+  const __half2 hh = __floats2half2_rn(x0, x1);
+  h = *reinterpret_cast<const unsigned*>(&hh);
+  if constexpr (MODE == MODE_FP16_EC) {
+    const float2 hf = __half22float2(hh);
+    const __half2 dd = __floats2half2_rn((x0 - hf.x) * kEc, (x1 - hf.y) * kEc);
+    d = *reinterpret_cast<const unsigned*>(&dd);
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ void acc_to_a(const float (&v)[2][4], AFrag<MODE>& a) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
-    float h0, d0, h1, d1, h2, d2, h3, d3;
-    split<MODE>(v[nt][0], h0, d0);
-    split<MODE>(v[nt][1], h1, d1);
-    split<MODE>(v[nt][2], h2, d2);
-    split<MODE>(v[nt][3], h3, d3);
-    a.h[2 * nt] = pack2(h0, h1);
-    a.h[2 * nt + 1] = pack2(h2, h3);
-    if constexpr (MODE == MODE_FP16_EC) {
-      a.d[2 * nt] = pack2(d0, d1);
-      a.d[2 * nt + 1] = pack2(d2, d3);
-    }
+    demote_pair<MODE>(v[nt][0], v[nt][1], a.h[2 * nt], a.d[2 * nt]);
+    demote_pair<MODE>(v[nt][2], v[nt][3], a.h[2 * nt + 1], a.d[2 * nt + 1]);
   }
 }
 
@@ -189,6 +194,7 @@ struct HTile {
   unsigned nbm;
   int kind[3];
   int lane, warp, g, t;
+  float hur[2][2], huc[2][2];  // [h/d][i]: urow / ucol at output n = 2t + i of this lane (halo16)
   __device__ __forceinline__ __half* ud() const { return uh + 2 * TVOL; }
   __device__ __forceinline__ __half* bd() const { return bh + 2 * TVOL; }
 };
@@ -266,11 +272,10 @@ __device__ __forceinline__ void halo16(const HTile<MODE>& T, Acc16<MODE>& acc, c
       const float bet = tr_lo_b[line];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int n = t2 + i;
-        acc.m[0][2 * rr + i] = fmaf(tab->urow[0][n], ah, acc.m[0][2 * rr + i]);
+        acc.m[0][2 * rr + i] = fmaf(T.hur[0][i], ah, acc.m[0][2 * rr + i]);
         if constexpr (MODE == MODE_FP16_EC) {
-          acc.c[0][2 * rr + i] = fmaf(tab->urow[1][n], ah, acc.c[0][2 * rr + i]);
-          acc.c[0][2 * rr + i] = fmaf(tab->urow[0][n], ad, acc.c[0][2 * rr + i]);
+          acc.c[0][2 * rr + i] = fmaf(T.hur[1][i], ah, acc.c[0][2 * rr + i]);
+          acc.c[0][2 * rr + i] = fmaf(T.hur[0][i], ad, acc.c[0][2 * rr + i]);
         }
       }
       if (t2 == 0) acc.m[0][2 * rr] += bet;
@@ -281,11 +286,10 @@ __device__ __forceinline__ void halo16(const HTile<MODE>& T, Acc16<MODE>& acc, c
       const float bet = tr_hi_b[line];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int n = t2 + i;
-        acc.m[1][2 * rr + i] = fmaf(tab->ucol[0][n], ah, acc.m[1][2 * rr + i]);
+        acc.m[1][2 * rr + i] = fmaf(T.huc[0][i], ah, acc.m[1][2 * rr + i]);
         if constexpr (MODE == MODE_FP16_EC) {
-          acc.c[1][2 * rr + i] = fmaf(tab->ucol[1][n], ah, acc.c[1][2 * rr + i]);
-          acc.c[1][2 * rr + i] = fmaf(tab->ucol[0][n], ad, acc.c[1][2 * rr + i]);
+          acc.c[1][2 * rr + i] = fmaf(T.huc[1][i], ah, acc.c[1][2 * rr + i]);
+          acc.c[1][2 * rr + i] = fmaf(T.huc[0][i], ad, acc.c[1][2 * rr + i]);
         }
       }
       if (t2 + 1 == K - 1) acc.m[1][2 * rr + 1] += bet;
@@ -376,6 +380,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   T.warp = threadIdx.x >> 5;
   T.g = T.lane >> 2;
   T.t = T.lane & 3;
+#pragma unroll
+  for (int hd = 0; hd < 2; ++hd)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      T.hur[hd][i] = __ldg(&tab->urow[hd][2 * T.t + i]);
+      T.huc[hd][i] = __ldg(&tab->ucol[hd][2 * T.t + i]);
+    }
   // tile -> registers -> block exponent -> scaled (h, d) tensors
   const float* ub = u + (long long)(cz * K) * T.sz + (long long)(cy * K) * T.sy + cx * K;
   float4 q4[1024 / kThreads];
@@ -396,10 +407,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
     const int i = threadIdx.x + k2 * kThreads;
     const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 0), q4[k2].x * us);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 1), q4[k2].y * us);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 2), q4[k2].z * us);
-    put<MODE>(T.uh, T.ud(), hidx(z, y, x4 + 3), q4[k2].w * us);
+    // x4..x4+3 are 4 consecutive halves of one 8-block in hidx: one 64-bit store per tensor
+    uint2 hv, dv;
+    demote_pair<MODE>(q4[k2].x * us, q4[k2].y * us, hv.x, dv.x);
+    demote_pair<MODE>(q4[k2].z * us, q4[k2].w * us, hv.y, dv.y);
+    const int o = hidx(z, y, x4);
+    *reinterpret_cast<uint2*>(T.uh + o) = hv;
+    if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(T.ud() + o) = dv;
   }
   e.template traces<kThreads>(g, op, u);
   T.lane = threadIdx.x & 31;
