@@ -384,7 +384,7 @@ def extras(sf, hier, lvl, k, u, v):
         from bench_solve import solve_once
 
         for mode in (P.FP64, P.FP16_EC):
-            r = solve_once(h6, 6, mode, reps=1)
+            r = solve_once(h6, 6, mode, reps=2)
             res[f"solve_q{k}_l6_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
     except Exception as exc:  # secondary measurement only
         res["solve_error"] = repr(exc)[:200]
