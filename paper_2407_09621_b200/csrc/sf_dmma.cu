@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  T.sLf = &tab->L[0][0][0];  // per-lane fragments from the L1-cached device table (coalesced)
-  prologue_fast(T, g, op, u, f);
+  prologue_fast(T, g, op, u, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
   xy_stages(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
@@ -233,11 +232,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __re
   Tile T;
   int batch;
   if (!tile_setup_band(T, smem, g, bd, batch)) return;
-  T.sLf = &tab->L[0][0][0];
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue_fast(T, g, op, xo, f);
+  prologue_fast(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -440,11 +438,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
   Tile T;
   int batch;
   if (!tile_setup_band(T, smem, g, bd, batch)) return;
-  T.sLf = &tab->L[0][0][0];
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
-  prologue_fast(T, g, op, x, f);
+  prologue_fast(T, g, op, x, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;

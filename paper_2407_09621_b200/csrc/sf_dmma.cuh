@@ -738,8 +738,15 @@ __device__ __forceinline__ void prologue_xs(Tile& T, const Geom& g, const OpT& o
 // index computation per element (the prologue was half of the kernel's instructions).
 template <class OpT>
 __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                              const Frags& f) {
+                                              const Frags& f, const double* __restrict__ ltab = nullptr) {
   const int tid = threadIdx.x;
+  // optional: the L_smooth fragment table (4 kinds x 8 x 32 doubles) -> shared memory, so the
+  // stage loops read it with LDS; loads issued here, stored after the trace loads are in flight
+  double lt[4];
+  if (ltab) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lt[i] = __ldg(ltab + tid + kThreads * i);
+  }
   // 32-bit element strides (host guarantees 24 * sz < 2^31): one IMAD.WIDE per address
   const int sy = (int)T.sy, sz = (int)T.sz;
   const long long txy = (long long)(T.cy * K) * sy + T.cx * K;  // tile origin within a z plane
@@ -801,6 +808,11 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
       pl[0] = alpha;
       pl[TRP] = beta;
     }
+  }
+  if (ltab) {
+    double* dst = const_cast<double*>(T.sLf);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[tid + kThreads * i] = lt[i];
   }
   cp_async_wait_all();
   __syncthreads();
