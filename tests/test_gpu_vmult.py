@@ -91,9 +91,9 @@ def test_tensor_in_tensor_out_and_determinism():
     assert v1.is_cuda and torch.equal(v1, v2)
 
 
-@pytest.mark.parametrize("k,lvl", [(7, 6), (3, 7)])
+@pytest.mark.parametrize("k,lvl", [(7, 6), (3, 7), (7, 7), (3, 8)])
 def test_large_vmult_symmetry_and_linearity(k, lvl):
-    """At the bench sizes (1.3e8 DoF) parity is checked through properties."""
+    """At the bench sizes (1.3e8 and 1.07e9 DoF) parity is checked through properties."""
     hier = sf.build_hierarchy(lvl, k, max_dofs=2**31)
     n = hier.n_dofs(lvl)
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -185,3 +185,16 @@ def test_streamed_host_vmult_matches_device(mode, slab_cells):
         dz.STREAM_MIN_DOFS = old
     assert isinstance(w, np.ndarray) and w.dtype == mode.storage_dtype
     assert np.abs(w - ref.cpu().numpy()).max() <= 1e-12 * float(ref.abs().max()) or mode is not P.FP64
+
+
+def test_full_size_constants_annihilated_in_interior():
+    """Q7 level 7 (1.07e9 DoF, the bench workload): A 1 = 0 away from the Nitsche boundary cells."""
+    k, lvl = 7, 7
+    hier = sf.build_hierarchy(lvl, k, max_dofs=2**31)
+    n, K = hier.n_cells(lvl), k + 1
+    u = torch.ones(hier.n_dofs(lvl), dtype=torch.float64, device="cuda")
+    v = sf.apply_operator(hier, lvl, u).reshape(n * K, n * K, n * K)
+    inner = v[K:-K, K:-K, K:-K]
+    scale = float(sf.apply_operator(hier, lvl, torch.randn_like(u)).abs().max())
+    assert float(inner.abs().max()) <= 1e-12 * scale
+    assert float(v.abs().max()) > 1e-6 * scale  # the boundary layer is not zero
