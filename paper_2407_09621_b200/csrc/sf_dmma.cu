@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __re
   Tile T;
   int batch;
   if (!tile_setup_band(T, smem, g, bd, batch)) return;
+  prefetch_tile_rows_l2(T, b);
+  prefetch_ahead_l2(g, bd, T, xo);
   Frags f;
   Halo h;
   init_frags(T, op, f, h);
@@ -438,6 +440,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
   Tile T;
   int batch;
   if (!tile_setup_band(T, smem, g, bd, batch)) return;
+  prefetch_tile_rows_l2(T, b);
+  prefetch_ahead_l2(g, bd, T, x);
   Frags f;
   Halo h;
   init_frags(T, op, f, h);

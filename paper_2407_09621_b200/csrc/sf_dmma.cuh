@@ -199,6 +199,15 @@ __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd,
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
+// L2 prefetch of this tile's rows of a second input (the right-hand side b the colour /
+// restriction kernels read in their z stage): DRAM latency paid during the prologue, not there.
+__device__ __forceinline__ void prefetch_tile_rows_l2(const Tile& T, const double* __restrict__ p0) {
+  if (threadIdx.x >= 256) return;
+  const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
+  const double* p = p0 + (long long)(T.cz * K + z) * T.sz + (long long)(T.cy * K + y) * T.sy + T.cx * K;
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 __device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g, int tile_id) {
   T.sU = smem;
   T.sB = smem + VOL;
