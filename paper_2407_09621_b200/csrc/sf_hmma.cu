@@ -350,6 +350,19 @@ __device__ __forceinline__ void trace_masses_tc(const HTile<MODE>& T, const HTab
   }
 }
 
+// L2 prefetch of this tile's rows of b (read in the z stage of the colour / restriction kernels)
+__device__ __forceinline__ void prefetch_b_rows(const Geom& g, const float* __restrict__ b) {
+  if ((int)blockIdx.x >= g.ntx * g.nty * g.ntz) return;
+  int tx, ty, tz;
+  tile_coords<K>(g, blockIdx.x, tx, ty, tz);
+  const long long sy = (long long)g.nx * K, sz = sy * (long long)g.ny * K;
+  const int cx = g.tx0 + 2 * tx, cy = g.ty0 + 2 * ty, cz = g.tz0 + 2 * tz;
+  for (int r = threadIdx.x; r < 256; r += kThreads) {
+    const float* p = b + (long long)(cz * K + (r >> 4)) * sz + (long long)(cy * K + (r & 15)) * sy + cx * K;
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+  }
+}
+
 // prologue + x/y stages; leaves c in U and dd in B (f16 tensors), trace planes ready
 template <int MODE>
 __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<K, MODE>& op,
@@ -540,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
                                                           const HTables* __restrict__ tab) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
+  prefetch_b_rows(g, b);
   if (!tile_front<MODE>(T, smem, g, op, tab, xo)) return;
   __syncthreads();
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
@@ -688,6 +702,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
                                                                   const HPTab* __restrict__ pt) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
+  prefetch_b_rows(g, b);
   if (!tile_front<MODE>(T, smem, g, op, tab, x)) return;
   __syncthreads();
   BFrag<MODE> bm, bl;
