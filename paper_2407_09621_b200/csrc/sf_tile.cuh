@@ -215,7 +215,7 @@ struct TileEngine {
           base = reinterpret_cast<const S*>(g.ghost_lo) + (long long)(Z + K) * sz + (long long)Y * sy + X;
         }
         constexpr int V = 16 / sizeof(S);  // elements per 16-byte vector
-        if (axis == 0 && V == 4 && K % V == 0) {  // (fp64: scalar loads keep the generic kernels at 3 CTAs/SM)
+        if (axis == 0 && K % V == 0) {
           // x faces: the neighbour's K nodes are contiguous -- 16-byte loads (4x / 2x fewer
           // L1 wavefronts than scalar loads that each touch a different row)
 #pragma unroll
