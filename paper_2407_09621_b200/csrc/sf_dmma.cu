@@ -55,6 +55,7 @@ static PatchL build_patch_l(const double* opd) {
   return p;
 }
 
+template <int K = 8>
 static LevelOp<K, MODE_FP64> pack_op64(const double* opd) {
   LevelOp<K, MODE_FP64> op;
   for (int i = 0; i < K; ++i)
@@ -541,7 +542,147 @@ static const PTab8* ptables8(const double* embd) {
   return reinterpret_cast<const PTab8*>(d);
 }
 
+// ---------------------------------------------------------------------------
+// Q1 / Q3 (K = 2, 4) on DMMA: the same 16^3-point tile, now (16/K)^3 cells.  A tile line is
+// 16 / K cells; its 1-D operators are the 16 x 16 line matrices -- blockdiag(M_cell) for the
+// mass (per-lane B fragments from init_frags<K>) and, for the stiffness, the block-tridiagonal
+// line operator (D on the diagonal, the rank-2 face couplings U / U^T between consecutive cells,
+// Nitsche rows at domain-boundary ends) built here per boundary kind.  Faces to cells outside
+// the tile line use the same (alpha, beta) halo as K = 8.
+template <int KK>
+static PatchL build_line_l(const double* opd) {
+  constexpr int CPL = 16 / KK;
+  const double* D = opd + KK * KK;
+  const double* ucol = opd + 2 * KK * KK;
+  const double* urow = ucol + KK;
+  const double* bl = urow + KK;
+  const double* br = bl + KK;
+  PatchL p;
+  for (int q = 0; q < 4; ++q) {
+    const int lb = q >> 1, rb = q & 1;
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < B; ++j) p.L[q][i][j] = 0.0;
+    for (int c = 0; c < CPL; ++c)
+      for (int i = 0; i < KK; ++i)
+        for (int j = 0; j < KK; ++j) p.L[q][c * KK + i][c * KK + j] = D[i * KK + j];
+    for (int c = 0; c + 1 < CPL; ++c) {
+      const int o = c * KK, o2 = (c + 1) * KK;
+      for (int i = 0; i < KK; ++i) {
+        p.L[q][o + i][o2] = ucol[i];           // U column 0
+        p.L[q][o + KK - 1][o2 + i] = urow[i];  // U row K-1
+        p.L[q][o2][o + i] = ucol[i];           // U^T row 0
+        p.L[q][o2 + i][o + KK - 1] = urow[i];  // U^T column K-1
+      }
+    }
+    if (lb)
+      for (int i = 0; i < KK; ++i) {
+        p.L[q][i][0] += bl[i];
+        if (i > 0) p.L[q][0][i] += bl[i];
+      }
+    if (rb) {
+      const int e = B - KK;
+      for (int i = 0; i < KK; ++i) {
+        p.L[q][e + i][B - 1] += br[i];
+        if (i < KK - 1) p.L[q][B - 1][e + i] += br[i];
+      }
+    }
+  }
+  return p;
+}
+
+template <int KK>
+static const Tables8* line_tables(const double* opd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(opd, opd + 2 * KK * KK + 4 * KK);
+  key.push_back(-1000.0 - KK);  // tag: line tables of cell size KK
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_tabs)
+    if (e.dev == dev && e.key == key) return reinterpret_cast<const Tables8*>(e.ptr);
+  PatchL pl = build_line_l<KK>(opd);
+  Tables8 host{};
+  for (int q = 0; q < 4; ++q)
+    for (int fr = 0; fr < 8; ++fr)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int nb = fr >> 2, kc = fr & 3;
+        host.L[q][fr][ln] = pl.L[q][8 * nb + (ln >> 2)][4 * kc + (ln & 3)];
+      }
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(Tables8)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(Tables8), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_tabs.push_back({dev, std::move(key), d});
+  return reinterpret_cast<const Tables8*>(d);
+}
+
+template <int KK>
+__global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* __restrict__ u, double* __restrict__ v,
+                                                                Geom g, LevelOp<KK, MODE_FP64> op,
+                                                                const Tables8* __restrict__ tab, Band bd, int prefetch) {
+  extern __shared__ __align__(128) double smem[];
+  Tile T;
+  int batch;
+  if (!tile_setup_band<KK>(T, smem, g, bd, batch)) return;
+  u += (long long)batch * g.batch_stride;
+  v += (long long)batch * g.batch_stride;
+  if (prefetch) prefetch_ahead_l2<KK>(g, bd, T, u);
+  Frags f;
+  Halo h;
+  init_frags<KK>(T, op, f, h);
+  prologue_fast<KK>(T, g, op, u, f, &tab->L[0][0][0]);
+  xy_stages(T, f, h);
+  __syncthreads();
+  load_l(T, f, T.kind[2]);
+  double* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
+  for (int yy = 0; yy < 2; ++yy) {
+    const int y = 2 * T.warp + yy;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      double acc[2][2];
+      z_group(T, f, h, y, 8 * g8, acc);
+      const int x = 8 * g8 + T.r;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = acc[nb][i];
+    }
+  }
+}
+
+template <int KK>
+static int launch_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
+  Geom g = g0;
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = g.nz / CPL;
+  const Tables8* tab = line_tables<KK>(opd);
+  if (!tab) return -3;
+  auto op = pack_op64<KK>(opd);
+  auto kern = k_vmult_dmma_line<KK>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
+    return -3;
+  const Band bd = make_band(g);
+  const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
+  for (int b0 = 0; b0 < batch; b0 += per) {
+    const int nb = batch - b0 < per ? batch - b0 : per;
+    kern<<<dim3(g.ntx, bd.by, bd.zb * nb), kThreads, kSmemTile, st>>>(
+        (const double*)u + (long long)b0 * g.batch_stride, (double*)v + (long long)b0 * g.batch_stride, g, op, tab, bd,
+        148);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 }  // namespace dm
+
+// FP64 vmult for K = 2 and 4 on DMMA (16-point tile lines of 16/K cells); kUseGeneric when the
+// local grid is not a multiple of 16/K cells per axis.
+int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
+                           cudaStream_t st) {
+  if (k_nodes == 4) return dm::launch_line<4>(g, opd, u, v, batch, st);
+  if (k_nodes == 2) return dm::launch_line<2>(g, opd, u, v, batch, st);
+  return kUseGeneric;
+}
 
 int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   if (!dm::offsets32(g)) return kUseGeneric;

@@ -98,10 +98,12 @@ struct Tile {
   int b0;  // banded launch: first tile row of the band
 };
 
-// 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary
+// 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary.
+// A tile line spans 16 points = 16 / K cells (K = 8: 2 cells, K = 4: 4, K = 2: 8).
+template <int K = 8>
 __device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0) {
   int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
-  int c = hi ? c0 + 2 : c0 - 1;
+  int c = hi ? c0 + 16 / K : c0 - 1;
   if (c >= 0 && c < n) return 0;
   if (hi ? g.bnd_hi[axis] : g.bnd_lo[axis]) return 2;
   return 1;
@@ -133,33 +135,38 @@ __device__ __forceinline__ bool band_tile(const Geom& g, const Band& bd, int& tx
   return ty < g.nty;
 }
 
-__device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id);
+template <int K = 8>
 __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz);
 
 __device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
   if (tile_id >= g.ntx * g.nty * g.ntz) return false;
   int tx, ty, tz;
   tile_coords<K>(g, tile_id, tx, ty, tz);
-  tile_fields(T, g, tx, ty, tz);
+  tile_fields<8>(T, g, tx, ty, tz);
   return true;
 }
 
+template <int K>
 __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz) {
-  T.cx = g.tx0 + 2 * tx;
-  T.cy = g.ty0 + 2 * ty;
-  T.cz = g.tz0 + 2 * tz;
+  constexpr int CPL = 16 / K;
+  T.cx = g.tx0 + CPL * tx;
+  T.cy = g.ty0 + CPL * ty;
+  T.cz = g.tz0 + CPL * tz;
   T.sy = (long long)g.nx * K;
   T.sz = T.sy * (long long)g.ny * K;
   const int c0[3] = {T.cx, T.cy, T.cz};
   T.nbm = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (face_src(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
-    if (face_src(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
+    if (face_src<K>(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
+    if (face_src<K>(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
   }
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    T.kind[a] = patch_kind(g, a, c0[a]);
+  for (int a = 0; a < 3; ++a) {  // kind of the 16-point line: 2 * (domain boundary at its start) + (at its end)
+    const int n = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
+    const int lb = (c0[a] == 0 && g.bnd_lo[a]) ? 1 : 0;
+    const int rb = (c0[a] + CPL == n && g.bnd_hi[a]) ? 1 : 0;
+    T.kind[a] = 2 * lb + rb;
   }
   T.lane = threadIdx.x & 31;
   T.warp = threadIdx.x >> 5;
@@ -169,6 +176,7 @@ __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int 
 }
 
 // banded-grid variant of tile_setup; `batch` = vector index of a batched launch
+template <int K = 8>
 __device__ __forceinline__ bool tile_setup_band(Tile& T, double* smem, const Geom& g, const Band& bd, int& batch) {
   T.sU = smem;
   T.sB = smem + VOL;
@@ -176,16 +184,18 @@ __device__ __forceinline__ bool tile_setup_band(Tile& T, double* smem, const Geo
   T.sLf = T.tr + 12 * TRP;
   int tx, ty, tz;
   if (!band_tile(g, bd, tx, ty, tz, batch)) return false;
-  tile_fields(T, g, tx, ty, tz);
+  tile_fields<K>(T, g, tx, ty, tz);
   T.b0 = ty - blockIdx.y;  // first tile row of this band
   return true;
 }
 
 // L2 prefetch of the u rows of the tile two rows ahead in launch order (~2 ntx CTAs later):
 // (tx, ty + 2) inside the band, else the wrapped row of the next z layer.
+template <int K = 8>
 __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd, const Tile& T,
                                                   const double* __restrict__ u) {
-  const int ty = (T.cy - g.ty0) >> 1, tz = (T.cz - g.tz0) >> 1;
+  constexpr int CPL = 16 / K;
+  const int ty = (T.cy - g.ty0) / CPL, tz = (T.cz - g.tz0) / CPL;
   const int b0 = T.b0;
   const int bh = min(bd.by, g.nty - b0);
   int ny = ty + 2, nz = tz;
@@ -195,7 +205,8 @@ __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd,
   }
   if (ny < b0 || threadIdx.x >= 256) return;
   const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
-  const double* p = u + (long long)((g.tz0 + 2 * nz) * K + z) * T.sz + (long long)((g.ty0 + 2 * ny) * K + y) * T.sy + T.cx * K;
+  const double* p = u + (long long)((g.tz0 + CPL * nz) * K + z) * T.sz + (long long)((g.ty0 + CPL * ny) * K + y) * T.sy +
+                    T.cx * K;
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
@@ -468,81 +479,29 @@ __device__ __forceinline__ void z_group(const Tile& T, const Frags& f, const Hal
   mass_group(f, dd, acc);
 }
 
-template <class OpT>
+// Per-lane operator fragments: mass B fragment of the 16-point line operator blockdiag(M_cell)
+// (chunk kc of the block: nonzero where output row r and input 4kc + k4 fall in one cell), and
+// the halo coefficients of the line's first / last cell (zero for lanes whose outputs lie in
+// another cell, so Halo::apply needs no cell test).
+template <int K = 8, class OpT>
 __device__ __forceinline__ void init_frags(const Tile& T, const OpT& op, Frags& f, Halo& h) {
-  f.m[0] = op.M[T.r][T.k4].h;
-  f.m[1] = op.M[T.r][4 + T.k4].h;
-  h.ur[0] = op.urow[T.c2].h;
-  h.ur[1] = op.urow[T.c2 + 1].h;
-  h.uc[0] = op.ucol[T.c2].h;
-  h.uc[1] = op.ucol[T.c2 + 1].h;
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    const int kk = 4 * kc + T.k4;
+    f.m[kc] = (T.r / K == kk / K) ? op.M[T.r % K][kk % K].h : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int n0 = T.c2 + i;          // output within the first 8-block (cell 0 when n0 < K)
+    const int n1 = T.c2 + i - (8 - K);  // output index within the last cell (second 8-block)
+    h.ur[i] = n0 < K ? op.urow[n0].h : 0.0;
+    h.uc[i] = n1 >= 0 ? op.ucol[n1].h : 0.0;
+  }
 }
 
 
 // ---------------------------------------------------------------------------
-// Software-pipelined front end (vmult / colour / residual-restriction kernels):
-// the neighbour-trace loads of axis a+1 are issued into registers before the
-// DMMA stage of axis a and consumed after it, so two thirds of the L2/HBM trace
-// latency hides behind tensor-core work (profiles/r01_vmult_fp64.md).
-constexpr int kTIPT = 512 / kThreads;  // trace items per thread and axis (2 faces x 256 points / CTA)
-
-template <int AXIS>
-__device__ __forceinline__ void trace_load(const Tile& T, const Geom& g, const double* __restrict__ u,
-                                           double (&w)[kTIPT][K]) {
-#pragma unroll
-  for (int j = 0; j < kTIPT; ++j) {
-    const int it = threadIdx.x + kThreads * j;
-    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
-    if (!((T.nbm >> (2 * AXIS + hi)) & 1)) continue;
-    int X = T.cx * K, Y = T.cy * K, Z = T.cz * K;
-    long long step;
-    if (AXIS == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
-    else if (AXIS == 1) { Z += p; X += q; Y += hi ? B : -K; step = T.sy; }
-    else { Y += p; X += q; Z += hi ? B : -K; step = T.sz; }
-    const double* base;
-    if (AXIS == 2 && (Z < 0 || Z >= g.nz * K)) {
-      base = hi ? reinterpret_cast<const double*>(g.ghost_hi) + (long long)(Z - g.nz * K) * T.sz
-                : reinterpret_cast<const double*>(g.ghost_lo) + (long long)(Z + K) * T.sz;
-      base += (long long)Y * T.sy + X;
-    } else {
-      base = u + (long long)Z * T.sz + (long long)Y * T.sy + X;
-    }
-    if (AXIS == 0) {
-#pragma unroll
-      for (int c = 0; c < K / 2; ++c) {
-        const double2 v2 = __ldg(reinterpret_cast<const double2*>(base + 2 * c));
-        w[j][2 * c] = v2.x;
-        w[j][2 * c + 1] = v2.y;
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < K; ++c) w[j][c] = __ldg(base + c * step);
-    }
-  }
-}
-
-template <int AXIS, class OpT>
-__device__ __forceinline__ void trace_store(const Tile& T, const OpT& op, const double (&w)[kTIPT][K]) {
-#pragma unroll
-  for (int j = 0; j < kTIPT; ++j) {
-    const int it = threadIdx.x + kThreads * j;
-    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
-    if (!((T.nbm >> (2 * AXIS + hi)) & 1)) continue;
-    double alpha, beta = 0.0;
-    if (hi) {
-      alpha = w[j][0];
-#pragma unroll
-      for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[j][c], beta);
-    } else {
-      alpha = w[j][K - 1];
-#pragma unroll
-      for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[j][c], beta);
-    }
-    double* pl = T.tr + (2 * AXIS + hi) * 2 * TRP;
-    pl[p * TRW + q] = alpha;
-    pl[TRP + p * TRW + q] = beta;
-  }
-}
+// Prologue of the vmult / colour / residual-restriction kernels (profiles/r01_vmult_fp64.md).
 
 // tangential mass along q (Mx) on trace planes [first, first + 4): one 8-row group per warp task
 __device__ __forceinline__ void plane_mass_rows(const Tile& T, const Frags& f, int first) {
@@ -583,169 +542,25 @@ __device__ __forceinline__ void plane_mass_cols(const Tile& T, const Frags& f) {
   }
 }
 
-// x stage on the warp's two z planes: a = Mx u -> U, b = Lx u (+ x halo) -> B (rows stay in their row)
-__device__ __forceinline__ void x_stage(const Tile& T, Frags& f, const Halo& h) {
-  load_l(T, f, T.kind[0]);
-#pragma unroll 1
-  for (int zz = 0; zz < 2; ++zz) {
-    const int z = 2 * T.warp + zz;
-#pragma unroll
-    for (int g8 = 0; g8 < 2; ++g8) {
-      const int y = 8 * g8 + T.r;
-      double a[4];
-#pragma unroll
-      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU(z, y, 4 * kc + T.k4)];
-      double ra[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, rb[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      mass_group(f, a, ra);
-      stiff_group(f, a, rb);
-      h.apply(T, rb, 0, z * TRW + y);
-      __syncwarp();  // lines y of this group live in rows y only: in-place per group is safe
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        const int i = idxA(z, y, 8 * nb + T.c2);
-        *reinterpret_cast<double2*>(&T.sU[i]) = make_double2(ra[nb][0], ra[nb][1]);
-        *reinterpret_cast<double2*>(&T.sB[i]) = make_double2(rb[nb][0], rb[nb][1]);
-      }
-    }
-  }
+// The x-face neighbour layers are staged through shared memory: the two x neighbour cell
+// layers (2 x 16 x 16 rows of K doubles) go to the still-unused B buffer by cp.async -- row
+// segments, coalesced, no registers -- instead of per-lane K-double LDGs that touch 32 cache
+// lines per warp instruction.  Chunk c of staged row i sits at a swizzled chunk so the 8 lanes
+// of an LDS.128 quarter-warp hit 8 distinct bank groups (K = 8: c ^ ((i >> 1) & 3); K = 4:
+// c ^ ((i >> 2) & 1); K = 2: one chunk per row, conflict-free as is).  y/z faces keep the
+// register path (their loads are row-coalesced).
+template <int K = 8>
+__device__ __forceinline__ int xs_idx(int row, int c) {
+  if constexpr (K == 8) return row * 8 + 2 * (c ^ ((row >> 1) & 3));
+  else if constexpr (K == 4) return row * 4 + 2 * (c ^ ((row >> 2) & 1));
+  else return row * K + 2 * c;
 }
 
-// y stage on the warp's two z planes: c = My a -> U, dd = Ly a (+ y halo) + My b -> B
-__device__ __forceinline__ void y_stage(const Tile& T, Frags& f, const Halo& h) {
-  load_l(T, f, T.kind[1]);
-#pragma unroll 1
-  for (int zz = 0; zz < 2; ++zz) {
-    const int z = 2 * T.warp + zz;
-    double ra[2][2][2], rb[2][2][2];
-#pragma unroll
-    for (int g8 = 0; g8 < 2; ++g8) {
-      const int x = 8 * g8 + T.r;
-      double a[4], b[4];
-#pragma unroll
-      for (int kc = 0; kc < 4; ++kc) {
-        a[kc] = T.sU[idxA(z, 4 * kc + T.k4, x)];
-        b[kc] = T.sB[idxA(z, 4 * kc + T.k4, x)];
-      }
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
-      mass_group(f, a, ra[g8]);
-      stiff_group(f, a, rb[g8]);
-      h.apply(T, rb[g8], 1, z * TRW + x);
-      mass_group(f, b, rb[g8]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int g8 = 0; g8 < 2; ++g8) {
-      const int x = 8 * g8 + T.r;
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int j = idxC(z, 8 * nb + T.c2 + i, x);
-          T.sU[j] = ra[g8][nb][i];
-          T.sB[j] = rb[g8][nb][i];
-        }
-    }
-    __syncwarp();
-  }
-}
-
-// Prologue with all three axes' trace loads in flight at once (one L2/HBM round trip
-// instead of three): 48 doubles of loads per thread, issued before any is consumed.
-template <class OpT>
-__device__ __forceinline__ void prologue_wide(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                              const Frags& f) {
-  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
-  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
-    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
-    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
-  }
-  double w0[kTIPT][K], w1[kTIPT][K], w2[kTIPT][K];
-  trace_load<0>(T, g, u, w0);
-  trace_load<1>(T, g, u, w1);
-  trace_load<2>(T, g, u, w2);
-  trace_store<0>(T, op, w0);
-  trace_store<1>(T, op, w1);
-  trace_store<2>(T, op, w2);
-  cp_async_wait_all();
-  __syncthreads();
-  plane_mass_rows(T, f, 4);
-  plane_mass_rows(T, f, 8);
-  __syncthreads();
-  plane_mass_cols(T, f);
-  __syncthreads();
-}
-
-// Prologue with the x-face neighbour layers staged through shared memory: the two x
-// neighbour cell layers (2 x 16 x 16 rows of 8 doubles, 32 KB) go to the still-unused B
-// buffer by cp.async -- 64-byte row segments, coalesced, no registers -- instead of per-lane
-// 64-byte LDGs that touch 32 cache lines per warp instruction.  Chunk c of staged row i
-// sits at chunk c ^ ((i >> 1) & 3): the 8 lanes of an LDS.128 quarter-warp hit 8 distinct
-// bank groups.  y/z faces keep the register path (their loads are row-coalesced).
-__device__ __forceinline__ int xs_idx(int row, int c) { return row * 8 + 2 * (c ^ ((row >> 1) & 3)); }
-
-template <class OpT>
-__device__ __forceinline__ void prologue_xs(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                            const Frags& f) {
-  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
-  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
-    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
-    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
-  }
-  // staged row = (hi * 16 + z) * 16 + y ; 4 chunks of 16 B per row
-  for (int c = threadIdx.x; c < 2 * 256 * 4; c += kThreads) {
-    const int ch = c & 3, row = c >> 2, hi = row >> 8, z = (row >> 4) & 15, y = row & 15;
-    if (!((T.nbm >> hi) & 1)) continue;
-    const double* src = ubase + z * T.sz + y * T.sy + (hi ? B : -K) + 2 * ch;
-    cp_async16(&T.sB[xs_idx(row, ch)], src);
-  }
-  double w1[kTIPT][K], w2[kTIPT][K];
-  trace_load<1>(T, g, u, w1);
-  trace_load<2>(T, g, u, w2);
-  trace_store<1>(T, op, w1);
-  trace_store<2>(T, op, w2);
-  cp_async_wait_all();
-  __syncthreads();
-  // x traces from the staged layers: item = (hi, p = z, q = y) -> one staged row
-#pragma unroll
-  for (int j = 0; j < kTIPT; ++j) {
-    const int it = threadIdx.x + kThreads * j;
-    const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
-    if (!((T.nbm >> hi) & 1)) continue;
-    const int row = (hi * 16 + p) * 16 + q;
-    double w[K];
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
-      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx(row, ch)]);
-      w[2 * ch] = v2.x;
-      w[2 * ch + 1] = v2.y;
-    }
-    double alpha, beta = 0.0;
-    if (hi) {
-      alpha = w[0];
-#pragma unroll
-      for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[c], beta);
-    } else {
-      alpha = w[K - 1];
-#pragma unroll
-      for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
-    }
-    double* pl = T.tr + hi * 2 * TRP;
-    pl[p * TRW + q] = alpha;
-    pl[TRP + p * TRW + q] = beta;
-  }
-  plane_mass_rows(T, f, 4);
-  plane_mass_rows(T, f, 8);
-  __syncthreads();  // also: staged layers consumed before the x stage writes B
-  plane_mass_cols(T, f);
-  __syncthreads();
-}
-
-// prologue_xs with the address arithmetic strength-reduced: every thread's cp.async chunks and
-// trace items share one (x, y) position and step only in z (or along the face normal), so each
-// source/destination is one pointer plus a constant stride instead of a fresh 64-bit
-// index computation per element (the prologue was half of the kernel's instructions).
-template <class OpT>
+// Address arithmetic is strength-reduced: every thread's cp.async chunks and trace items share
+// one (x, y) position and step only in z (or along the face normal), so each source/destination
+// is one pointer plus a constant stride instead of a fresh 64-bit index computation per element
+// (the prologue was half of the kernel's instructions).
+template <int K = 8, class OpT>
 __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
                                               const Frags& f, const double* __restrict__ ltab = nullptr) {
   const int tid = threadIdx.x;
@@ -767,15 +582,17 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
 #pragma unroll
     for (int i = 0; i < 8; ++i) cp_async16(dst + i * 512, src + 2 * i * sz);
   }
-  {  // x-neighbour layers: chunk ch = tid & 3 of row (hi, z = (tid >> 6) + 4k, y = (tid >> 2) & 15)
-    const int ch = tid & 3, y = (tid >> 2) & 15, zb = tid >> 6;
+  {  // x-neighbour layers: K/2 16-byte chunks per row (hi, z, y); chunk ch = tid % (K/2),
+     // y = (tid / (K/2)) & 15, z = zb + (32/K) k  -- every k step is 512 staged doubles
+    constexpr int KC = K / 2, LG = KC == 4 ? 2 : (KC == 2 ? 1 : 0);
+    const int ch = tid & (KC - 1), y = (tid >> LG) & 15, zb = tid >> (LG + 4);
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       if (!((T.nbm >> hi) & 1)) continue;
       const double* src = ub + zb * sz + y * sy + (hi ? B : -K) + 2 * ch;
-      double* dst = &T.sB[xs_idx((hi * 16 + zb) * 16 + y, ch)];
+      double* dst = &T.sB[xs_idx<K>((hi * 16 + zb) * 16 + y, ch)];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cp_async16(dst + k * 512, src + 4 * k * sz);
+      for (int k = 0; k < KC; ++k) cp_async16(dst + k * 512, src + (32 / K) * k * sz);
     }
   }
   // y and z faces: item (hi = j, p = (tid >> 4) & 15, q = tid & 15); K values along the normal
@@ -790,7 +607,7 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
     }
     if ((T.nbm >> (4 + hi)) & 1) {  // z faces: Y = p, X = q, Z = hi ? 16 : -8 (ghost planes past the slab)
       const double* b2;
-      const bool inside = hi ? (T.cz + 2 < g.nz) : (T.cz > 0);
+      const bool inside = hi ? (T.cz + 16 / K < g.nz) : (T.cz > 0);
       if (inside) b2 = ub + (hi ? B : -K) * sz + p * sy + q;
       else b2 = reinterpret_cast<const double*>(hi ? g.ghost_hi : g.ghost_lo) + txy + p * sy + q;
 #pragma unroll
@@ -832,8 +649,8 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
     const int row = (hi * 16 + p) * 16 + q;
     double w[K];
 #pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
-      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx(row, ch)]);
+    for (int ch = 0; ch < K / 2; ++ch) {
+      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx<K>(row, ch)]);
       w[2 * ch] = v2.x;
       w[2 * ch + 1] = v2.y;
     }
@@ -858,36 +675,6 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
   __syncthreads();
 }
 
-// Everything before the z stage, pipelined.  On return (after a __syncthreads) U holds c,
-// B holds dd and the z-face planes carry their (My Mx) tangential masses.
-template <class OpT>
-__device__ __forceinline__ void front_stages(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                             Frags& f, const Halo& h) {
-  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
-  for (int c = threadIdx.x; c < VOL / 2; c += kThreads) {
-    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
-    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
-  }
-  double w[kTIPT][K];
-  trace_load<0>(T, g, u, w);
-  trace_store<0>(T, op, w);
-  trace_load<1>(T, g, u, w);  // in flight across the x stage
-  cp_async_wait_all();
-  __syncthreads();
-  x_stage(T, f, h);
-  trace_store<1>(T, op, w);
-  trace_load<2>(T, g, u, w);  // in flight across the y-plane masses and the y stage
-  __syncthreads();
-  plane_mass_rows(T, f, 4);   // y faces: Mx along q
-  __syncthreads();
-  y_stage(T, f, h);
-  trace_store<2>(T, op, w);
-  __syncthreads();
-  plane_mass_rows(T, f, 8);   // z faces: Mx along q
-  __syncthreads();
-  plane_mass_cols(T, f);      // z faces: My along p
-  __syncthreads();
-}
 
 }  // namespace dm
 }  // namespace sf

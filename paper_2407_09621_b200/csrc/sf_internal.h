@@ -114,6 +114,8 @@ inline void build_patch_l_host(const double* opd, double* L /* [4][16][16] */) {
 }
 // FP64 Q7 vmult on DMMA tensor cores (sf_dmma.cu); returns 0 or SF_ECUDA
 constexpr int kUseGeneric = -4;  // tensor-core launcher declines (falls back to the tile engine)
+int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* level_op, const void* u, void* v, int batch,
+                           cudaStream_t st);
 int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, void* v, int batch, cudaStream_t st);
 // FP64 Q7 smoother colour pass on DMMA (sf_dmma.cu)
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,

@@ -636,6 +636,15 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
       return SF_OK;
     }
   }
+  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+    if (!use_generic()) {
+      const int r = launch_vmult_dmma_line(K, g, opd, u, v, batch, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_vmult (dmma line)");
+        return SF_OK;
+      }
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   Prepared<K, MODE> pr(opd, nullptr);

@@ -129,15 +129,17 @@ def test_slab_ghosts_reproduce_the_full_operator():
     assert float(torch.linalg.norm(got - full) / torch.linalg.norm(full)) <= 1e-14
 
 
-def test_tensor_core_path_matches_cuda_core_path(tmp_path):
-    """The DMMA Q7 kernel and the generic CUDA-core tile engine agree (SUMFACT_B200_GENERIC=1)."""
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (1, 5), (3, 2)])
+def test_tensor_core_path_matches_cuda_core_path(tmp_path, k, lvl):
+    """The DMMA kernels (Q7 tiles; Q3/Q1 16-point line tiles) and the generic CUDA-core tile engine
+    agree (SUMFACT_B200_GENERIC=1)."""
     import os
     import subprocess
     import sys
 
     code = ("import numpy as np, sys; sys.path.insert(0, %r); import paper_2407_09621_b200 as sf; "
-            "h = sf.build_hierarchy(3, 7); u = np.random.default_rng(11).standard_normal(h.n_dofs(3)); "
-            "np.save(%r, sf.apply_operator(h, 3, u))")
+            f"h = sf.build_hierarchy({lvl}, {k}); u = np.random.default_rng(11).standard_normal(h.n_dofs({lvl})); "
+            f"np.save(%r, sf.apply_operator(h, {lvl}, u))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for flag in ("0", "1"):
@@ -174,7 +176,7 @@ def test_streamed_host_vmult_matches_device(mode, slab_cells):
     dz._stream_vmult(hier, lvl, u, v, mode, slab_cells=slab_cells)
     ref = torch.empty(n, dtype=mode.torch_dtype, device="cuda")
     dz.vmult_device(hier, lvl, u.cuda(), ref, mode)
-    assert torch.equal(v, ref.cpu()) or mode is not P.FP64
+    # (slabs thinner than a 16-point tile line use the CUDA-core tile engine: same value to rounding)
     assert float((v - ref.cpu()).norm() / ref.norm().cpu()) <= (1e-15 if mode is P.FP64 else 1e-6)
     # the public API takes this path for large host inputs
     old = dz.STREAM_MIN_DOFS
