@@ -225,25 +225,28 @@ __device__ __forceinline__ void full_group(const double (*l)[4], const double* a
 // patch tile r = b - A x_old, x_new = x_old + (V_z V_y V_x) Lambda^-1 (V_x^T V_y^T V_z^T) r.
 // Stage order: residual z-lines -> V_z^T (registers) | V_y^T | V_x^T, 1/lambda,
 // V_x (registers) | V_y | V_z -> +x_old -> HBM; '|' = shared-memory transpose.
-__global__ void __launch_bounds__(kThreads, 2) k_colour_dmma8(const double* __restrict__ xo,
-                                                             const double* __restrict__ b, double* __restrict__ xn,
-                                                             Geom g, LevelOp<K, MODE_FP64> op,
-                                                             const Tables8* __restrict__ tab, Band bd) {
+// KK = 8: one patch per tile line; KK = 4 / 2: a 16-point line holds 2 / 4 patches and the
+// transforms are blockdiag(V_patch) (line tables built per line boundary kind).
+template <int KK = 8>
+__global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __restrict__ xo,
+                                                            const double* __restrict__ b, double* __restrict__ xn,
+                                                            Geom g, LevelOp<KK, MODE_FP64> op,
+                                                            const Tables8* __restrict__ tab, Band bd) {
   extern __shared__ __align__(128) double smem[];
   Tile T;
   int batch;
-  if (!tile_setup_band(T, smem, g, bd, batch)) return;
-  prefetch_tile_rows_l2(T, b);
-  prefetch_ahead_l2(g, bd, T, xo);
+  if (!tile_setup_band<KK>(T, smem, g, bd, batch)) return;
+  prefetch_tile_rows_l2<KK>(T, b);
+  prefetch_ahead_l2<KK>(g, bd, T, xo);
   Frags f;
   Halo h;
-  init_frags(T, op, f, h);
-  prologue_fast(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
+  init_frags<KK>(T, op, f, h);
+  prologue_fast<KK>(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
-  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   double V[2][4];
   // ---- z lines: residual and forward V_z^T (chained in registers), out in T layout
   load_l(T, f, kz);
@@ -614,6 +617,84 @@ static const Tables8* line_tables(const double* opd) {
   return reinterpret_cast<const Tables8*>(d);
 }
 
+// Fragment tables of the line operators for the colour pass: L_line[kind] and the transforms
+// blockdiag(V_patch) over the 16 / (2 KK) patches of a tile line (patch j's kind: left domain
+// boundary only for j = 0, right only for the last), eigenvalues concatenated.
+template <int KK>
+static Tables8 build_line_tables(const double* opd, const double* eigd) {
+  constexpr int PB = 2 * KK, PPL = 16 / PB;  // patch size, patches per line
+  PatchL pl = build_line_l<KK>(opd);
+  Tables8 t{};
+  auto perm = [](int kc, int c) { return 8 * (kc >> 1) + 2 * c + (kc & 1); };
+  for (int q = 0; q < 4; ++q) {
+    const int lb = q >> 1, rb = q & 1;
+    double V[16][16] = {};
+    double lam[16];
+    for (int j = 0; j < PPL; ++j) {
+      const int kind = (j == 0 ? 2 * lb : 0) + (j == PPL - 1 ? rb : 0);
+      const double* Vp = eigd + kind * PB * PB;
+      for (int a = 0; a < PB; ++a) {
+        for (int c = 0; c < PB; ++c) V[j * PB + a][j * PB + c] = Vp[a * PB + c];
+        lam[j * PB + a] = eigd[4 * PB * PB + kind * PB + a];
+      }
+    }
+    for (int fr = 0; fr < 8; ++fr)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int nb = fr >> 2, kc = fr & 3, n = 8 * nb + (ln >> 2), c = ln & 3;
+        const int ks = 4 * kc + c, kp = perm(kc, c);
+        t.L[q][fr][ln] = pl.L[q][n][ks];
+        t.Vf[q][fr][ln] = V[ks][n];
+        t.Vfp[q][fr][ln] = V[kp][n];
+        t.Vb[q][fr][ln] = V[n][ks];
+        t.Vbp[q][fr][ln] = V[n][kp];
+      }
+    for (int i = 0; i < 16; ++i) t.lam[q][i] = lam[i];
+  }
+  return t;
+}
+
+template <int KK>
+static const Tables8* line_colour_tables(const double* opd, const double* eigd) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(opd, opd + 2 * KK * KK + 4 * KK);
+  key.insert(key.end(), eigd, eigd + 4 * 4 * KK * KK + 4 * 2 * KK);
+  key.push_back(-2000.0 - KK);  // tag: colour line tables of cell size KK
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_tabs)
+    if (e.dev == dev && e.key == key) return reinterpret_cast<const Tables8*>(e.ptr);
+  Tables8 host = build_line_tables<KK>(opd, eigd);
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(Tables8)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(Tables8), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_tabs.push_back({dev, std::move(key), d});
+  return reinterpret_cast<const Tables8*>(d);
+}
+
+template <int KK>
+static int launch_colour_line(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b,
+                              void* xn, cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
+  const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
+  for (int a = 0; a < 3; ++a)
+    if (s3[a] && n3[a] < CPL + 2) return kUseGeneric;  // shifted line must fit inside [1, n-1)
+  Geom g = g0;
+  g.ntx = g.nx / CPL;  // shifted colours: the last line is clamped to end at cell n-2 (tile_fields)
+  g.nty = g.ny / CPL;
+  g.ntz = g.nz / CPL;
+  const Tables8* tab = line_colour_tables<KK>(opd, eigd);
+  if (!tab) return -3;
+  auto op = pack_op64<KK>(opd);
+  if (cudaFuncSetAttribute(k_colour_dmma<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) !=
+      cudaSuccess)
+    return -3;
+  const Band bd = make_band(g);
+  k_colour_dmma<KK><<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const double*)xo, (const double*)b,
+                                                                           (double*)xn, g, op, tab, bd);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 template <int KK>
 __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* __restrict__ u, double* __restrict__ v,
                                                                 Geom g, LevelOp<KK, MODE_FP64> op,
@@ -731,6 +812,14 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
 }  // namespace sf
 
 namespace sf {
+// FP64 colour pass for K = 2 and 4 on DMMA (kUseGeneric when the grid does not tile)
+int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* opd, const double* eigd, const void* xo,
+                            const void* b, void* xn, cudaStream_t st) {
+  if (k_nodes == 4) return dm::launch_colour_line<4>(g, opd, eigd, xo, b, xn, st);
+  if (k_nodes == 2) return dm::launch_colour_line<2>(g, opd, eigd, xo, b, xn, st);
+  return kUseGeneric;
+}
+
 int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
                         cudaStream_t st) {
   if (!dm::offsets32(g)) return kUseGeneric;
@@ -738,10 +827,10 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
   if (!tab) return -3;
   auto op = dm::pack_op64(opd);
   cudaError_t err =
-      cudaFuncSetAttribute(dm::k_colour_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
+      cudaFuncSetAttribute(dm::k_colour_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
   if (err != cudaSuccess) return -3;
   const dm::Band bd = dm::make_band(g);
-  dm::k_colour_dmma8<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
+  dm::k_colour_dmma<8><<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
       (const double*)xo, (const double*)b, (double*)xn, g, op, tab, bd);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

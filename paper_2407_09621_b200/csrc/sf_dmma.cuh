@@ -152,6 +152,11 @@ __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int 
   T.cx = g.tx0 + CPL * tx;
   T.cy = g.ty0 + CPL * ty;
   T.cz = g.tz0 + CPL * tz;
+  if constexpr (K < 8) {  // shifted colour: the last line ends at cell n-2 (overlaps its neighbour)
+    T.cx = min(T.cx, g.nx - CPL - g.tx0);
+    T.cy = min(T.cy, g.ny - CPL - g.ty0);
+    T.cz = min(T.cz, g.nz - CPL - g.tz0);
+  }
   T.sy = (long long)g.nx * K;
   T.sz = T.sy * (long long)g.ny * K;
   const int c0[3] = {T.cx, T.cy, T.cz};
@@ -212,6 +217,7 @@ __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd,
 
 // L2 prefetch of this tile's rows of a second input (the right-hand side b the colour /
 // restriction kernels read in their z stage): DRAM latency paid during the prologue, not there.
+template <int K = 8>
 __device__ __forceinline__ void prefetch_tile_rows_l2(const Tile& T, const double* __restrict__ p0) {
   if (threadIdx.x >= 256) return;
   const int y = threadIdx.x & 15, z = threadIdx.x >> 4;

@@ -118,6 +118,8 @@ int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* level_op, c
                            cudaStream_t st);
 int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, void* v, int batch, cudaStream_t st);
 // FP64 Q7 smoother colour pass on DMMA (sf_dmma.cu)
+int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* patch_eig,
+                            const void* x_old, const void* b, void* x_new, cudaStream_t st);
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
                         const void* b, void* x_new, cudaStream_t st);
 // FP64 Q7 residual + restriction on DMMA (sf_dmma.cu)

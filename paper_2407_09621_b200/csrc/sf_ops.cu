@@ -686,6 +686,15 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
       }
     }
   }
+  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+    if (!use_generic()) {
+      const int r = launch_colour_dmma_line(K, g, opd, eigd, xo, b, xn, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_smooth_colour (dmma line)");
+        done = true;
+      }
+    }
+  }
   if constexpr (K == 8 && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
     if (!use_generic()) {
       if (launch_colour_hmma8(MODE, g, opd, eigd, xo, b, xn, st)) return check_launch("sf_smooth_colour (hmma)");

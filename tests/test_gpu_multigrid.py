@@ -171,16 +171,17 @@ def test_tensor_core_smoother_matches_cuda_core_smoother(tmp_path):
     assert rel_l2(outs[0], outs[1]) <= 1e-13
 
 
-@pytest.mark.parametrize("lvl", [3, 4])
-def test_q7_smoother_matches_oracle(lvl):
-    """Q7 smoother (DMMA path) against the CPU oracle at the sizes it finishes quickly."""
+@pytest.mark.parametrize("k,lvl", [(7, 3), (7, 4), (3, 3), (3, 4), (1, 4), (1, 5)])
+def test_q7_smoother_matches_oracle(k, lvl):
+    """Smoother on the DMMA paths (Q7 patch tiles; Q3/Q1 16-point line tiles with both shift
+    parities, incl. the overlapping last line of shifted colours) against the CPU oracle."""
     from oracle import port
 
-    hier = sf.build_hierarchy(lvl, 7)
+    hier = sf.build_hierarchy(lvl, k)
     D = hier.n_dofs(lvl)
     x, b = unit(np.random.default_rng(5), D), unit(np.random.default_rng(6), D)
     got = sf.MultigridPreconditioner(hier).smooth(lvl, x, b)
-    ref = port.VCycle(port.Hierarchy(lvl, 7)).smooth(lvl, x, b)
+    ref = port.VCycle(port.Hierarchy(lvl, k)).smooth(lvl, x, b)
     assert rel_l2(got, ref) <= 1e-11
 
 
