@@ -377,6 +377,7 @@ def extras(sf, hier, lvl, k, u, v):
         ms = timeit(lambda: mg._smooth_device(6, x, b, mode), reps=2)
         res[f"smooth_step_q{k}_l6_{mode.value}_ms"] = ms
     del x, b, mg
+    torch.cuda.empty_cache()  # the vmult benches above leave large cached blocks; solves allocate afresh
     # time-to-solution (BASELINE configs[3]): FGMRES(fp64) + V-cycle(fp64 | fp16_ec), Q7 level 6,
     # 1.34e8 DoF, setup excluded (tools/bench_solve.py)
     try:
