@@ -52,13 +52,14 @@ def ref_flops_per_dof(k, level):
 
 
 def kernel_flops_per_dof(k):
-    """Tensor-pipe flops the FP64 Q7 vmult kernel executes per DoF: one 2x2x2-cell tile
+    """Tensor-pipe flops the FP64 vmult kernel executes per DoF: one 16^3-point tile
     (4096 DoF) issues 1376 DMMA.8x8x4 (512 flop each): x stage 384, y stage 512, z stage 384, trace-plane
-    masses 96.  This is the figure ncu's DMMA-pipe utilisation measures, so frac and the pipe % agree."""
-    if k != 7:
-        K = k + 1  # CUDA-core tile engine: line stages 7K + 9 - 3/K MACs + traces/masses (DESIGN.md §4.4)
-        return 2 * (7 * K + 9 - 3.0 / K + 3.0 * (K - 1) / K + 6.0) + 2
-    return 1376 * 512 / 4096
+    masses 96 -- for Q7 (2x2x2-cell tiles) and for Q3/Q1 (16-point line tiles of 4 / 8 cells) alike.
+    This is the figure ncu's DMMA-pipe utilisation measures, so frac and the pipe % agree."""
+    if k in (1, 3, 7):
+        return 1376 * 512 / 4096
+    K = k + 1  # CUDA-core tile engine: line stages 7K + 9 - 3/K MACs + traces/masses (DESIGN.md §3)
+    return 2 * (7 * K + 9 - 3.0 / K + 3.0 * (K - 1) / K + 6.0) + 2
 
 
 class ClockSampler:
@@ -264,7 +265,8 @@ def main():
     hbm, hbm_src = peaks()
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved_tf / FP64_PEAK_TFLOPS) if achieved_tf else None, "traffic": None,
-                "kernel": "sf::dm::k_vmult_dmma8" if k == 7 else f"sf::k_vmult<{K},0>",
+                "kernel": {7: "sf::dm::k_vmult_dmma8", 3: "sf::dm::k_vmult_dmma_line<4>",
+                           1: "sf::dm::k_vmult_dmma_line<2>"}.get(k, f"sf::k_vmult<{K},0>"),
                 "kernel_ms": kms,
                 "flops_per_dof": kernel_flops_per_dof(k),
                 "peak_source": "measured DMMA microbenchmark (profiles/r01_microbench_fp64.md)",

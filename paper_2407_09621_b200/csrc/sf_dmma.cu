@@ -123,87 +123,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
 
 
 
-// Persistent warp-specialised variant: 8 consumer warps run the x/y/z stages of
-// tile i while 4 producer warps stage tile i+1 (cp.async tile, L2 trace loads,
-// trace-plane masses) into the other half of a double buffer.  Named barriers:
-// FULL[b] (producers arrive, consumers sync), EMPTY[b] (consumers arrive,
-// producers sync), CONS (consumers only), PROD (producers only).
-constexpr int kCons = 256, kProd = 128, kWsThreads = kCons + kProd;
-constexpr size_t kSmemWs = sizeof(double) * (2 * (VOL + 12 * TRP) + VOL + 4 * 8 * 32);
-enum { BAR_FULL0 = 1, BAR_EMPTY0 = 3, BAR_CONS = 5, BAR_PROD = 6 };
-
-__global__ void __launch_bounds__(kWsThreads, 1) k_vmult_dmma8_ws(const double* __restrict__ u,
-                                                                 double* __restrict__ v, Geom g,
-                                                                 LevelOp<K, MODE_FP64> op,
-                                                                 const Tables8* __restrict__ tab) {
-  extern __shared__ __align__(128) double smem[];
-  double* sUbuf[2] = {smem, smem + VOL};
-  double* trbuf[2] = {smem + 2 * VOL, smem + 2 * VOL + 12 * TRP};
-  double* sB = smem + 2 * VOL + 24 * TRP;
-  double* sLf = sB + VOL;
-  const int ntiles = g.ntx * g.nty * g.ntz;
-  const int tid = threadIdx.x;
-  Tile T;
-  T.sB = sB;
-  T.sLf = sLf;  // written below through the non-const alias
-  tile_geom(T, g, 0);  // lane/warp fields
-  for (int i = tid; i < 4 * 8 * 32; i += kWsThreads) {
-    const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
-    sLf[i] = (&tab->L[0][0][0])[i];
-  }
-  Frags f;
-  Halo h;
-  init_frags(T, op, f, h);
-  __syncthreads();
-  int n = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ++n;
-
-  if (tid >= kCons) {  // ---------------- producers
-    const int ptid = tid - kCons;
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int b = it & 1;
-      if (it >= 2) bar_sync(BAR_EMPTY0 + b, kWsThreads);
-      T.sU = sUbuf[b];
-      T.tr = trbuf[b];
-      tile_geom(T, g, t);
-      T.warp = ptid >> 5;
-      produce<kProd>(T, g, op, u, f, ptid, [] { bar_sync(BAR_PROD, kProd); });
-      bar_arrive(BAR_FULL0 + b, kWsThreads);
-    }
-    for (int j = n - 2 < 0 ? 0 : n - 2; j < n; ++j) bar_sync(BAR_EMPTY0 + (j & 1), kWsThreads);
-    return;
-  }
-  // ---------------- consumers
-  int it = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int b = it & 1;
-    T.sU = sUbuf[b];
-    T.tr = trbuf[b];
-    tile_geom(T, g, t);
-    bar_sync(BAR_FULL0 + b, kWsThreads);
-    xy_stages(T, f, h);
-    bar_sync(BAR_CONS, kCons);
-    load_l(T, f, T.kind[2]);
-    double* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
-    for (int yy = 0; yy < 2; ++yy) {
-      const int y = 2 * T.warp + yy;
-#pragma unroll
-      for (int g8 = 0; g8 < 2; ++g8) {
-        double acc[2][2];
-        z_group(T, f, h, y, 8 * g8, acc);
-        const int x = 8 * g8 + T.r;
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = acc[nb][i];
-      }
-    }
-    bar_sync(BAR_CONS, kCons);  // sB / sU[b] free before the next tile reuses them
-    bar_arrive(BAR_EMPTY0 + b, kWsThreads);
-  }
-}
 
 
 __device__ __forceinline__ void load_frag(const double* tab /* [8][32] */, double (*l)[4], int lane) {
@@ -772,23 +691,6 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
   static const double zero_eig[4 * 256 + 4 * 16] = {0};
   const dm::Tables8* tab = dm::tables8(opd, zero_eig);
   if (!tab) return -3;
-  static const int ws = [] {
-    const char* e = getenv("SUMFACT_B200_DMMA_WS");
-    return (e && *e == '1') ? 1 : 0;  // opt-in: measured slower than two independent CTAs per SM
-  }();
-  if (ws && batch == 1) {
-    cudaError_t err =
-        cudaFuncSetAttribute(dm::k_vmult_dmma8_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemWs);
-    if (err != cudaSuccess) return -3;
-    int sms = 148;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int tiles = g.ntx * g.nty * g.ntz;
-    const int grid = tiles < sms ? tiles : sms;
-    dm::k_vmult_dmma8_ws<<<grid, dm::kWsThreads, dm::kSmemWs, st>>>((const double*)u, (double*)v, g, op, tab);
-    return cudaGetLastError() == cudaSuccess ? 0 : -3;
-  }
   auto kern = dm::k_vmult_dmma8;
   static const int pf = [] {
     const char* e = getenv("SUMFACT_B200_PREFETCH");

@@ -138,13 +138,6 @@ __device__ __forceinline__ bool band_tile(const Geom& g, const Band& bd, int& tx
 template <int K = 8>
 __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz);
 
-__device__ __forceinline__ bool tile_geom(Tile& T, const Geom& g, int tile_id) {
-  if (tile_id >= g.ntx * g.nty * g.ntz) return false;
-  int tx, ty, tz;
-  tile_coords<K>(g, tile_id, tx, ty, tz);
-  tile_fields<8>(T, g, tx, ty, tz);
-  return true;
-}
 
 template <int K>
 __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int ty, int tz) {
@@ -225,42 +218,9 @@ __device__ __forceinline__ void prefetch_tile_rows_l2(const Tile& T, const doubl
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
-__device__ __forceinline__ bool tile_setup(Tile& T, double* smem, const Geom& g, int tile_id) {
-  T.sU = smem;
-  T.sB = smem + VOL;
-  T.tr = T.sB + VOL;
-  T.sLf = T.tr + 12 * TRP;
-  return tile_geom(T, g, tile_id);
-}
 
-// L2 prefetch of the u rows of tile `tile_id` (one 128-byte row per thread, 256 rows): issued
-// ~one wave of CTAs ahead so the tile's own cp.async (and its neighbours' trace loads) hit L2.
-__device__ __forceinline__ void prefetch_tile_l2(const Geom& g, const double* __restrict__ u, int tile_id) {
-  if (tile_id >= g.ntx * g.nty * g.ntz || threadIdx.x >= 256) return;
-  int tx, ty, tz;
-  tile_coords<K>(g, tile_id, tx, ty, tz);
-  const long long sy = (long long)g.nx * K, sz = sy * (long long)g.ny * K;
-  const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
-  const double* p = u + (long long)((g.tz0 + 2 * tz) * K + z) * sz + (long long)((g.ty0 + 2 * ty) * K + y) * sy +
-                    (g.tx0 + 2 * tx) * K;
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
 
-// named barriers (id 0 is __syncthreads)
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
 
-// L_smooth[kind] as per-lane fragments: 4 kinds x 8 (nb,kc) x 32 lanes (conflict-free loads)
-__device__ __forceinline__ void stage_l_frags(const Tile& T, const double* Lsrc /* [4][16][16] */) {
-  double* dst = const_cast<double*>(T.sLf);
-  for (int i = threadIdx.x; i < 4 * 8 * 32; i += kThreads) {
-    const int kind = i >> 8, fr = (i >> 5) & 7, ln = i & 31;
-    const int nb = fr >> 2, kc = fr & 3;
-    dst[i] = Lsrc[kind * 256 + (8 * nb + (ln >> 2)) * 16 + 4 * kc + (ln & 3)];
-  }
-}
 
 __device__ __forceinline__ void load_l(const Tile& T, Frags& f, int kind) {
 #pragma unroll
@@ -269,120 +229,6 @@ __device__ __forceinline__ void load_l(const Tile& T, Frags& f, int kind) {
     for (int kc = 0; kc < 4; ++kc) f.l[nb][kc] = T.sLf[(kind * 8 + nb * 4 + kc) * 32 + T.lane];
 }
 
-// ---------------------------------------------------------------------------
-// Producer side of a tile: cp.async u -> sU (U layout); neighbour face traces
-// (alpha, beta) straight from L2/HBM into tr; then the tangential masses of the
-// y (Mx) and z (My Mx) trace planes on DMMA.  Executed by NP threads (tid in
-// [0, NP)); `bar` synchronises exactly those threads.
-template <int NP, class OpT, class Bar>
-__device__ __forceinline__ void produce(const Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                       const Frags& f, int tid, Bar bar) {
-  const double* ubase = u + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
-  for (int c = tid; c < VOL / 2; c += NP) {
-    const int x2 = c & 7, y = (c >> 3) & 15, z = c >> 7;
-    cp_async16(&T.sU[idxU(z, y, 2 * x2)], ubase + z * T.sz + y * T.sy + 2 * x2);
-  }
-  constexpr int IPT = 512 / NP;  // items per thread per axis (2 faces x 256 positions)
-#pragma unroll
-  for (int axis = 0; axis < 3; ++axis) {
-    double w[IPT][K];
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const int it = tid + NP * j;
-      const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
-      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
-      int X = T.cx * K, Y = T.cy * K, Z = T.cz * K;
-      long long step;
-      if (axis == 0) { Z += p; Y += q; X += hi ? B : -K; step = 1; }
-      else if (axis == 1) { Z += p; X += q; Y += hi ? B : -K; step = T.sy; }
-      else { Y += p; X += q; Z += hi ? B : -K; step = T.sz; }
-      const double* base;
-      if (axis == 2 && (Z < 0 || Z >= g.nz * K)) {
-        base = hi ? reinterpret_cast<const double*>(g.ghost_hi) + (long long)(Z - g.nz * K) * T.sz
-                  : reinterpret_cast<const double*>(g.ghost_lo) + (long long)(Z + K) * T.sz;
-        base += (long long)Y * T.sy + X;
-      } else {
-        base = u + (long long)Z * T.sz + (long long)Y * T.sy + X;
-      }
-      if (axis == 0) {
-#pragma unroll
-        for (int c = 0; c < K / 2; ++c) {
-          const double2 v2 = __ldg(reinterpret_cast<const double2*>(base + 2 * c));
-          w[j][2 * c] = v2.x;
-          w[j][2 * c + 1] = v2.y;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < K; ++c) w[j][c] = __ldg(base + c * step);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const int it = tid + NP * j;
-      const int hi = it >> 8, p = (it >> 4) & 15, q = it & 15;
-      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
-      double alpha, beta = 0.0;
-      if (hi) {
-        alpha = w[j][0];
-#pragma unroll
-        for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[j][c], beta);
-      } else {
-        alpha = w[j][K - 1];
-#pragma unroll
-        for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[j][c], beta);
-      }
-      double* pl = T.tr + (2 * axis + hi) * 2 * TRP;
-      pl[p * TRW + q] = alpha;
-      pl[TRP + p * TRW + q] = beta;
-    }
-  }
-  cp_async_wait_all();
-  bar();
-  // Mx along q on the y-face (2,3) and z-face (4,5) planes: 8 planes x 2 row groups
-  const int pw = tid >> 5;
-  for (int task = pw; task < 16; task += NP / 32) {
-    const int plane = 4 + (task >> 1);
-    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
-    double* P = T.tr + plane * TRP + (task & 1) * 8 * TRW;
-    double a[4];
-#pragma unroll
-    for (int kc = 0; kc < 4; ++kc) a[kc] = P[T.r * TRW + 4 * kc + T.k4];
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    mass_group(f, a, acc);
-    __syncwarp();
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      P[T.r * TRW + 8 * nb + T.c2] = acc[nb][0];
-      P[T.r * TRW + 8 * nb + T.c2 + 1] = acc[nb][1];
-    }
-  }
-  bar();
-  // My along p on the z-face planes: 4 planes x 2 column groups
-  for (int task = pw; task < 8; task += NP / 32) {
-    const int plane = 8 + (task >> 1);
-    if (!((T.nbm >> (plane >> 1)) & 1)) continue;
-    double* P = T.tr + plane * TRP + (task & 1) * 8;
-    double a[4];
-#pragma unroll
-    for (int kc = 0; kc < 4; ++kc) a[kc] = P[(4 * kc + T.k4) * TRW + T.r];
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    mass_group(f, a, acc);
-    __syncwarp();
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      P[(8 * nb + T.c2) * TRW + T.r] = acc[nb][0];
-      P[(8 * nb + T.c2 + 1) * TRW + T.r] = acc[nb][1];
-    }
-  }
-}
-
-// whole CTA as producer (non-specialised kernels)
-template <class OpT>
-__device__ __forceinline__ void prologue(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
-                                         const Frags& f) {
-  produce<kThreads>(T, g, op, u, f, threadIdx.x, [] { __syncthreads(); });
-  __syncthreads();
-}
 
 // rank-2 halo update of a stiffness fragment (lo neighbour -> cell 0, hi -> cell 1)
 struct Halo {
