@@ -202,20 +202,20 @@ def main():
         from paper_2407_09621_b200 import slab
 
         comm = slab.SlabComm()
-        op = slab.DistributedOperator.weak(hier, lvl, comm)  # NCCL K-plane halo + ghosted vmult
+        op = slab.DistributedOperator.weak(hier, lvl, comm)  # NCCL K-plane halo overlapped with the interior
         glo, ghi = op.ghosts(torch.float64)
         grid = _native.SfGrid(n, n, n, glo.data_ptr() if comm.lo is not None else None,
                               ghi.data_ptr() if comm.hi is not None else None)
 
         def step(timed=False):
-            slab.exchange_face_planes(comm, op.slab, u, glo, ghi)
-            if timed:
-                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                ev[0].record()
+            op.apply(u, v, P.FP64)
+
+        def kernel_only(timed=False):  # the vmult kernel alone (ghost planes as left by the last exchange)
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
             vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
-            if timed:
-                ev[1].record()
-                kernel_events.append(ev)
+            ev[1].record()
+            kernel_events.append(ev)
     else:
         grid = hier.grid(lvl)
 
@@ -242,6 +242,10 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        for _ in range(3):
+            kernel_only()
+        torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         if shared:

@@ -64,6 +64,11 @@ const char* sf_last_error(void);
 int sf_vmult(int mode, int k, const sf_grid* grid, const double* level_op, const void* u, void* v, int batch,
              void* stream);
 
+/* v = A u restricted to the cells [z0, z1) along z (even bounds; batch 1): the interior / boundary
+ * split of a z-slab vmult, so the interior overlaps the ghost-plane exchange (slab.py). */
+int sf_vmult_zrange(int mode, int k, const sf_grid* grid, int z0, int z1, const double* level_op, const void* u,
+                    void* v, void* stream);
+
 /* One colour of the multiplicative vertex-patch smoother: x_new = x_old + sum over
  * the colour's patches of P^-1 (b - A x_old)|patch; uncovered cells copied.
  * shift[i] in {0,1} along tensor axis i (x = 0).  x_old != x_new.

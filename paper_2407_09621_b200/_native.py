@@ -48,6 +48,7 @@ def lib():
             "sf_last_error": ([], ctypes.c_char_p),
             "sf_vec_last_error": ([], ctypes.c_char_p),
             "sf_vmult": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_i, c_p], c_i),
+            "sf_vmult_zrange": ([c_i, c_i, P_grid, c_i, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_smooth_colour": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_residual_restrict": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_prolongate_add": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p], c_i),
@@ -70,7 +71,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_smooth_colour", "sf_residual_restrict",
+EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "sf_smooth_colour", "sf_residual_restrict",
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
             "sf_contract")
 

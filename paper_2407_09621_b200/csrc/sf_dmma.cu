@@ -651,11 +651,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* _
 template <int KK>
 static int launch_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   constexpr int CPL = 16 / KK;
-  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
+  // z extent: the caller's tile range [tz0, tz0 + 2 ntz) cells (whole array or a slab sub-range)
+  const int zc = 2 * g0.ntz;
+  if (g0.nx % CPL || g0.ny % CPL || zc % CPL || !offsets32(g0)) return kUseGeneric;
   Geom g = g0;
   g.ntx = g.nx / CPL;
   g.nty = g.ny / CPL;
-  g.ntz = g.nz / CPL;
+  g.ntz = zc / CPL;
   const Tables8* tab = line_tables<KK>(opd);
   if (!tab) return -3;
   auto op = pack_op64<KK>(opd);

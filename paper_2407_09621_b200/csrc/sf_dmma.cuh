@@ -145,10 +145,10 @@ __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int 
   T.cx = g.tx0 + CPL * tx;
   T.cy = g.ty0 + CPL * ty;
   T.cz = g.tz0 + CPL * tz;
-  if constexpr (K < 8) {  // shifted colour: the last line ends at cell n-2 (overlaps its neighbour)
-    T.cx = min(T.cx, g.nx - CPL - g.tx0);
-    T.cy = min(T.cy, g.ny - CPL - g.ty0);
-    T.cz = min(T.cz, g.nz - CPL - g.tz0);
+  if constexpr (K < 8) {  // shifted colour (odd offset): the last line ends at cell n-2 (overlaps its neighbour)
+    if (g.tx0 & 1) T.cx = min(T.cx, g.nx - CPL - g.tx0);
+    if (g.ty0 & 1) T.cy = min(T.cy, g.ny - CPL - g.ty0);
+    if (g.tz0 & 1) T.cz = min(T.cz, g.nz - CPL - g.tz0);
   }
   T.sy = (long long)g.nx * K;
   T.sz = T.sy * (long long)g.ny * K;

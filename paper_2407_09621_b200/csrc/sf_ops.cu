@@ -617,10 +617,15 @@ static bool use_generic() {
 }
 
 template <int K, int MODE>
-static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, void* v, int batch, cudaStream_t st,
+                        int z0 = 0, int z1 = -1) {
   Geom g;
   int rc = make_geom(gr, K, 0, 0, 0, g);
   if (rc) return rc;
+  if (z1 >= 0) {  // tiles of the z-cell range [z0, z1) only (interior / boundary split of a slab)
+    g.tz0 = z0;
+    g.ntz = (z1 - z0) / 2;
+  }
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (!use_generic()) {
       const int r = launch_vmult_dmma8(g, opd, u, v, batch, st);
@@ -842,6 +847,19 @@ int sf_vmult(int mode, int k, const sf_grid* grid, const double* level_op, const
   if (batch < 1) return fail(SF_EINVAL, "batch must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
 #define CALL(K, M) launch_vmult<K, M>(grid, level_op, u, v, batch, st)
+  SF_DISPATCH(k, mode, CALL);
+#undef CALL
+}
+
+int sf_vmult_zrange(int mode, int k, const sf_grid* grid, int z0, int z1, const double* level_op, const void* u,
+                    void* v, void* stream) {
+  int rc = check_common(mode, k);
+  if (rc) return rc;
+  if (!u || !v || !level_op || !grid) return fail(SF_EINVAL, "null pointer");
+  if (z0 < 0 || z1 > grid->nz || z0 >= z1 || (z0 & 1) || (z1 & 1))
+    return fail(SF_EINVAL, "z range must be an even, non-empty subrange of [0, nz)");
+  cudaStream_t st = (cudaStream_t)stream;
+#define CALL(K, M) launch_vmult<K, M>(grid, level_op, u, v, 1, st, z0, z1)
   SF_DISPATCH(k, mode, CALL);
 #undef CALL
 }

@@ -61,10 +61,13 @@ class SlabComm:
     def _staged(self, tensors):
         return self.backend == "gloo" and any(t.is_cuda for t in tensors)
 
-    def exchange(self, send_lo=None, recv_lo=None, send_hi=None, recv_hi=None):
-        """send_lo -> rank-1 (lands in its recv_hi); send_hi -> rank+1 (lands in its recv_lo)."""
+    def exchange_start(self, send_lo=None, recv_lo=None, send_hi=None, recv_hi=None):
+        """Post the neighbour exchange (send_lo -> rank-1's recv_hi, send_hi -> rank+1's recv_lo).
+
+        NCCL: the transfers run on NCCL's stream once the current stream's prior work is done, so
+        kernels enqueued after this call overlap them.  Returns a handle for exchange_finish."""
         if self.world == 1:
-            return
+            return None
         pairs = []
         if self.lo is not None:
             pairs.append((send_lo, recv_lo, self.lo))
@@ -80,10 +83,21 @@ class SlabComm:
                 s, r = snd.contiguous(), rcv
             ops.append(self.dist.P2POp(self.dist.isend, s, self._global(peer), self.group))
             ops.append(self.dist.P2POp(self.dist.irecv, r, self._global(peer), self.group))
-        for req in self.dist.batch_isend_irecv(ops):
+        return self.dist.batch_isend_irecv(ops), back
+
+    def exchange_finish(self, handle):
+        """Make the current stream wait for a posted exchange (and land host-staged receives)."""
+        if handle is None:
+            return
+        reqs, back = handle
+        for req in reqs:
             req.wait()
         for r, rcv in back:
             rcv.copy_(r)
+
+    def exchange(self, send_lo=None, recv_lo=None, send_hi=None, recv_hi=None):
+        """send_lo -> rank-1 (lands in its recv_hi); send_hi -> rank+1 (lands in its recv_lo)."""
+        self.exchange_finish(self.exchange_start(send_lo, recv_lo, send_hi, recv_hi))
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         """In-place SUM over ranks (fixed NCCL/gloo reduction order for a fixed world: deterministic)."""
@@ -224,13 +238,31 @@ class DistributedOperator:
         return g
 
     def apply(self, u: torch.Tensor, v: torch.Tensor, mode: PrecisionMode = PrecisionMode.FP64):
+        """v = A u on the slab.  With neighbours, the ghost-plane exchange overlaps the interior:
+        post the exchange, run the tiles that never read a ghost plane (sf_vmult_zrange over
+        [t, nz - t)), then -- once the planes have landed -- the two boundary tile layers."""
         sl, c = self.slab, self.comm
         glo, ghi = self.ghosts(u.dtype)
-        exchange_face_planes(c, sl, u, glo, ghi)
         grid = _grid(sl.n, sl.nz, glo.data_ptr() if c.lo is not None else None,
                      ghi.data_ptr() if c.hi is not None else None)
-        vmult_device(self.hier, self.level, u, v, mode, grid=grid)
+        t = 16 // sl.K if sl.K in (2, 4) else 2  # tile height in cells (DMMA line tiles for Q1/Q3)
+        if c.world == 1 or sl.nz < 3 * t:
+            exchange_face_planes(c, sl, u, glo, ghi)
+            vmult_device(self.hier, self.level, u, v, mode, grid=grid)
+            return v
+        Kp = sl.K * sl.plane
+        handle = c.exchange_start(send_lo=u[:Kp], recv_lo=glo, send_hi=u[u.numel() - Kp:], recv_hi=ghi)
+        self._zrange(grid, t, sl.nz - t, u, v, mode)
+        c.exchange_finish(handle)
+        self._zrange(grid, 0, t, u, v, mode)
+        self._zrange(grid, sl.nz - t, sl.nz, u, v, mode)
         return v
+
+    def _zrange(self, grid, z0, z1, u, v, mode):
+        lm = self.hier.matrices(self.level)
+        rc = _native.lib().sf_vmult_zrange(mode.code, self.hier.degree, grid, z0, z1, _native.host_ptr(lm.cell_op),
+                                           device.ptr(u), device.ptr(v), device.stream_ptr())
+        _native.check(rc, "sf_vmult_zrange")
 
     def __call__(self, u: torch.Tensor) -> torch.Tensor:
         v = torch.empty_like(u)

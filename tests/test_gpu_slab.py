@@ -8,7 +8,7 @@ from slab_launch import run
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,k,lvl", [(2, 7, 3), (4, 3, 4), (2, 2, 3), (4, 7, 4)])
+@pytest.mark.parametrize("world,k,lvl", [(2, 7, 3), (4, 3, 4), (2, 2, 3), (4, 7, 4), (2, 7, 4), (2, 3, 4)])
 def test_distributed_vmult_and_vcycle_fp64(world, k, lvl):
     res = run(world, "--case", "gpu", "--degree", k, "--level", lvl, "--mode", "fp64")
     for r in res:
