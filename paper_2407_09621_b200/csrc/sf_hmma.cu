@@ -351,28 +351,38 @@ __device__ __forceinline__ void trace_masses_tc(const HTile<MODE>& T, const HTab
 }
 
 // L2 prefetch of this tile's rows of b (read in the z stage of the colour / restriction kernels)
+template <int KK = K>
 __device__ __forceinline__ void prefetch_b_rows(const Geom& g, const float* __restrict__ b) {
   if ((int)blockIdx.x >= g.ntx * g.nty * g.ntz) return;
+  constexpr int CPL = 16 / KK;
   int tx, ty, tz;
-  tile_coords<K>(g, blockIdx.x, tx, ty, tz);
-  const long long sy = (long long)g.nx * K, sz = sy * (long long)g.ny * K;
-  const int cx = g.tx0 + 2 * tx, cy = g.ty0 + 2 * ty, cz = g.tz0 + 2 * tz;
+  tile_coords<8>(g, blockIdx.x, tx, ty, tz);
+  const long long sy = (long long)g.nx * KK, sz = sy * (long long)g.ny * KK;
+  int cx = g.tx0 + CPL * tx, cy = g.ty0 + CPL * ty, cz = g.tz0 + CPL * tz;
+  if (CPL > 2) {
+    if (g.tx0 & 1) cx = min(cx, g.nx - CPL - g.tx0);
+    if (g.ty0 & 1) cy = min(cy, g.ny - CPL - g.ty0);
+    if (g.tz0 & 1) cz = min(cz, g.nz - CPL - g.tz0);
+  }
   for (int r = threadIdx.x; r < 256; r += kThreads) {
-    const float* p = b + (long long)(cz * K + (r >> 4)) * sz + (long long)(cy * K + (r & 15)) * sy + cx * K;
+    const float* p = b + (long long)(cz * KK + (r >> 4)) * sz + (long long)(cy * KK + (r & 15)) * sy + cx * KK;
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
   }
 }
 
 // prologue + x/y stages; leaves c in U and dd in B (f16 tensors), trace planes ready
-template <int MODE>
-__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<K, MODE>& op,
+// KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells); the tile is a
+// 16^3-point box either way, the line operators come from the tables.
+template <int MODE, int KK = K>
+__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<KK, MODE>& op,
                                            const HTables* tab, const float* __restrict__ u) {
   T.uh = reinterpret_cast<__half*>(smem);
   T.bh = T.uh + TVOL;
   T.tr = reinterpret_cast<float*>(smem + sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL);
   if (MODE == MODE_FP16_EC) T.bh = T.uh + TVOL;  // layout: uh | bh | ud | bd
   T.s_exp = reinterpret_cast<int*>(T.tr + 12 * 16 * 17);
-  TileEngine<K, MODE, 1> e(smem, g);
+  constexpr int CPL = 16 / KK;
+  TileEngine<KK, MODE, 1, 16> e(smem, g);
   e.tr = T.tr;
   e.s_exp = T.s_exp;
   int cx, cy, cz;
@@ -387,7 +397,8 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   for (int a = 0; a < 3; ++a) {
     if (e.face_src(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
     if (e.face_src(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
-    T.kind[a] = patch_kind(g, a, c0[a]);
+    const int n = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);  // kind of the 16-point line
+    T.kind[a] = 2 * ((c0[a] == 0 && g.bnd_lo[a]) ? 1 : 0) + ((c0[a] + CPL == n && g.bnd_hi[a]) ? 1 : 0);
   }
   T.lane = threadIdx.x & 31;
   T.warp = threadIdx.x >> 5;
@@ -396,12 +407,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
 #pragma unroll
   for (int hd = 0; hd < 2; ++hd)
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      T.hur[hd][i] = __ldg(&tab->urow[hd][2 * T.t + i]);
-      T.huc[hd][i] = __ldg(&tab->ucol[hd][2 * T.t + i]);
+    for (int i = 0; i < 2; ++i) {  // zero for lanes whose outputs are not in the line's first / last cell
+      const int n0 = 2 * T.t + i, n1 = 2 * T.t + i - (8 - KK);
+      T.hur[hd][i] = n0 < KK ? __ldg(&tab->urow[hd][n0]) : 0.f;
+      T.huc[hd][i] = n1 >= 0 ? __ldg(&tab->ucol[hd][n1]) : 0.f;
     }
   // tile -> registers -> block exponent -> scaled (h, d) tensors
-  const float* ub = u + (long long)(cz * K) * T.sz + (long long)(cy * K) * T.sy + cx * K;
+  const float* ub = u + (long long)(cz * KK) * T.sz + (long long)(cy * KK) * T.sy + cx * KK;
   float4 q4[1024 / kThreads];
   float mx = 0.f;
 #pragma unroll
@@ -518,19 +530,19 @@ __device__ __forceinline__ void z_lines(const HTile<MODE>& T, const HTables* tab
 }
 
 // accumulator element (nt, i): line = g + 8*(i>>1), output = 8nt + 2t + (i&1)
-template <int MODE>
+template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restrict__ u, float* __restrict__ v, Geom g,
-                                                         LevelOp<K, MODE> op, const HTables* __restrict__ tab) {
+                                                         LevelOp<KK, MODE> op, const HTables* __restrict__ tab) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
   u += (long long)blockIdx.y * g.batch_stride;
   v += (long long)blockIdx.y * g.batch_stride;
-  if (!tile_front<MODE>(T, smem, g, op, tab, u)) return;
+  if (!tile_front<MODE, KK>(T, smem, g, op, tab, u)) return;
   __syncthreads();
   BFrag<MODE> bm, bl;
   load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
-  float* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  float* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   const float os = pow2f(-(op.sc.aA + T.eu));
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
@@ -547,19 +559,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
 }
 
 // smoother colour pass (see sf_dmma.cu k_colour_dmma8 for the stage order)
-template <int MODE>
+template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restrict__ xo, const float* __restrict__ b,
-                                                          float* __restrict__ xn, Geom g, LevelOp<K, MODE> op,
+                                                          float* __restrict__ xn, Geom g, LevelOp<KK, MODE> op,
                                                           const HTables* __restrict__ tab) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
-  prefetch_b_rows(g, b);
-  if (!tile_front<MODE>(T, smem, g, op, tab, xo)) return;
+  prefetch_b_rows<KK>(g, b);
+  if (!tile_front<MODE, KK>(T, smem, g, op, tab, xo)) return;
   __syncthreads();
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
   int q, j;
   lane_qj(T.lane, q, j);
-  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   BFrag<MODE> bm, bl, bv;
   load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   load_b<MODE>(bl, &tab->L[kz][0][0][0][0], T.lane);
@@ -825,31 +837,26 @@ static void pack_op_frags(int mode, const double* Op /* [16][16] */, unsigned* d
       }
 }
 
-static HTables build_tables(int mode, const double* opd, const double* eigd) {
+static HTables build_tables(int mode, int KK, const double* opd, const double* eigd) {
   HTables t;
   std::memset(&t, 0, sizeof(t));
-  double Mp[256] = {0};
-  for (int c = 0; c < 2; ++c)
-    for (int i = 0; i < K; ++i)
-      for (int jj = 0; jj < K; ++jj) Mp[(c * K + i) * 16 + c * K + jj] = opd[i * K + jj];
+  double Mp[256], L[4][256], V[4][256], lam[4][16];
+  build_line_ops_host(KK, opd, eigd, Mp, &L[0][0], eigd ? &V[0][0] : nullptr, &lam[0][0]);
   pack_op_frags(mode, Mp, &t.M[0][0][0][0]);
-  double L[4][256];
-  build_patch_l_host(opd, &L[0][0]);
   for (int q = 0; q < 4; ++q) pack_op_frags(mode, L[q], &t.L[q][0][0][0][0]);
   if (eigd) {
     for (int q = 0; q < 4; ++q) {
-      const double* V = eigd + q * 256;
       double VT[256];
       for (int i = 0; i < 16; ++i)
-        for (int jj = 0; jj < 16; ++jj) VT[i * 16 + jj] = V[jj * 16 + i];
+        for (int jj = 0; jj < 16; ++jj) VT[i * 16 + jj] = V[q][jj * 16 + i];
       pack_op_frags(mode, VT, &t.Vf[q][0][0][0][0]);
-      pack_op_frags(mode, V, &t.Vb[q][0][0][0][0]);
-      for (int i = 0; i < 16; ++i) t.lam[q][i] = eigd[4 * 256 + q * 16 + i];
+      pack_op_frags(mode, V[q], &t.Vb[q][0][0][0][0]);
+      for (int i = 0; i < 16; ++i) t.lam[q][i] = lam[q][i];
     }
   }
-  const double* ucol = opd + 2 * K * K;
-  const double* urow = ucol + K;
-  for (int i = 0; i < K; ++i) {
+  const double* ucol = opd + 2 * KK * KK;
+  const double* urow = ucol + KK;
+  for (int i = 0; i < KK; ++i) {
     unsigned short h, d;
     split_host(mode, ucol[i], h, d);
     t.ucol[0][i] = __half2float(*reinterpret_cast<__half*>(&h));
@@ -869,18 +876,20 @@ struct Entry {
 };
 static std::vector<Entry> g_cache;
 
-static const HTables* tables(int mode, const double* opd, const double* eigd) {
+static const HTables* tables(int mode, const double* opd, const double* eigd, int KK = K) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<double> key(opd, opd + 2 * K * K + 4 * K);
-  if (eigd) key.insert(key.end(), eigd, eigd + 4 * 256 + 4 * 16);
+  const int nop = 2 * KK * KK + 4 * KK, neig = 4 * 4 * KK * KK + 4 * 2 * KK;
+  std::vector<double> key(opd, opd + nop);
+  if (eigd) key.insert(key.end(), eigd, eigd + neig);
   key.push_back(eigd ? 1.0 : 0.0);
+  key.push_back((double)KK);
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& e : g_cache)
     if (e.dev == dev && e.mode == mode && e.key == key) return reinterpret_cast<const HTables*>(e.ptr);
   double op_s[2 * K * K + 4 * K], eig_s[4 * 256 + 4 * 16];
-  level_scales(K, opd, eigd, op_s, eigd ? eig_s : nullptr);
-  HTables host = build_tables(mode, op_s, eigd ? eig_s : nullptr);
+  level_scales(KK, opd, eigd, op_s, eigd ? eig_s : nullptr);
+  HTables host = build_tables(mode, KK, op_s, eigd ? eig_s : nullptr);
   void* d = nullptr;
   if (cudaMalloc(&d, sizeof(HTables)) != cudaSuccess) return nullptr;
   if (cudaMemcpy(d, &host, sizeof(HTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
@@ -888,23 +897,23 @@ static const HTables* tables(int mode, const double* opd, const double* eigd) {
   return reinterpret_cast<const HTables*>(d);
 }
 
-template <int MODE>
-static LevelOp<K, MODE> pack_op_h(const double* opd_raw, const double* eig_raw) {
-  Prepared<K, MODE> pr(opd_raw, eig_raw);
+template <int MODE, int KK = K>
+static LevelOp<KK, MODE> pack_op_h(const double* opd_raw, const double* eig_raw) {
+  Prepared<KK, MODE> pr(opd_raw, eig_raw);
   const double* opd = pr.opd;
-  LevelOp<K, MODE> op;
+  LevelOp<KK, MODE> op;
   op.sc = pr.sc;
-  for (int i = 0; i < K; ++i)
-    for (int jj = 0; jj < K; ++jj) {
-      op.M[i][jj] = pack_me<MODE>(opd[i * K + jj]);
-      op.D[i][jj] = pack_me<MODE>(opd[K * K + i * K + jj]);
+  for (int i = 0; i < KK; ++i)
+    for (int jj = 0; jj < KK; ++jj) {
+      op.M[i][jj] = pack_me<MODE>(opd[i * KK + jj]);
+      op.D[i][jj] = pack_me<MODE>(opd[KK * KK + i * KK + jj]);
     }
-  const double* vv = opd + 2 * K * K;
-  for (int i = 0; i < K; ++i) {
+  const double* vv = opd + 2 * KK * KK;
+  for (int i = 0; i < KK; ++i) {
     op.ucol[i] = pack_me<MODE>(vv[i]);
-    op.urow[i] = pack_me<MODE>(vv[K + i]);
-    op.bl[i] = pack_me<MODE>(vv[2 * K + i]);
-    op.br[i] = pack_me<MODE>(vv[3 * K + i]);
+    op.urow[i] = pack_me<MODE>(vv[KK + i]);
+    op.bl[i] = pack_me<MODE>(vv[2 * KK + i]);
+    op.br[i] = pack_me<MODE>(vv[3 * KK + i]);
   }
   return op;
 }
@@ -937,6 +946,52 @@ static int colour(const Geom& g, const double* opd, const double* eigd, const vo
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+
+// Q3 / Q1 (KK = 4, 2): the 16-point tile-line kernels; kUseGeneric when the grid does not tile
+template <int MODE, int KK>
+static int vmult_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  const int zc = 2 * g0.ntz;  // the caller's z range in cells
+  if (g0.nx % CPL || g0.ny % CPL || zc % CPL) return kUseGeneric;
+  Geom g = g0;
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = zc / CPL;
+  const HTables* tab = tables(MODE, opd, nullptr, KK);
+  if (!tab) return -3;
+  auto op = pack_op_h<MODE, KK>(opd, nullptr);
+  if (cudaFuncSetAttribute(k_vmult_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes<MODE>()) != cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_vmult_h8<MODE, KK><<<dim3(tiles, batch), kThreads, smem_bytes<MODE>(), st>>>((const float*)u, (float*)v, g, op,
+                                                                                 tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+template <int MODE, int KK>
+static int colour_line(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
+                       cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
+  const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
+  for (int a = 0; a < 3; ++a)
+    if (s3[a] && n3[a] < CPL + 2) return kUseGeneric;
+  Geom g = g0;
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = g.nz / CPL;
+  const HTables* tab = tables(MODE, opd, eigd, KK);
+  if (!tab) return -3;
+  auto op = pack_op_h<MODE, KK>(opd, eigd);
+  if (cudaFuncSetAttribute(k_colour_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes<MODE>()) != cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_colour_h8<MODE, KK><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)xo, (const float*)b, (float*)xn, g,
+                                                                     op, tab);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
 
 static std::vector<std::pair<std::vector<double>, void*>> g_pcache;
 
@@ -991,6 +1046,26 @@ static int resid_restrict(const Geom& g, const double* opd, const double* embd, 
 }
 
 }  // namespace hm
+
+int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
+                           cudaStream_t st) {
+  const bool ec = mode == MODE_FP16_EC;
+  if (k_nodes == 4) return ec ? hm::vmult_line<MODE_FP16_EC, 4>(g, opd, u, v, batch, st)
+                              : hm::vmult_line<MODE_FP16, 4>(g, opd, u, v, batch, st);
+  if (k_nodes == 2) return ec ? hm::vmult_line<MODE_FP16_EC, 2>(g, opd, u, v, batch, st)
+                              : hm::vmult_line<MODE_FP16, 2>(g, opd, u, v, batch, st);
+  return kUseGeneric;
+}
+
+int launch_colour_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const double* eigd,
+                            const void* xo, const void* b, void* xn, cudaStream_t st) {
+  const bool ec = mode == MODE_FP16_EC;
+  if (k_nodes == 4) return ec ? hm::colour_line<MODE_FP16_EC, 4>(g, opd, eigd, xo, b, xn, st)
+                              : hm::colour_line<MODE_FP16, 4>(g, opd, eigd, xo, b, xn, st);
+  if (k_nodes == 2) return ec ? hm::colour_line<MODE_FP16_EC, 2>(g, opd, eigd, xo, b, xn, st)
+                              : hm::colour_line<MODE_FP16, 2>(g, opd, eigd, xo, b, xn, st);
+  return kUseGeneric;
+}
 
 int launch_vmult_hmma8(int mode, const Geom& g, const double* opd, const void* u, void* v, int batch,
                        cudaStream_t st) {

@@ -112,6 +112,65 @@ inline void build_patch_l_host(const double* opd, double* L /* [4][16][16] */) {
       }
   }
 }
+// host: the 16-point tile-line operators for cell size KK in {2, 4, 8} (16/KK cells per line):
+// L_line[(lb,rb)] = block-tridiagonal (D, rank-2 U / U^T between consecutive cells, Nitsche at the
+// line ends), M_line = blockdiag(M_cell), and the patch transforms / eigenvalues of the line's
+// 16/(2KK) vertex patches (patch j's kind: left boundary only for j = 0, right only for the last).
+inline void build_line_ops_host(int KK, const double* opd, const double* eigd, double* M /*[256]*/,
+                                double* L /*[4][256]*/, double* V /*[4][256] or null*/, double* lam /*[4][16]*/) {
+  const int CPL = 16 / KK, PB = 2 * KK, PPL = 16 / PB;
+  const double* D = opd + KK * KK;
+  const double* ucol = opd + 2 * KK * KK;
+  const double* urow = ucol + KK;
+  const double* bl = urow + KK;
+  const double* br = bl + KK;
+  for (int i = 0; i < 256; ++i) M[i] = 0.0;
+  for (int c = 0; c < CPL; ++c)
+    for (int i = 0; i < KK; ++i)
+      for (int j = 0; j < KK; ++j) M[(c * KK + i) * 16 + c * KK + j] = opd[i * KK + j];
+  for (int q = 0; q < 4; ++q) {
+    double* P = L + q * 256;
+    const int lb = q >> 1, rb = q & 1;
+    for (int i = 0; i < 256; ++i) P[i] = 0.0;
+    for (int c = 0; c < CPL; ++c)
+      for (int i = 0; i < KK; ++i)
+        for (int j = 0; j < KK; ++j) P[(c * KK + i) * 16 + c * KK + j] = D[i * KK + j];
+    for (int c = 0; c + 1 < CPL; ++c) {
+      const int o = c * KK, o2 = (c + 1) * KK;
+      for (int i = 0; i < KK; ++i) {
+        P[(o + i) * 16 + o2] = ucol[i];
+        P[(o + KK - 1) * 16 + o2 + i] = urow[i];
+        P[o2 * 16 + o + i] = ucol[i];
+        P[(o2 + i) * 16 + o + KK - 1] = urow[i];
+      }
+    }
+    if (lb)
+      for (int i = 0; i < KK; ++i) {
+        P[i * 16] += bl[i];
+        if (i > 0) P[i] += bl[i];
+      }
+    if (rb) {
+      const int e = 16 - KK;
+      for (int i = 0; i < KK; ++i) {
+        P[(e + i) * 16 + 15] += br[i];
+        if (i < KK - 1) P[15 * 16 + e + i] += br[i];
+      }
+    }
+    if (V) {
+      double* W = V + q * 256;
+      for (int i = 0; i < 256; ++i) W[i] = 0.0;
+      for (int j = 0; j < PPL; ++j) {
+        const int kind = (j == 0 ? 2 * lb : 0) + (j == PPL - 1 ? rb : 0);
+        const double* Vp = eigd + kind * PB * PB;
+        for (int a = 0; a < PB; ++a) {
+          for (int c = 0; c < PB; ++c) W[(j * PB + a) * 16 + j * PB + c] = Vp[a * PB + c];
+          lam[q * 16 + j * PB + a] = eigd[4 * PB * PB + kind * PB + a];
+        }
+      }
+    }
+  }
+}
+
 // FP64 Q7 vmult on DMMA tensor cores (sf_dmma.cu); returns 0 or SF_ECUDA
 constexpr int kUseGeneric = -4;  // tensor-core launcher declines (falls back to the tile engine)
 int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* level_op, const void* u, void* v, int batch,
@@ -128,6 +187,10 @@ int launch_resid_restrict_dmma8(const Geom& g, const double* level_op, const dou
 // FP16 / FP16-EC Q7 kernels on HMMA (sf_hmma.cu)
 int launch_resid_restrict_hmma8(int mode, const Geom& g, const double* level_op, const double* embedding,
                                 const void* x, const void* b, void* coarse, cudaStream_t st);
+int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* level_op, const void* u, void* v,
+                           int batch, cudaStream_t st);
+int launch_colour_hmma_line(int mode, int k_nodes, const Geom& g, const double* level_op, const double* patch_eig,
+                            const void* x_old, const void* b, void* x_new, cudaStream_t st);
 int launch_vmult_hmma8(int mode, const Geom& g, const double* level_op, const void* u, void* v, int batch,
                        cudaStream_t st);
 int launch_colour_hmma8(int mode, const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,

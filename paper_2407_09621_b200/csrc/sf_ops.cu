@@ -650,6 +650,15 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
       }
     }
   }
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (!use_generic()) {
+      const int r = launch_vmult_hmma_line(MODE, K, g, opd, u, v, batch, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_vmult (hmma line)");
+        return SF_OK;
+      }
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   Prepared<K, MODE> pr(opd, nullptr);
@@ -696,6 +705,15 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
       const int r = launch_colour_dmma_line(K, g, opd, eigd, xo, b, xn, st);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_smooth_colour (dmma line)");
+        done = true;
+      }
+    }
+  }
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (!use_generic()) {
+      const int r = launch_colour_hmma_line(MODE, K, g, opd, eigd, xo, b, xn, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_smooth_colour (hmma line)");
         done = true;
       }
     }

@@ -95,9 +95,12 @@ __device__ __forceinline__ int patch_kind(const Geom& g, int axis, int c0) {
   return 2 * lb + rb;
 }
 
-template <int K, int MODE, int TPC>
+// BL = points per tile line: 2K (2-cell tiles, the generic engine) or 16 (the 16-point line
+// tiles of the tensor-core kernels, 16/K cells; only tile_cells / face_src / traces are used then).
+template <int K, int MODE, int TPC, int BL = 2 * K>
 struct TileEngine {
-  static constexpr int B = 2 * K;
+  static constexpr int B = BL;
+  static constexpr int CPL = BL / K;  // cells per tile line
   static constexpr int P = B + 1;          // padded row pitch (conflict-free x lines)
   static constexpr int VOL = B * B * P;    // one padded tile
   static constexpr int PL = B * P;         // one padded face plane
@@ -134,17 +137,22 @@ struct TileEngine {
     int id = tile0 + t;
     if (id >= ntiles_total) return false;
     int tx, ty, tz;
-    tile_coords<K>(g, id, tx, ty, tz);
-    cx = g.tx0 + 2 * tx;
-    cy = g.ty0 + 2 * ty;
-    cz = g.tz0 + 2 * tz;
+    tile_coords<BL / 2>(g, id, tx, ty, tz);  // band sized by the tile's bytes
+    cx = g.tx0 + CPL * tx;
+    cy = g.ty0 + CPL * ty;
+    cz = g.tz0 + CPL * tz;
+    if constexpr (CPL > 2) {  // shifted colour (odd offset): the last line ends at cell n-2
+      if (g.tx0 & 1) cx = min(cx, g.nx - CPL - g.tx0);
+      if (g.ty0 & 1) cy = min(cy, g.ny - CPL - g.ty0);
+      if (g.tz0 & 1) cz = min(cz, g.nz - CPL - g.tz0);
+    }
     return true;
   }
 
   // 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary
   __device__ __forceinline__ static int face_src(const Geom& g, int axis, int hi, int c0) {
     int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
-    int c = hi ? c0 + 2 : c0 - 1;
+    int c = hi ? c0 + CPL : c0 - 1;
     if (c >= 0 && c < n) return 0;
     if (hi ? g.bnd_hi[axis] : g.bnd_lo[axis]) return 2;
     return 1;
