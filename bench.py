@@ -393,6 +393,11 @@ def extras(sf, hier, lvl, k, u, v):
         for mode in (P.FP64, P.FP16_EC):
             r = solve_once(h6, 6, mode, reps=2)
             res[f"solve_q{k}_l6_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
+        del h6
+        h37 = sf.build_hierarchy(7, 3, max_dofs=2**34)  # Q3 level 7: the other 1.34e8-DoF solve config
+        for mode in (P.FP64, P.FP16_EC):
+            r = solve_once(h37, 7, mode, reps=2)
+            res[f"solve_q3_l7_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
     except Exception as exc:  # secondary measurement only
         res["solve_error"] = repr(exc)[:200]
     return res
