@@ -270,3 +270,17 @@ def test_fused_residual_restriction_q7(mode):
     restrict_device(hier, lvl, bt, out, mode, x=xt)
     err = rel_l2(out.cpu().numpy(), ref)
     assert err <= (1e-12 if mode is P.FP64 else 5e-3 if mode is P.FP16 else 1e-5), err
+
+
+@pytest.mark.parametrize("k", [2, 4, 5, 6])
+def test_cuda_core_degrees_smoother_matches_oracle(k):
+    """Degrees served by the CUDA-core tile engine (K = k+1 does not divide 16): fp64 smoother sweep."""
+    from oracle import port
+
+    lvl = 2 if k > 2 else 3
+    hier = sf.build_hierarchy(lvl, k)
+    D = hier.n_dofs(lvl)
+    x, b = unit(np.random.default_rng(5), D), unit(np.random.default_rng(6), D)
+    got = sf.MultigridPreconditioner(hier).smooth(lvl, x, b)
+    ref = port.VCycle(port.Hierarchy(lvl, k)).smooth(lvl, x, b)
+    assert rel_l2(got, ref) <= 1e-11

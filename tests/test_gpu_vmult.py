@@ -200,3 +200,21 @@ def test_full_size_constants_annihilated_in_interior():
     scale = float(sf.apply_operator(hier, lvl, torch.randn_like(u)).abs().max())
     assert float(inner.abs().max()) <= 1e-12 * scale
     assert float(v.abs().max()) > 1e-6 * scale  # the boundary layer is not zero
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("mode", [P.FP32, P.FP16, P.FP16_EC])
+def test_every_degree_and_mode_against_oracle(k, mode):
+    """Every compiled degree in every low-precision mode (tensor-core line/patch tiles for k = 1, 3, 7,
+    the CUDA-core tile engine otherwise) against the oracle port's own low-precision apply: same
+    per-contraction demotion semantics, so the two error levels agree within a small factor."""
+    lvl = 3 if k <= 3 else 2
+    hier = sf.build_hierarchy(lvl, k)
+    u = np.random.default_rng(k).standard_normal(hier.n_dofs(lvl))
+    H = port.Hierarchy(lvl, k)
+    ref64 = port.apply_operator(H, lvl, u)
+    ref_low = port.apply_operator(H, lvl, u.astype(np.float32), mode.value)
+    v = sf.apply_operator(hier, lvl, u, mode)
+    err, ref_err = rel_l2(v, ref64), rel_l2(ref_low, ref64)
+    assert err <= 3.0 * ref_err + 1e-7, (err, ref_err)
+    assert err >= ref_err / 30.0  # same precision class (not silently fp64)
