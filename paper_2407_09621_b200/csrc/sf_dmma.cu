@@ -353,26 +353,27 @@ struct PTab8 {
   double P[16][8];    // embedding P[fine][coarse]
 };
 
-__global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const double* __restrict__ x,
-                                                                     const double* __restrict__ b,
-                                                                     double* __restrict__ coarse, Geom g,
-                                                                     LevelOp<K, MODE_FP64> op,
-                                                                     const Tables8* __restrict__ tab,
-                                                                     const PTab8* __restrict__ pt, Band bd) {
+template <int KK = 8>
+__global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const double* __restrict__ x,
+                                                                    const double* __restrict__ b,
+                                                                    double* __restrict__ coarse, Geom g,
+                                                                    LevelOp<KK, MODE_FP64> op,
+                                                                    const Tables8* __restrict__ tab,
+                                                                    const PTab8* __restrict__ pt, Band bd) {
   extern __shared__ __align__(128) double smem[];
   Tile T;
   int batch;
-  if (!tile_setup_band(T, smem, g, bd, batch)) return;
-  prefetch_tile_rows_l2(T, b);
-  prefetch_ahead_l2(g, bd, T, x);
+  if (!tile_setup_band<KK>(T, smem, g, bd, batch)) return;
+  prefetch_tile_rows_l2<KK>(T, b);
+  prefetch_ahead_l2<KK>(g, bd, T, x);
   Frags f;
   Halo h;
-  init_frags(T, op, f, h);
-  prologue_fast(T, g, op, x, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
+  init_frags<KK>(T, op, f, h);
+  prologue_fast<KK>(T, g, op, x, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
   xy_stages(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
-  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   load_l(T, f, T.kind[2]);
   double pfr[4];
 #pragma unroll
@@ -426,9 +427,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
     double v[16];
 #pragma unroll
     for (int xx = 0; xx < 16; ++xx) v[xx] = S2[(zc * 8 + yc) * 16 + xx];
-    const long long syc = (long long)(g.nx / 2) * K, szc = syc * (long long)(g.ny / 2) * K;
-    double* out = coarse + (long long)((T.cz / 2) * K + zc) * szc + (long long)((T.cy / 2) * K + yc) * syc +
-                  (T.cx / 2) * K;
+    const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
+    double* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
+                  (T.cx / 2) * KK;
 #pragma unroll
     for (int xc = 0; xc < 8; ++xc) {
       double s = 0.0;
@@ -441,14 +442,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma8(const doub
 
 static std::vector<std::pair<std::vector<double>, void*>> g_ptabs;
 
-static const PTab8* ptables8(const double* embd) {
+// Embedding along a 16-point tile line: blockdiag of the cell-pair embedding P (2KK x KK) over
+// the line's 16 / (2KK) coarse cells -> a 16 x 8 matrix (KK = 8: P itself).
+static const PTab8* ptables8(const double* embd_raw, int KK = 8) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<double> key(embd, embd + 16 * 8);
+  std::vector<double> key(embd_raw, embd_raw + 2 * KK * KK);
   key.push_back((double)dev);
+  key.push_back((double)KK);
   std::lock_guard<std::mutex> lk(g_tab_mu);
   for (auto& e : g_ptabs)
     if (e.first == key) return reinterpret_cast<const PTab8*>(e.second);
+  double embd[16 * 8] = {};
+  for (int c = 0; c < 16 / (2 * KK); ++c)
+    for (int i = 0; i < 2 * KK; ++i)
+      for (int j = 0; j < KK; ++j) embd[(c * 2 * KK + i) * 8 + c * KK + j] = embd_raw[i * KK + j];
   PTab8 host;
   for (int kc = 0; kc < 4; ++kc)
     for (int ln = 0; ln < 32; ++ln) {
@@ -741,6 +749,38 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
 }  // namespace sf
 
 namespace sf {
+namespace dm {
+template <int KK>
+static int launch_restrict_line(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
+                                void* coarse, cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
+  Geom g = g0;
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = g.nz / CPL;
+  const Tables8* tab = line_tables<KK>(opd);
+  const PTab8* pt = ptables8(embd, KK);
+  if (!tab || !pt) return -3;
+  auto op = pack_op64<KK>(opd);
+  if (cudaFuncSetAttribute(k_resid_restrict_dmma<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) !=
+      cudaSuccess)
+    return -3;
+  const Band bd = make_band(g);
+  k_resid_restrict_dmma<KK><<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>(
+      (const double*)x, (const double*)b, (double*)coarse, g, op, tab, pt, bd);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+}  // namespace dm
+
+// FP64 residual + restriction for K = 2 and 4 on DMMA line tiles (kUseGeneric when the grid does not tile)
+int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* opd, const double* embd, const void* x,
+                                    const void* b, void* coarse, cudaStream_t st) {
+  if (k_nodes == 4) return dm::launch_restrict_line<4>(g, opd, embd, x, b, coarse, st);
+  if (k_nodes == 2) return dm::launch_restrict_line<2>(g, opd, embd, x, b, coarse, st);
+  return kUseGeneric;
+}
+
 int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
                                 void* coarse, cudaStream_t st) {
   if (!dm::offsets32(g)) return kUseGeneric;
@@ -750,11 +790,11 @@ int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* 
   const dm::PTab8* pt = dm::ptables8(embd);
   if (!tab || !pt) return -3;
   auto op = dm::pack_op64(opd);
-  if (cudaFuncSetAttribute(dm::k_resid_restrict_dmma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(dm::k_resid_restrict_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)dm::kSmemTile) != cudaSuccess)
     return -3;
   const dm::Band bd = dm::make_band(g);
-  dm::k_resid_restrict_dmma8<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
+  dm::k_resid_restrict_dmma<8><<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
       (const double*)x, (const double*)b, (double*)coarse, g, op, tab, pt, bd);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

@@ -705,22 +705,22 @@ struct HPTab {
   float P[2][16][8];      // [h/d] demoted embedding
 };
 
-template <int MODE>
+template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* __restrict__ x,
                                                                   const float* __restrict__ b,
                                                                   float* __restrict__ coarse, Geom g,
-                                                                  LevelOp<K, MODE> op,
+                                                                  LevelOp<KK, MODE> op,
                                                                   const HTables* __restrict__ tab,
                                                                   const HPTab* __restrict__ pt) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
-  prefetch_b_rows(g, b);
-  if (!tile_front<MODE>(T, smem, g, op, tab, x)) return;
+  prefetch_b_rows<KK>(g, b);
+  if (!tile_front<MODE, KK>(T, smem, g, op, tab, x)) return;
   __syncthreads();
   BFrag<MODE> bm, bl;
   load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
-  const long long off0 = (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
@@ -795,9 +795,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
     Op<MODE> w[16];
 #pragma unroll
     for (int xx = 0; xx < 16; ++xx) w[xx] = prep<MODE>(S2[(zc * 8 + yc) * 16 + xx]);
-    const long long syc = (long long)(g.nx / 2) * K, szc = syc * (long long)(g.ny / 2) * K;
-    float* out = coarse + (long long)((T.cz / 2) * K + zc) * szc + (long long)((T.cy / 2) * K + yc) * syc +
-                 (T.cx / 2) * K;
+    const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
+    float* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
+                 (T.cx / 2) * KK;
     const float back = pow2f(-er);
 #pragma unroll
     for (int xc = 0; xc < 8; ++xc) {
@@ -995,12 +995,17 @@ static int colour_line(const Geom& g0, const double* opd, const double* eigd, co
 
 static std::vector<std::pair<std::vector<double>, void*>> g_pcache;
 
-static const HPTab* ptables(int mode, const double* embd) {
+static const HPTab* ptables(int mode, const double* embd_raw, int KK = K) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<double> key(embd, embd + 16 * 8);
+  std::vector<double> key(embd_raw, embd_raw + 2 * KK * KK);
   key.push_back((double)dev);
   key.push_back((double)mode);
+  key.push_back((double)KK);
+  double embd[16 * 8] = {};  // 16-point tile line -> 8 coarse points: blockdiag of the cell-pair embedding
+  for (int c = 0; c < 16 / (2 * KK); ++c)
+    for (int i = 0; i < 2 * KK; ++i)
+      for (int j = 0; j < KK; ++j) embd[(c * 2 * KK + i) * 8 + c * KK + j] = embd_raw[i * KK + j];
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& e : g_pcache)
     if (e.first == key) return reinterpret_cast<const HPTab*>(e.second);
@@ -1045,6 +1050,28 @@ static int resid_restrict(const Geom& g, const double* opd, const double* embd, 
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+template <int MODE, int KK>
+static int resid_restrict_line(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
+                               void* coarse, cudaStream_t st) {
+  constexpr int CPL = 16 / KK;
+  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
+  Geom g = g0;
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = g.nz / CPL;
+  const HTables* tab = tables(MODE, opd, nullptr, KK);
+  const HPTab* pt = ptables(MODE, embd, KK);
+  if (!tab || !pt) return -3;
+  auto op = pack_op_h<MODE, KK>(opd, nullptr);
+  if (cudaFuncSetAttribute(k_resid_restrict_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes<MODE>()) != cudaSuccess)
+    return -3;
+  const int tiles = g.ntx * g.nty * g.ntz;
+  k_resid_restrict_h8<MODE, KK><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)x, (const float*)b,
+                                                                             (float*)coarse, g, op, tab, pt);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 }  // namespace hm
 
 int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
@@ -1077,6 +1104,16 @@ int launch_colour_hmma8(int mode, const Geom& g, const double* opd, const double
                         void* xn, cudaStream_t st) {
   return mode == MODE_FP16 ? hm::colour<MODE_FP16>(g, opd, eigd, xo, b, xn, st)
                            : hm::colour<MODE_FP16_EC>(g, opd, eigd, xo, b, xn, st);
+}
+
+int launch_resid_restrict_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const double* embd,
+                                    const void* x, const void* b, void* coarse, cudaStream_t st) {
+  const bool ec = mode == MODE_FP16_EC;
+  if (k_nodes == 4) return ec ? hm::resid_restrict_line<MODE_FP16_EC, 4>(g, opd, embd, x, b, coarse, st)
+                              : hm::resid_restrict_line<MODE_FP16, 4>(g, opd, embd, x, b, coarse, st);
+  if (k_nodes == 2) return ec ? hm::resid_restrict_line<MODE_FP16_EC, 2>(g, opd, embd, x, b, coarse, st)
+                              : hm::resid_restrict_line<MODE_FP16, 2>(g, opd, embd, x, b, coarse, st);
+  return kUseGeneric;
 }
 
 int launch_resid_restrict_hmma8(int mode, const Geom& g, const double* opd, const double* embd, const void* x,

@@ -182,9 +182,14 @@ int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* level_op, 
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
                         const void* b, void* x_new, cudaStream_t st);
 // FP64 Q7 residual + restriction on DMMA (sf_dmma.cu)
+int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* embedding,
+                                    const void* x, const void* b, void* coarse, cudaStream_t st);
 int launch_resid_restrict_dmma8(const Geom& g, const double* level_op, const double* embedding, const void* x,
                                 const void* b, void* coarse, cudaStream_t st);
 // FP16 / FP16-EC Q7 kernels on HMMA (sf_hmma.cu)
+int launch_resid_restrict_hmma_line(int mode, int k_nodes, const Geom& g, const double* level_op,
+                                    const double* embedding, const void* x, const void* b, void* coarse,
+                                    cudaStream_t st);
 int launch_resid_restrict_hmma8(int mode, const Geom& g, const double* level_op, const double* embedding,
                                 const void* x, const void* b, void* coarse, cudaStream_t st);
 int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* level_op, const void* u, void* v,

@@ -753,6 +753,24 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
   if (gr->ghost_lo || gr->ghost_hi) {
     // restriction is slab-local (aligned tiles); ghosts only feed the operator
   }
+  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+    if (with_op && !use_generic()) {
+      const int r = launch_resid_restrict_dmma_line(K, g, opd, embd, x, b, coarse, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_residual_restrict (dmma line)");
+        return SF_OK;
+      }
+    }
+  }
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (with_op && !use_generic()) {
+      const int r = launch_resid_restrict_hmma_line(MODE, K, g, opd, embd, x, b, coarse, st);
+      if (r != kUseGeneric) {
+        if (r) return check_launch("sf_residual_restrict (hmma line)");
+        return SF_OK;
+      }
+    }
+  }
   if constexpr (K == 8 && MODE == MODE_FP64) {
     if (with_op && !use_generic()) {
       const int r = launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st);

@@ -248,22 +248,23 @@ def test_ec_solve_keeps_fp64_iteration_count_at_scale(k, lvl):
     assert res[P.FP16_EC][1] <= 1.5 * res[P.FP64][1] + 1e-12
 
 
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (1, 5), (3, 3)])
 @pytest.mark.parametrize("mode", [P.FP64, P.FP16, P.FP16_EC])
-def test_fused_residual_restriction_q7(mode):
-    """sf_residual_restrict with x (tensor-core fused kernel) == restrict(b - A x)."""
+def test_fused_residual_restriction(mode, k, lvl):
+    """sf_residual_restrict with x (the fused tensor-core kernels: Q7 patch tiles, Q3/Q1 line tiles)
+    == restrict(b - A x)."""
     import torch
 
     from oracle import port
     from paper_2407_09621_b200.multigrid import restrict_device
 
-    lvl = 3
-    H = port.Hierarchy(lvl, 7)
+    H = port.Hierarchy(lvl, k)
     rng = np.random.default_rng(17)
     x = unit(rng, H.n_dofs(lvl))
     b = unit(rng, H.n_dofs(lvl))
     r = b - port.apply_operator(H, lvl, x)
     ref = port.restrict(H, lvl, r)
-    hier = sf.build_hierarchy(lvl, 7)
+    hier = sf.build_hierarchy(lvl, k)
     xt = torch.from_numpy(x).to("cuda", mode.torch_dtype)
     bt = torch.from_numpy(b).to("cuda", mode.torch_dtype)
     out = torch.empty(hier.n_dofs(lvl - 1), dtype=mode.torch_dtype, device="cuda")
