@@ -291,7 +291,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
       for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const long long o = off0 + (long long)(8 * nb + c2 + i) * T.sz + (long long)y * T.sy + x;
+          const int z = 8 * nb + c2 + i;
+          if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
+          const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
           xn[o] = __ldg(xo + o) + acc[nb][i];
         }
     }

@@ -96,6 +96,7 @@ struct Tile {
   int kind[3];
   int r, k4, c2, lane, warp;
   int b0;  // banded launch: first tile row of the band
+  int skip[3];  // leading points per axis already written by the previous tile (clamped last line)
 };
 
 // 0: neighbour inside the local array, 1: ghost (z only), 2: domain boundary.
@@ -145,10 +146,17 @@ __device__ __forceinline__ void tile_fields(Tile& T, const Geom& g, int tx, int 
   T.cx = g.tx0 + CPL * tx;
   T.cy = g.ty0 + CPL * ty;
   T.cz = g.tz0 + CPL * tz;
+  T.skip[0] = T.skip[1] = T.skip[2] = 0;
   if constexpr (K < 8) {  // shifted colour (odd offset): the last line ends at cell n-2 (overlaps its neighbour)
+    const int ux = T.cx, uy = T.cy, uz = T.cz;
     if (g.tx0 & 1) T.cx = min(T.cx, g.nx - CPL - g.tx0);
     if (g.ty0 & 1) T.cy = min(T.cy, g.ny - CPL - g.ty0);
     if (g.tz0 & 1) T.cz = min(T.cz, g.nz - CPL - g.tz0);
+    // the overlapped patches were written by the previous line, whose position along the line gave
+    // them different (rounding-level) arithmetic: only one writer, so results are deterministic
+    T.skip[0] = (ux - T.cx) * K;
+    T.skip[1] = (uy - T.cy) * K;
+    T.skip[2] = (uz - T.cz) * K;
   }
   T.sy = (long long)g.nx * K;
   T.sz = T.sy * (long long)g.ny * K;

@@ -195,6 +195,7 @@ struct HTile {
   int kind[3];
   int lane, warp, g, t;
   float hur[2][2], huc[2][2];  // [h/d][i]: urow / ucol at output n = 2t + i of this lane (halo16)
+  int skip[3];                 // line tiles: leading points per axis owned by the previous tile
   __device__ __forceinline__ __half* ud() const { return uh + 2 * TVOL; }
   __device__ __forceinline__ __half* bd() const { return bh + 2 * TVOL; }
 };
@@ -390,6 +391,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
   __syncthreads();
   T.cx = cx; T.cy = cy; T.cz = cz;
+  T.skip[0] = e.skip[0]; T.skip[1] = e.skip[1]; T.skip[2] = e.skip[2];
   T.sy = e.sy; T.sz = e.sz;
   T.nbm = 0;
   const int c0[3] = {cx, cy, cz};
@@ -691,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
         const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
         xn[o] = __ldg(xo + o) + acc.val(nt, i) * cs;
       }

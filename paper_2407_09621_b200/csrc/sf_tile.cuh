@@ -117,6 +117,7 @@ struct TileEngine {
   int eu = 0;  // block exponent of the input tile (binary16 modes), u^ = 2^eu u
   int ntiles_total;
   int tile0;
+  mutable int skip[3] = {0, 0, 0};  // line tiles: leading points per axis owned by the previous tile
   long long sy, sz;
 
   __device__ __forceinline__ TileEngine(char* smem, const Geom& g) {
@@ -142,9 +143,13 @@ struct TileEngine {
     cy = g.ty0 + CPL * ty;
     cz = g.tz0 + CPL * tz;
     if constexpr (CPL > 2) {  // shifted colour (odd offset): the last line ends at cell n-2
+      const int ux = cx, uy = cy, uz = cz;
       if (g.tx0 & 1) cx = min(cx, g.nx - CPL - g.tx0);
       if (g.ty0 & 1) cy = min(cy, g.ny - CPL - g.ty0);
       if (g.tz0 & 1) cz = min(cz, g.nz - CPL - g.tz0);
+      skip[0] = (ux - cx) * K;  // leading points written by the previous line (single writer)
+      skip[1] = (uy - cy) * K;
+      skip[2] = (uz - cz) * K;
     }
     return true;
   }

@@ -285,3 +285,20 @@ def test_cuda_core_degrees_smoother_matches_oracle(k):
     got = sf.MultigridPreconditioner(hier).smooth(lvl, x, b)
     ref = port.VCycle(port.Hierarchy(lvl, k)).smooth(lvl, x, b)
     assert rel_l2(got, ref) <= 1e-11
+
+
+@pytest.mark.parametrize("k,mode", [(7, P.FP64), (7, P.FP16_EC), (3, P.FP64)])
+def test_graph_replayed_vcycle_is_identical(k, mode):
+    """enable_graph(): the captured V-cycle replays the same kernels -> bitwise the eager result."""
+    import torch
+
+    lvl = 4 if k == 3 else 3
+    hier = sf.build_hierarchy(lvl, k)
+    b = torch.from_numpy(unit(np.random.default_rng(9), hier.n_dofs(lvl))).cuda()
+    eager = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).apply(b, lvl)
+    mg = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).enable_graph()
+    for _ in range(2):
+        got = mg.apply(b, lvl)
+        assert torch.equal(got, eager)
+    b2 = torch.from_numpy(unit(np.random.default_rng(10), hier.n_dofs(lvl))).cuda()
+    assert torch.equal(mg.apply(b2, lvl), sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).apply(b2, lvl))

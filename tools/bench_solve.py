@@ -22,11 +22,11 @@ from paper_2407_09621_b200.discretization import assemble_rhs_separable, l2_erro
 from paper_2407_09621_b200.experiments import make_operator  # noqa: E402
 
 
-def solve_once(hier, level, mode, tol=1e-8, reps=2):
+def solve_once(hier, level, mode, tol=1e-8, reps=2, graph=False):
     t0 = time.perf_counter()
     sine = lambda x: np.sin(np.pi * x)
     b = assemble_rhs_separable(hier, level, sine, 3.0 * math.pi**2)
-    mg = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).setup()
+    mg = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).setup().enable_graph(graph)
     A = make_operator(hier, level)
     M = lambda v: mg.apply(v, level)
     M(b)  # warm-up: workspaces, table uploads
@@ -42,7 +42,7 @@ def solve_once(hier, level, mode, tol=1e-8, reps=2):
     l2 = l2_error_separable(hier, level, x, sine)
     return {"degree": hier.degree, "level": level, "dofs": hier.n_dofs(level), "mode": mode.value,
             "iterations": rep.iterations, "solve_s": best, "setup_s": setup, "l2_error": l2,
-            "final_rel_res": rep.final_relative_residual, "converged": rep.converged}
+            "final_rel_res": rep.final_relative_residual, "converged": rep.converged, "cuda_graph": graph}
 
 
 if __name__ == "__main__":
@@ -51,7 +51,8 @@ if __name__ == "__main__":
     ap.add_argument("--level", type=int, default=6)
     ap.add_argument("--modes", default="fp64,fp16_ec,fp16")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--graph", action="store_true", help="replay V-cycles from captured CUDA graphs")
     a = ap.parse_args()
     hier = sf.build_hierarchy(a.level, a.degree, max_dofs=2**34)
     for m in a.modes.split(","):
-        print(json.dumps(solve_once(hier, a.level, sf.PrecisionMode.parse(m), reps=a.reps)), flush=True)
+        print(json.dumps(solve_once(hier, a.level, sf.PrecisionMode.parse(m), reps=a.reps, graph=a.graph)), flush=True)
