@@ -1,12 +1,12 @@
-"""Solve driver (mirror of src/experiments.py:44-103, run_solve)."""
+"""Solve driver and measurement harnesses (mirror of src/experiments.py: run_solve :57-103,
+convergence_study :106-127, error_profile :130-148)."""
 from __future__ import annotations
 
 from dataclasses import dataclass
 
 import torch
 
-from .discretization import (MeshHierarchy, assemble_rhs, build_hierarchy, h1_seminorm_error, l2_error,
-                             sine_product_problem, vmult_device)
+from .discretization import MeshHierarchy, build_hierarchy, sine_product_problem, vmult_device
 from .krylov import fgmres, gmres
 from .multigrid import MultigridPreconditioner, VCycleConfig
 from .precision import PrecisionMode

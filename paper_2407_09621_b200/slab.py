@@ -20,7 +20,6 @@ The numerics per rank are the single-GPU kernels; only the data movement is adde
 """
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -28,7 +27,7 @@ import torch
 
 from . import _native, device
 from .discretization import MeshHierarchy, vmult_device
-from .multigrid import MultigridPreconditioner, VCycleConfig, _native_kinds  # noqa: F401
+from .multigrid import MultigridPreconditioner, VCycleConfig
 from .precision import PrecisionMode
 
 GHOST_CELLS = 2  # smoother halo: a cell's colour update depends on x at most 2 cells away
@@ -418,4 +417,3 @@ def scatter_slab(x_global, comm: SlabComm, sl: SlabLevel) -> torch.Tensor:
 __all__ = ["SlabComm", "SlabLevel", "slab_levels", "DistributedOperator", "DistributedMultigrid",
            "fgmres_distributed", "scatter_slab", "exchange_face_planes", "refresh_ghost_cells", "GHOST_CELLS"]
 
-_ = ctypes  # (ctypes structures come from _native)
