@@ -17,11 +17,14 @@ def test_distributed_vmult_and_vcycle_fp64(world, k, lvl):
         assert r["vcycle_rel_err"] <= 1e-12, r
 
 
-@pytest.mark.parametrize("mode", ["fp16", "fp16_ec", "fp32"])
-def test_distributed_vcycle_low_precision(mode):
-    res = run(2, "--case", "gpu", "--degree", 7, "--level", 3, "--mode", mode)
+@pytest.mark.parametrize("k,lvl,mode", [(7, 3, "fp16"), (7, 3, "fp16_ec"), (7, 3, "fp32"), (3, 5, "fp16_ec"),
+                                        (3, 5, "fp16")])
+def test_distributed_vcycle_low_precision(k, lvl, mode):
+    res = run(2, "--case", "gpu", "--degree", k, "--level", lvl, "--mode", mode)
     for r in res:
-        assert r["vcycle_rel_err"] <= 1e-5, r
+        # (block exponents are per tile; the slab tiling of the extended arrays differs from the
+        # single-GPU one for the line tiles, so agreement is to low-precision rounding)
+        assert r["vcycle_rel_err"] <= (1e-5 if k == 7 else 2e-3 if mode == "fp16" else 1e-5), r
 
 
 @pytest.mark.parametrize("world,k,lvl,mode", [(2, 7, 4, "fp64"), (2, 7, 4, "fp16_ec"), (4, 3, 5, "fp64")])
