@@ -45,6 +45,11 @@ __device__ __forceinline__ int hidx(int z, int y, int x) {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
 __device__ __forceinline__ void ldsm4(unsigned (&r)[4], const __half* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -416,6 +421,25 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     }
   // tile -> registers -> block exponent -> scaled (h, d) tensors
   const float* ub = u + (long long)(cz * KK) * T.sz + (long long)(cy * KK) * T.sy + cx * KK;
+  // EC: the two x-neighbour cell layers (256 rows of KK floats per face) go to the still-free
+  // B tensors by cp.async -- coalesced 16-byte chunks instead of per-lane KK-float loads that
+  // touch 32 cache lines per warp instruction; the x traces are formed from shared memory below.
+  constexpr bool kStageX = (MODE == MODE_FP16_EC) && (KK == 8 || KK == 4);
+  constexpr int XC = KK / 4;  // 16-byte chunks per staged row
+  if constexpr (kStageX) {
+    const int sy = (int)T.sy, sz = (int)T.sz;
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      if (!((T.nbm >> hi) & 1)) continue;
+      float* dst = reinterpret_cast<float*>(hi ? T.bd() : T.bh);
+#pragma unroll
+      for (int k2 = 0; k2 < 256 * XC / kThreads; ++k2) {
+        const int c = threadIdx.x + kThreads * k2, ch = c % XC, row = c / XC, y = row & 15, z = row >> 4;
+        const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;  // conflict-free LDS.128 quarter-warps
+        cp_async16(dst + row * KK + 4 * sw, ub + z * sz + y * sy + (hi ? 16 : -KK) + 4 * ch);
+      }
+    }
+  }
   float4 q4[1024 / kThreads];
   float mx = 0.f;
 #pragma unroll
@@ -426,6 +450,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q4[k2].x), fabsf(q4[k2].y)), fmaxf(fabsf(q4[k2].z), fabsf(q4[k2].w))));
   }
   smax(&T.s_exp[0], mx);
+  if constexpr (kStageX) cp_async_wait_all();
   __syncthreads();
   T.eu = block_exp(__int_as_float(T.s_exp[0]));
   e.eu = T.eu;
@@ -442,7 +467,38 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     *reinterpret_cast<uint2*>(T.uh + o) = hv;
     if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(T.ud() + o) = dv;
   }
-  e.template traces<kThreads>(g, op, u);
+  if constexpr (kStageX) {
+    // x traces from the staged rows: item (hi, p = z, q = y); EC beta in fp32 (as TileEngine::traces)
+#pragma unroll
+    for (int k2 = 0; k2 < 512 / kThreads; ++k2) {
+      const int it = threadIdx.x + kThreads * k2, hi = it >> 8, row = it & 255, p = row >> 4, q = row & 15;
+      if (!((T.nbm >> hi) & 1)) continue;
+      const float* src = reinterpret_cast<const float*>(hi ? T.bd() : T.bh) + row * KK;
+      float w[KK];
+#pragma unroll
+      for (int ch = 0; ch < XC; ++ch) {
+        const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;
+        const float4 v4 = *reinterpret_cast<const float4*>(src + 4 * sw);
+        w[4 * ch] = v4.x; w[4 * ch + 1] = v4.y; w[4 * ch + 2] = v4.z; w[4 * ch + 3] = v4.w;
+      }
+      float alpha, bs = 0.f;
+      if (hi) {
+        alpha = w[0] * us;
+#pragma unroll
+        for (int jj = 1; jj < KK; ++jj) bs = fmaf(op.urow[jj].h + op.urow[jj].d / kEcScale, w[jj] * us, bs);
+      } else {
+        alpha = w[KK - 1] * us;
+#pragma unroll
+        for (int jj = 0; jj < KK - 1; ++jj) bs = fmaf(op.ucol[jj].h + op.ucol[jj].d / kEcScale, w[jj] * us, bs);
+      }
+      float* pl = T.tr + (hi * 2) * (16 * 17);
+      pl[p * 17 + q] = alpha;
+      pl[16 * 17 + p * 17 + q] = bs;
+    }
+    e.template traces<kThreads, 1>(g, op, u);
+  } else {
+    e.template traces<kThreads>(g, op, u);
+  }
   T.lane = threadIdx.x & 31;
   T.warp = threadIdx.x >> 5;
   T.g = T.lane >> 2;

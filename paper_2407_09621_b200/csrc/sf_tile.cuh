@@ -193,13 +193,13 @@ struct TileEngine {
   // ---------------------------------------------------------------- stage 1
   // Face traces of the neighbour cell layers, one axis at a time with all of a
   // thread's loads for that axis in flight before any use (high MLP).
-  template <int NTH = 256>
+  template <int NTH = 256, int FIRST_AXIS = 0>
   __device__ __forceinline__ void traces(const Geom& g, const LevelOp<K, MODE>& op, const S* __restrict__ u) {
     constexpr int ITEMS = TPC * 2 * B * B;  // per axis: 2 faces x B^2 positions per tile
     constexpr int IPT = (ITEMS + NTH - 1) / NTH;
     const C us = uscale();
 #pragma unroll
-    for (int axis = 0; axis < 3; ++axis) {
+    for (int axis = FIRST_AXIS; axis < 3; ++axis) {
       C w[IPT][K];
       bool act[IPT];
 #pragma unroll
