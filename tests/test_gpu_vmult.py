@@ -218,3 +218,21 @@ def test_every_degree_and_mode_against_oracle(k, mode):
     err, ref_err = rel_l2(v, ref64), rel_l2(ref_low, ref64)
     assert err <= 3.0 * ref_err + 1e-7, (err, ref_err)
     assert err >= ref_err / 30.0  # same precision class (not silently fp64)
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 7), (3, 8)])
+def test_full_size_low_precision_error_levels(k, lvl):
+    """1.07e9 DoF: the tensor-core FP16 / FP16-EC / FP32 vmults keep their precision class at the bench
+    size (the power-of-two range management keeps binary16 operands normal), measured against FP64."""
+    hier = sf.build_hierarchy(lvl, k, max_dofs=2**31)
+    g = torch.Generator(device="cuda").manual_seed(21)
+    u64 = torch.randn(hier.n_dofs(lvl), dtype=torch.float64, device="cuda", generator=g)
+    ref = sf.apply_operator(hier, lvl, u64)
+    u32 = u64.float()
+    del u64
+    errs = {}
+    for mode in (P.FP32, P.FP16, P.FP16_EC):
+        v = sf.apply_operator(hier, lvl, u32, mode)
+        errs[mode] = float((v.double() - ref).norm() / ref.norm())
+        del v
+    assert errs[P.FP32] < 1e-5 and errs[P.FP16_EC] < 1e-5 and 1e-5 < errs[P.FP16] < 1e-2, errs
