@@ -88,3 +88,69 @@ def test_krylov_argument_guards():
         sf.fgmres(lambda v: v, None, None)
     with pytest.raises(ValueError):
         sf.gmres(lambda v: v, None, np.ones(3), tol=1.5)
+
+
+def _global_1d(k, L):
+    """The level's 1-D SIPG operator over all cells, rebuilt from the packed cell-wise blocks."""
+    lm = sf.build_hierarchy(L, k).matrices(L)
+    K, n = k + 1, 2**L
+    op = lm.cell_op
+    D = op[K * K:2 * K * K].reshape(K, K)
+    ucol, urow, bl, br = (op[2 * K * K + i * K:2 * K * K + (i + 1) * K] for i in range(4))
+    U = np.zeros((K, K)); U[:, 0] = ucol; U[K - 1, :] = urow
+    Bl = np.zeros((K, K)); Bl[:, 0] = bl; Bl[0, :] = bl
+    Br = np.zeros((K, K)); Br[:, K - 1] = br; Br[K - 1, :] = br
+    A1 = np.zeros((n * K, n * K))
+    for c in range(n):
+        s = slice(c * K, (c + 1) * K)
+        A1[s, s] = D + (Bl if c == 0 else 0) + (Br if c == n - 1 else 0)
+        if c + 1 < n:
+            s2 = slice((c + 1) * K, (c + 2) * K)
+            A1[s, s2], A1[s2, s] = U, U.T
+    return A1, lm
+
+
+@pytest.mark.parametrize("k", [1, 3, 7])
+def test_tile_line_operators_are_principal_submatrices(k):
+    """The tensor-core kernels contract 16-point tile lines (16/K cells) with the block-tridiagonal line
+    operator and couple to the cells outside the line through rank-2 (alpha, beta) halos.  For that to be
+    exact, the line operator must be the principal 16 x 16 submatrix of the global 1-D operator and the
+    coupling to the outside must touch only the face nodes -- checked for every line position."""
+    K = k + 1
+    A1, lm = _global_1d(k, 4)
+    n = 2**4
+    cpl = 16 // K
+    for c0 in range(0, n - cpl + 1, 2 if k == 7 else cpl):
+        s = slice(c0 * K, c0 * K + 16)
+        block = A1[s, s]
+        assert np.allclose(block, block.T)
+        outside = np.delete(A1[s, :], np.r_[s], axis=1)
+        rows, cols = np.nonzero(outside)
+        # only the line's first and last cell couple outside, each through a rank-2 face block
+        assert set(rows) <= set(range(K)) | set(range(16 - K, 16))
+        if outside.any():
+            assert np.linalg.matrix_rank(outside) <= 4
+    # the 2-cell (Q7 patch) line with Nitsche at both ends is L_smooth[(True, True)] at level 1
+    A1b, lmb = _global_1d(k, 1)
+    if k == 7:
+        assert np.allclose(A1b, lmb.L_smooth[(True, True)], atol=1e-12 * np.abs(A1b).max())
+
+
+def test_slab_levels_property_sweep():
+    """Every (max level, world) combination: slabs partition z, are even and >= 2 cells, agree across ranks."""
+    from paper_2407_09621_b200 import slab
+
+    for L in range(1, 7):
+        hier = sf.build_hierarchy(L, 1)
+        for G in (1, 2, 3, 4, 6, 8, 16):
+            per_rank = [slab.slab_levels(hier, r, G) for r in range(G)]
+            lv = sorted(per_rank[0])
+            assert all(sorted(p) == lv for p in per_rank)
+            for lvl in lv:
+                n = hier.n_cells(lvl)
+                nz = [p[lvl].nz for p in per_rank]
+                assert sum(nz) == n and all(z == nz[0] and z % 2 == 0 and z >= 2 for z in nz)
+                assert [p[lvl].z0 for p in per_rank] == list(range(0, n, nz[0]))
+                for p in per_rank:
+                    sl = p[lvl]
+                    assert sl.ext_dofs == sl.local_dofs + (sl.h_lo + sl.h_hi) * sl.cell_layer
