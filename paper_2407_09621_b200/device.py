@@ -53,16 +53,19 @@ def ptr(t: torch.Tensor) -> int:
 
 
 class Scratch:
-    """Per-device scratch for the deterministic reductions."""
+    """Scratch of the deterministic two-pass reductions, one per (device, stream): dots enqueued on
+    different streams never share partial-sum storage."""
 
     _buf: dict = {}
 
     @classmethod
     def dot(cls) -> torch.Tensor:
-        dev = torch.cuda.current_device()
-        if dev not in cls._buf:
-            cls._buf[dev] = torch.empty(_native.SF_DOT_SCRATCH, dtype=torch.float64, device="cuda")
-        return cls._buf[dev]
+        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+        buf = cls._buf.get(key)
+        if buf is None:
+            buf = torch.empty(_native.SF_DOT_SCRATCH, dtype=torch.float64, device="cuda")
+            cls._buf[key] = buf
+        return buf
 
 
 def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -191,7 +191,7 @@ def apply_operator(hier: MeshHierarchy, level: int, u, mode: PrecisionMode = Pre
 
 
 STREAM_MIN_DOFS = 1 << 24
-_STREAM_BUFS: dict = {}
+_STREAM_BUFS: dict = {}  # device staging buffers + streams of the streamed host vmult (one set per device)
 
 
 def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Tensor, mode: PrecisionMode,
@@ -212,7 +212,8 @@ def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Ten
     key = (torch.cuda.current_device(), dt, slab_cells, layer)
     bufs = _STREAM_BUFS.get(key)
     if bufs is None:
-        _STREAM_BUFS.clear()
+        for k_old in [k for k in _STREAM_BUFS if k[0] == key[0]]:  # keep one set per device
+            del _STREAM_BUFS[k_old]
         bufs = {"in": [torch.empty((slab_cells + 2) * layer, dtype=dt, device="cuda") for _ in range(2)],
                 "out": [torch.empty(slab_cells * layer, dtype=dt, device="cuda") for _ in range(2)],
                 "streams": [torch.cuda.Stream() for _ in range(3)]}
