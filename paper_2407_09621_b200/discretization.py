@@ -455,11 +455,12 @@ def assemble_rhs_separable(hier: MeshHierarchy, level: int, f1, scale: float = 1
     return (scale * b1[:, None, None] * b1[None, :, None] * b1[None, None, :]).reshape(-1).contiguous()
 
 
-def _separable_error_sq(hier, level, u_h, mats, factors, slab_cells=8):
+def _separable_error_sq(hier, level, u_h, mats, factors, slab_cells=8, nz=None):
     """sum_q w_q (I u_h - scale * f_z f_y f_x)^2 over k+3-point Gauss points, slab by slab on the device.
 
     mats[a]: (q, K) evaluation matrix along tensor axis a (values or derivatives);
-    factors[a]: the exact 1-D factor along axis a at the n*q points (scale folded into axis 0).
+    factors[a]: the exact 1-D factor along axis a at the n*q points (scale folded into axis 0);
+    nz: cells along z of u_h (a z-slab of the level; factors[2] then covers those nz cells).
     """
     from .basis import gauss_rule
 
@@ -469,9 +470,10 @@ def _separable_error_sq(hier, level, u_h, mats, factors, slab_cells=8):
     Sx, Sy, Sz = (torch.from_numpy(np.ascontiguousarray(m)).cuda() for m in mats)
     fx, fy, fz = (torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).cuda() for f in factors)
     w1 = torch.from_numpy(np.tile(rule.weights, n) * h).cuda()
-    U = u_h.reshape(n, K, n, K, n, K)
+    nzc = n if nz is None else nz
+    U = u_h.reshape(nzc, K, n, K, n, K)
     total = torch.zeros((), dtype=torch.float64, device="cuda")
-    for z0 in range(0, n, slab_cells):
+    for z0 in range(0, nzc, slab_cells):
         blk = U[z0:z0 + slab_cells]
         t = torch.einsum("qk,zkylxm->zqylxm", Sz, blk)
         t = torch.einsum("qk,zaykxm->zayqxm", Sy, t)

@@ -408,6 +408,39 @@ def fgmres_distributed(apply_A, apply_M, b: torch.Tensor, comm: SlabComm, tol=1e
     return _gmres_driver(apply_A, apply_M, b, tol, maxit, True, False, reduce=comm.allreduce_)
 
 
+def run_solve_distributed(degree: int, level: int, comm: SlabComm, mode: PrecisionMode = PrecisionMode.FP64,
+                          tol: float = 1e-8, maxit: int = 100, coarse_level: int = 1, pre_smooth: int = 1,
+                          post_smooth: int = 1, hier: MeshHierarchy | None = None):
+    """experiments.run_solve (experiments.py:57-103) on z-slabs: every rank assembles its slab of the
+    manufactured problem's load vector on the device, FGMRES runs on slab vectors with all-reduced inner
+    products, the preconditioner is the slab V-cycle, and the L2 error is an all-reduced sum of squares.
+    Returns (x_local, SolveReport, l2) on every rank."""
+    import math
+
+    from .discretization import _separable_error_sq, assemble_rhs_separable, build_hierarchy
+    from .basis import gauss_rule, lagrange_values
+
+    hier = hier or build_hierarchy(level, degree, max_dofs=2**34)
+    cfg = VCycleConfig(pre_smooth_steps=pre_smooth, post_smooth_steps=post_smooth, coarse_level=coarse_level,
+                       mode=mode)
+    mg = DistributedMultigrid(hier, cfg, comm, level).setup()
+    op = DistributedOperator(hier, level, comm)
+    sl = mg.slabs[level]
+    sine = lambda x: np.sin(np.pi * x)
+    b = assemble_rhs_separable(hier, level, sine, 3.0 * math.pi**2)[sl.global_slice].contiguous()
+    x, rep = fgmres_distributed(op, mg, b, comm, tol=tol, maxit=maxit)
+    # L2 error: the separable quadrature over this rank's z cells, all-reduced
+    rule = gauss_rule(hier.degree + 3)
+    S = lagrange_values(hier.basis.nodes, rule.points)
+    n, h = hier.n_cells(level), hier.h(level)
+    f = sine((np.arange(n)[:, None] + rule.points[None, :]) * h)
+    part = _separable_error_sq(hier, level, x, (S, S, S), (f, f, f[sl.z0:sl.z0 + sl.nz]), nz=sl.nz).reshape(1)
+    comm.allreduce_(part)
+    l2 = float(torch.sqrt(part))
+    rep.l2_error = l2
+    return x, rep, l2
+
+
 def scatter_slab(x_global, comm: SlabComm, sl: SlabLevel) -> torch.Tensor:
     """This rank's slab of a global vector (numpy or tensor) as a CUDA tensor."""
     t = x_global if isinstance(x_global, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_global))
@@ -415,5 +448,5 @@ def scatter_slab(x_global, comm: SlabComm, sl: SlabLevel) -> torch.Tensor:
 
 
 __all__ = ["SlabComm", "SlabLevel", "slab_levels", "DistributedOperator", "DistributedMultigrid",
-           "fgmres_distributed", "scatter_slab", "exchange_face_planes", "refresh_ghost_cells", "GHOST_CELLS"]
+           "fgmres_distributed", "run_solve_distributed", "scatter_slab", "exchange_face_planes", "refresh_ghost_cells", "GHOST_CELLS"]
 

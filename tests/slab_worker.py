@@ -120,6 +120,11 @@ def gpu_case(args):
         out["solve_rel_err"] = float((xl - ref).norm() / ref.norm())
         out["hist_single"] = [float(h) for h in rep1.residual_history]
         out["hist_dist"] = [float(h) for h in repl.residual_history]
+        # the public distributed driver: same iterations, same L2 error as run_solve
+        ref = sf.run_solve(k, L, mode=mode, hier=hier)
+        _, rep_d, l2_d = slab.run_solve_distributed(k, L, comm, mode=mode, hier=hier)
+        out["run_solve_its"], out["run_solve_dist_its"] = ref.report.iterations, rep_d.iterations
+        out["run_solve_l2"], out["run_solve_dist_l2"] = ref.l2, l2_d
     return out
 
 
