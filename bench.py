@@ -370,15 +370,17 @@ def extras(sf, hier, lvl, k, u, v):
     for mode in (P.FP32, P.FP16, P.FP16_EC):
         ms = timeit(lambda: vmult_device(hier, lvl, u32, v32, mode))
         res[f"vmult_q{k}_l{lvl}_{mode.value}_gdofs"] = D / ms / 1e6
-    del u32, v32
-    # Q3 level 8 fp64 (1.07e9 DoF)
+    # Q3 level 8 (1.07e9 DoF)
     h3 = sf.build_hierarchy(8, 3, max_dofs=2**34, min_level=8)
     ms = timeit(lambda: vmult_device(h3, 8, u, v, P.FP64))
     res["vmult_q3_l8_fp64_gdofs"] = h3.n_dofs(8) / ms / 1e6
-    # smoother colour pass, Q7 level 6, fp64 and fp16
+    ms = timeit(lambda: vmult_device(h3, 8, u32, v32, P.FP32))
+    res["vmult_q3_l8_fp32_gdofs"] = h3.n_dofs(8) / ms / 1e6
+    del u32, v32
+    # smoothing step (8 colour passes), Q7 level 6
     h6 = sf.build_hierarchy(6, k, max_dofs=2**34)
     D6 = h6.n_dofs(6)
-    for mode in (P.FP64, P.FP16):
+    for mode in (P.FP64, P.FP32, P.FP16):
         mg = sf.MultigridPreconditioner(h6, sf.VCycleConfig(mode=mode))
         x = torch.zeros(D6, dtype=mode.torch_dtype, device="cuda")
         b = torch.randn(D6, dtype=mode.torch_dtype, device="cuda")

@@ -2,8 +2,10 @@
 // schedule and the shared-memory layouts.
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "sf_dmma.cuh"
@@ -15,6 +17,17 @@ namespace dm {
 static bool offsets32(const Geom& g) {
   return 24LL * g.nx * g.ny * K * K < 2147483647LL;
 }
+
+// FP32 mode on the DMMA kernels: the operator data is demoted to fp32 values (as the reference's
+// contract_mode casts its matrices, precision.py:206-230) and stays fp64-typed in the tables.
+static const double* demote32(std::vector<double>& buf, const double* p, size_t n) {
+  buf.assign(p, p + n);
+  for (double& x : buf) x = (double)(float)x;
+  return buf.data();
+}
+static size_t op_len(int K) { return 2 * K * K + 4 * K; }
+static size_t eig_len(int K) { return 16 * K * K + 8 * K; }
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 struct PatchL {
   double L[4][B][B];  // L_smooth[kind], kind = 2*left_bnd + right_bnd
@@ -88,7 +101,8 @@ struct Tables8 {
   double lam[4][16];     // generalised eigenvalues per kind
 };
 
-__global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __restrict__ u, double* __restrict__ v,
+template <class S>
+__global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const S* __restrict__ u, S* __restrict__ v,
                                                             Geom g, LevelOp<K, MODE_FP64> op,
                                                             const Tables8* __restrict__ tab, Band bd, int prefetch) {
   extern __shared__ __align__(128) double smem[];
@@ -102,10 +116,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
   Halo h;
   init_frags(T, op, f, h);
   prologue_fast(T, g, op, u, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-  xy_stages(T, f, h);
+  xy_stages<S>(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
-  double* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
+  S* vb = v + (long long)(T.cz * K) * T.sz + (long long)(T.cy * K) * T.sy + T.cx * K;
   for (int yy = 0; yy < 2; ++yy) {
     const int y = 2 * T.warp + yy;
 #pragma unroll
@@ -116,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma8(const double* __res
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = acc[nb][i];
+        for (int i = 0; i < 2; ++i) vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = (S)acc[nb][i];
     }
   }
 }
@@ -146,9 +160,9 @@ __device__ __forceinline__ void full_group(const double (*l)[4], const double* a
 // V_x (registers) | V_y | V_z -> +x_old -> HBM; '|' = shared-memory transpose.
 // KK = 8: one patch per tile line; KK = 4 / 2: a 16-point line holds 2 / 4 patches and the
 // transforms are blockdiag(V_patch) (line tables built per line boundary kind).
-template <int KK = 8>
-__global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __restrict__ xo,
-                                                            const double* __restrict__ b, double* __restrict__ xn,
+template <int KK = 8, class S = double>
+__global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict__ xo,
+                                                            const S* __restrict__ b, S* __restrict__ xn,
                                                             Geom g, LevelOp<KK, MODE_FP64> op,
                                                             const Tables8* __restrict__ tab, Band bd) {
   extern __shared__ __align__(128) double smem[];
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
   Halo h;
   init_frags<KK>(T, op, f, h);
   prologue_fast<KK>(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-  xy_stages(T, f, h);
+  xy_stages<S>(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
 #pragma unroll
         for (int kc = 0; kc < 4; ++kc) {
           const int z = 8 * (kc >> 1) + c2 + (kc & 1);
-          a[kc] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - acc[kc >> 1][kc & 1];
+          a[kc] = rd<S>((double)__ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - acc[kc >> 1][kc & 1]);
         }
         double (*o)[2] = t[yy][g8];
         o[0][0] = o[0][1] = o[1][0] = o[1][1] = 0.0;
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-          for (int i = 0; i < 2; ++i) T.sU[idxT(8 * nb + c2 + i, 2 * w + yy, 8 * g8 + r)] = t[yy][g8][nb][i];
+          for (int i = 0; i < 2; ++i) T.sU[idxT(8 * nb + c2 + i, 2 * w + yy, 8 * g8 + r)] = rd<S>(t[yy][g8][nb][i]);
   }
   __syncthreads();
   // ---- warp-private z' planes: V_y^T | V_x^T, 1/lambda, V_x | V_y
@@ -225,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) T.sU[idxG(z, 8 * nb + c2 + i, 8 * g8 + r)] = o[g8][nb][i];
+        for (int i = 0; i < 2; ++i) T.sU[idxG(z, 8 * nb + c2 + i, 8 * g8 + r)] = rd<S>(o[g8][nb][i]);
     __syncwarp();
     load_frag(&tab->Vf[kx][0][0], V, lane);
     double Vb[2][4];
@@ -243,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         const int x = 8 * (kc >> 1) + c2 + (kc & 1);
-        a[kc] = acc[kc >> 1][kc & 1] / (lzy + __ldg(lamx + x));
+        a[kc] = rd<S>(acc[kc >> 1][kc & 1] / (lzy + __ldg(lamx + x)));
       }
       o[g8][0][0] = o[g8][0][1] = o[g8][1][0] = o[g8][1][1] = 0.0;
       full_group(Vb, a, o[g8]);
@@ -253,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
     for (int g8 = 0; g8 < 2; ++g8)
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
-        *reinterpret_cast<double2*>(&T.sU[idxA(z, 8 * g8 + r, 8 * nb + c2)]) = make_double2(o[g8][nb][0], o[g8][nb][1]);
+        *reinterpret_cast<double2*>(&T.sU[idxA(z, 8 * g8 + r, 8 * nb + c2)]) =
+            make_double2(rd<S>(o[g8][nb][0]), rd<S>(o[g8][nb][1]));
     __syncwarp();
     load_frag(&tab->Vb[ky][0][0], V, lane);
 #pragma unroll
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) T.sU[idxC(z, 8 * nb + c2 + i, 8 * g8 + r)] = o[g8][nb][i];
+        for (int i = 0; i < 2; ++i) T.sU[idxC(z, 8 * nb + c2 + i, 8 * g8 + r)] = rd<S>(o[g8][nb][i]);
     __syncwarp();
   }
   __syncthreads();
@@ -294,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const double* __res
           const int z = 8 * nb + c2 + i;
           if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
           const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
-          xn[o] = __ldg(xo + o) + acc[nb][i];
+          xn[o] = (S)((double)__ldg(xo + o) + rd<S>(acc[nb][i]));
         }
     }
   }
@@ -355,10 +370,10 @@ struct PTab8 {
   double P[16][8];    // embedding P[fine][coarse]
 };
 
-template <int KK = 8>
-__global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const double* __restrict__ x,
-                                                                    const double* __restrict__ b,
-                                                                    double* __restrict__ coarse, Geom g,
+template <int KK = 8, class S = double>
+__global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const S* __restrict__ x,
+                                                                    const S* __restrict__ b,
+                                                                    S* __restrict__ coarse, Geom g,
                                                                     LevelOp<KK, MODE_FP64> op,
                                                                     const Tables8* __restrict__ tab,
                                                                     const PTab8* __restrict__ pt, Band bd) {
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const doubl
   Halo h;
   init_frags<KK>(T, op, f, h);
   prologue_fast<KK>(T, g, op, x, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-  xy_stages(T, f, h);
+  xy_stages<S>(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
   const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
@@ -393,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const doubl
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         const int z = 8 * (kc >> 1) + c2 + (kc & 1);
-        a[kc] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx) - acc[kc >> 1][kc & 1];
+        a[kc] = rd<S>((double)__ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx) - acc[kc >> 1][kc & 1]);
       }
       keep[yy][g8][0] = keep[yy][g8][1] = 0.0;
 #pragma unroll
@@ -407,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const doubl
 #pragma unroll
     for (int g8 = 0; g8 < 2; ++g8)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) S1[(c2 + i) * 258 + (2 * w + yy) * 16 + 8 * g8 + r] = keep[yy][g8][i];
+      for (int i = 0; i < 2; ++i) S1[(c2 + i) * 258 + (2 * w + yy) * 16 + 8 * g8 + r] = rd<S>(keep[yy][g8][i]);
   __syncthreads();
   double* S2 = T.sU;  // [zc][yc][x]
   if (threadIdx.x < 128) {  // y lines (zc, x)
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const doubl
       double s = 0.0;
 #pragma unroll
       for (int y = 0; y < 16; ++y) s = fma(__ldg(&pt->P[y][yc]), v[y], s);
-      S2[(zc * 8 + yc) * 16 + xx] = s;
+      S2[(zc * 8 + yc) * 16 + xx] = rd<S>(s);
     }
   }
   __syncthreads();
@@ -430,14 +445,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const doubl
 #pragma unroll
     for (int xx = 0; xx < 16; ++xx) v[xx] = S2[(zc * 8 + yc) * 16 + xx];
     const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
-    double* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
+    S* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
                   (T.cx / 2) * KK;
 #pragma unroll
     for (int xc = 0; xc < 8; ++xc) {
       double s = 0.0;
 #pragma unroll
       for (int xx = 0; xx < 16; ++xx) s = fma(__ldg(&pt->P[xx][xc]), v[xx], s);
-      out[xc] = s;
+      out[xc] = (S)s;
     }
   }
 }
@@ -602,7 +617,7 @@ static const Tables8* line_colour_tables(const double* opd, const double* eigd) 
 
 template <int KK>
 static int launch_colour_line(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b,
-                              void* xn, cudaStream_t st) {
+                              void* xn, cudaStream_t st, bool f32) {
   constexpr int CPL = 16 / KK;
   if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
   const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
@@ -612,20 +627,29 @@ static int launch_colour_line(const Geom& g0, const double* opd, const double* e
   g.ntx = g.nx / CPL;  // shifted colours: the last line is clamped to end at cell n-2 (tile_fields)
   g.nty = g.ny / CPL;
   g.ntz = g.nz / CPL;
+  std::vector<double> o32, e32;
+  if (f32) {
+    if (!aligned16(xo)) return kUseGeneric;
+    opd = demote32(o32, opd, op_len(KK));
+    eigd = demote32(e32, eigd, eig_len(KK));
+  }
   const Tables8* tab = line_colour_tables<KK>(opd, eigd);
   if (!tab) return -3;
   auto op = pack_op64<KK>(opd);
-  if (cudaFuncSetAttribute(k_colour_dmma<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) !=
-      cudaSuccess)
-    return -3;
-  const Band bd = make_band(g);
-  k_colour_dmma<KK><<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const double*)xo, (const double*)b,
-                                                                           (double*)xn, g, op, tab, bd);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
+      return -3;
+    const Band bd = make_band(g);
+    kern<<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op, tab, bd);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(k_colour_dmma<KK, float>, (const float*)nullptr)
+             : go(k_colour_dmma<KK, double>, (const double*)nullptr);
 }
 
-template <int KK>
-__global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* __restrict__ u, double* __restrict__ v,
+template <int KK, class S>
+__global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const S* __restrict__ u, S* __restrict__ v,
                                                                 Geom g, LevelOp<KK, MODE_FP64> op,
                                                                 const Tables8* __restrict__ tab, Band bd, int prefetch) {
   extern __shared__ __align__(128) double smem[];
@@ -639,10 +663,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* _
   Halo h;
   init_frags<KK>(T, op, f, h);
   prologue_fast<KK>(T, g, op, u, f, &tab->L[0][0][0]);
-  xy_stages(T, f, h);
+  xy_stages<S>(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
-  double* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
+  S* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   for (int yy = 0; yy < 2; ++yy) {
     const int y = 2 * T.warp + yy;
 #pragma unroll
@@ -653,13 +677,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const double* _
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = acc[nb][i];
+        for (int i = 0; i < 2; ++i) vb[(long long)(8 * nb + T.c2 + i) * T.sz + (long long)y * T.sy + x] = (S)acc[nb][i];
     }
   }
 }
 
 template <int KK>
-static int launch_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+static int launch_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st,
+                       bool f32) {
   constexpr int CPL = 16 / KK;
   // z extent: the caller's tile range [tz0, tz0 + 2 ntz) cells (whole array or a slab sub-range)
   const int zc = 2 * g0.ntz;
@@ -668,21 +693,29 @@ static int launch_line(const Geom& g0, const double* opd, const void* u, void* v
   g.ntx = g.nx / CPL;
   g.nty = g.ny / CPL;
   g.ntz = zc / CPL;
+  std::vector<double> o32;
+  if (f32) {
+    if (!aligned16(u)) return kUseGeneric;
+    opd = demote32(o32, opd, op_len(KK));
+  }
   const Tables8* tab = line_tables<KK>(opd);
   if (!tab) return -3;
   auto op = pack_op64<KK>(opd);
-  auto kern = k_vmult_dmma_line<KK>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
-    return -3;
-  const Band bd = make_band(g);
-  const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
-  for (int b0 = 0; b0 < batch; b0 += per) {
-    const int nb = batch - b0 < per ? batch - b0 : per;
-    kern<<<dim3(g.ntx, bd.by, bd.zb * nb), kThreads, kSmemTile, st>>>(
-        (const double*)u + (long long)b0 * g.batch_stride, (double*)v + (long long)b0 * g.batch_stride, g, op, tab, bd,
-        148);
-  }
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
+      return -3;
+    const Band bd = make_band(g);
+    const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
+    for (int b0 = 0; b0 < batch; b0 += per) {
+      const int nb = batch - b0 < per ? batch - b0 : per;
+      kern<<<dim3(g.ntx, bd.by, bd.zb * nb), kThreads, kSmemTile, st>>>(
+          (const S*)u + (long long)b0 * g.batch_stride, (S*)v + (long long)b0 * g.batch_stride, g, op, tab, bd, 148);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(k_vmult_dmma_line<KK, float>, (const float*)nullptr)
+             : go(k_vmult_dmma_line<KK, double>, (const double*)nullptr);
 }
 
 }  // namespace dm
@@ -690,37 +723,47 @@ static int launch_line(const Geom& g0, const double* opd, const void* u, void* v
 // FP64 vmult for K = 2 and 4 on DMMA (16-point tile lines of 16/K cells); kUseGeneric when the
 // local grid is not a multiple of 16/K cells per axis.
 int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
-                           cudaStream_t st) {
-  if (k_nodes == 4) return dm::launch_line<4>(g, opd, u, v, batch, st);
-  if (k_nodes == 2) return dm::launch_line<2>(g, opd, u, v, batch, st);
+                           cudaStream_t st, bool f32) {
+  if (k_nodes == 4) return dm::launch_line<4>(g, opd, u, v, batch, st, f32);
+  if (k_nodes == 2) return dm::launch_line<2>(g, opd, u, v, batch, st, f32);
   return kUseGeneric;
 }
 
-int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st,
+                       bool f32) {
   if (!dm::offsets32(g)) return kUseGeneric;
   static_assert(dm::kSmemTile <= 113 * 1024, "two CTAs per SM");
+  std::vector<double> o32;
+  if (f32) {
+    if (!dm::aligned16(u)) return kUseGeneric;
+    opd = dm::demote32(o32, opd, dm::op_len(8));
+  }
   auto op = dm::pack_op64(opd);
   static const double zero_eig[4 * 256 + 4 * 16] = {0};
   const dm::Tables8* tab = dm::tables8(opd, zero_eig);
   if (!tab) return -3;
-  auto kern = dm::k_vmult_dmma8;
   static const int pf = [] {
     const char* e = getenv("SUMFACT_B200_PREFETCH");
     return e ? atoi(e) : 148;  // one CTA per SM ahead: +2.5% (profiles/r01_vmult_fp64.md)
   }();
 
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
-  if (err != cudaSuccess) return -3;
-  const dm::Band bd = dm::make_band(g);
-  // grid z = (z, band) x batch; split very large batches across launches (gridDim.z <= 65535)
-  const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
-  for (int b0 = 0; b0 < batch; b0 += per) {
-    const int nb = batch - b0 < per ? batch - b0 : per;
-    const double* ub = (const double*)u + (long long)b0 * g.batch_stride;
-    double* vb = (double*)v + (long long)b0 * g.batch_stride;
-    kern<<<dim3(g.ntx, bd.by, bd.zb * nb), dm::kThreads, dm::kSmemTile, st>>>(ub, vb, g, op, tab, bd, pf);
-  }
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
+    if (err != cudaSuccess) return -3;
+    const dm::Band bd = dm::make_band(g);
+    // grid z = (z, band) x batch; split very large batches across launches (gridDim.z <= 65535)
+    const int per = bd.zb > 65535 ? 1 : 65535 / bd.zb;
+    for (int b0 = 0; b0 < batch; b0 += per) {
+      const int nb = batch - b0 < per ? batch - b0 : per;
+      const S* ub = (const S*)u + (long long)b0 * g.batch_stride;
+      S* vb = (S*)v + (long long)b0 * g.batch_stride;
+      kern<<<dim3(g.ntx, bd.by, bd.zb * nb), dm::kThreads, dm::kSmemTile, st>>>(ub, vb, g, op, tab, bd, pf);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(dm::k_vmult_dmma8<float>, (const float*)nullptr)
+             : go(dm::k_vmult_dmma8<double>, (const double*)nullptr);
 }
 
 }  // namespace sf
@@ -728,25 +771,35 @@ int launch_vmult_dmma8(const Geom& g, const double* opd, const void* u, void* v,
 namespace sf {
 // FP64 colour pass for K = 2 and 4 on DMMA (kUseGeneric when the grid does not tile)
 int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* opd, const double* eigd, const void* xo,
-                            const void* b, void* xn, cudaStream_t st) {
-  if (k_nodes == 4) return dm::launch_colour_line<4>(g, opd, eigd, xo, b, xn, st);
-  if (k_nodes == 2) return dm::launch_colour_line<2>(g, opd, eigd, xo, b, xn, st);
+                            const void* b, void* xn, cudaStream_t st, bool f32) {
+  if (k_nodes == 4) return dm::launch_colour_line<4>(g, opd, eigd, xo, b, xn, st, f32);
+  if (k_nodes == 2) return dm::launch_colour_line<2>(g, opd, eigd, xo, b, xn, st, f32);
   return kUseGeneric;
 }
 
 int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool f32) {
   if (!dm::offsets32(g)) return kUseGeneric;
+  std::vector<double> o32, e32;
+  if (f32) {
+    if (!dm::aligned16(xo)) return kUseGeneric;
+    opd = dm::demote32(o32, opd, dm::op_len(8));
+    eigd = dm::demote32(e32, eigd, dm::eig_len(8));
+  }
   const dm::Tables8* tab = dm::tables8(opd, eigd);
   if (!tab) return -3;
   auto op = dm::pack_op64(opd);
-  cudaError_t err =
-      cudaFuncSetAttribute(dm::k_colour_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
-  if (err != cudaSuccess) return -3;
-  const dm::Band bd = dm::make_band(g);
-  dm::k_colour_dmma<8><<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
-      (const double*)xo, (const double*)b, (double*)xn, g, op, tab, bd);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile);
+    if (err != cudaSuccess) return -3;
+    const dm::Band bd = dm::make_band(g);
+    kern<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op,
+                                                                         tab, bd);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(dm::k_colour_dmma<8, float>, (const float*)nullptr)
+             : go(dm::k_colour_dmma<8, double>, (const double*)nullptr);
 }
 }  // namespace sf
 
@@ -754,50 +807,70 @@ namespace sf {
 namespace dm {
 template <int KK>
 static int launch_restrict_line(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
-                                void* coarse, cudaStream_t st) {
+                                void* coarse, cudaStream_t st, bool f32) {
   constexpr int CPL = 16 / KK;
   if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL || !offsets32(g0)) return kUseGeneric;
   Geom g = g0;
   g.ntx = g.nx / CPL;
   g.nty = g.ny / CPL;
   g.ntz = g.nz / CPL;
+  std::vector<double> o32, m32;
+  if (f32) {
+    if (!aligned16(x)) return kUseGeneric;
+    opd = demote32(o32, opd, op_len(KK));
+    embd = demote32(m32, embd, 2 * KK * KK);
+  }
   const Tables8* tab = line_tables<KK>(opd);
   const PTab8* pt = ptables8(embd, KK);
   if (!tab || !pt) return -3;
   auto op = pack_op64<KK>(opd);
-  if (cudaFuncSetAttribute(k_resid_restrict_dmma<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) !=
-      cudaSuccess)
-    return -3;
-  const Band bd = make_band(g);
-  k_resid_restrict_dmma<KK><<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>(
-      (const double*)x, (const double*)b, (double*)coarse, g, op, tab, pt, bd);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
+      return -3;
+    const Band bd = make_band(g);
+    kern<<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const S*)x, (const S*)b, (S*)coarse, g, op, tab,
+                                                                 pt, bd);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(k_resid_restrict_dmma<KK, float>, (const float*)nullptr)
+             : go(k_resid_restrict_dmma<KK, double>, (const double*)nullptr);
 }
 }  // namespace dm
 
 // FP64 residual + restriction for K = 2 and 4 on DMMA line tiles (kUseGeneric when the grid does not tile)
 int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* opd, const double* embd, const void* x,
-                                    const void* b, void* coarse, cudaStream_t st) {
-  if (k_nodes == 4) return dm::launch_restrict_line<4>(g, opd, embd, x, b, coarse, st);
-  if (k_nodes == 2) return dm::launch_restrict_line<2>(g, opd, embd, x, b, coarse, st);
+                                    const void* b, void* coarse, cudaStream_t st, bool f32) {
+  if (k_nodes == 4) return dm::launch_restrict_line<4>(g, opd, embd, x, b, coarse, st, f32);
+  if (k_nodes == 2) return dm::launch_restrict_line<2>(g, opd, embd, x, b, coarse, st, f32);
   return kUseGeneric;
 }
 
 int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
-                                void* coarse, cudaStream_t st) {
+                                void* coarse, cudaStream_t st, bool f32) {
   if (!dm::offsets32(g)) return kUseGeneric;
+  std::vector<double> o32, m32;
+  if (f32) {
+    if (!dm::aligned16(x)) return kUseGeneric;
+    opd = dm::demote32(o32, opd, dm::op_len(8));
+    embd = dm::demote32(m32, embd, 2 * 8 * 8);
+  }
   // L fragments come from the level tables (built without eigenvectors here)
   static const double zero_eig[4 * 256 + 4 * 16] = {0};
   const dm::Tables8* tab = dm::tables8(opd, zero_eig);
   const dm::PTab8* pt = dm::ptables8(embd);
   if (!tab || !pt) return -3;
   auto op = dm::pack_op64(opd);
-  if (cudaFuncSetAttribute(dm::k_resid_restrict_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)dm::kSmemTile) != cudaSuccess)
-    return -3;
-  const dm::Band bd = dm::make_band(g);
-  dm::k_resid_restrict_dmma<8><<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>(
-      (const double*)x, (const double*)b, (double*)coarse, g, op, tab, pt, bd);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kern, auto* ut) {
+    using S = std::remove_const_t<std::remove_pointer_t<decltype(ut)>>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::kSmemTile) != cudaSuccess)
+      return -3;
+    const dm::Band bd = dm::make_band(g);
+    kern<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>((const S*)x, (const S*)b, (S*)coarse, g, op,
+                                                                         tab, pt, bd);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return f32 ? go(dm::k_resid_restrict_dmma<8, float>, (const float*)nullptr)
+             : go(dm::k_resid_restrict_dmma<8, double>, (const double*)nullptr);
 }
 }  // namespace sf

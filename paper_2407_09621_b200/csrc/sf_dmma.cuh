@@ -61,7 +61,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Storage-precision demotion of a contraction output (FP32 mode on the FP64 tensor pipe: every
+// stage result is rounded to fp32 where the reference stores it in the mode's dtype,
+// precision.py:206-230); identity for fp64 storage.
+template <class S>
+__device__ __forceinline__ double rd(double x) {
+  if constexpr (sizeof(S) == 4) return (double)__double2float_rn(x);
+  else return x;
+}
 
 // Operator fragments held by one lane.
 struct Frags {
@@ -197,9 +210,9 @@ __device__ __forceinline__ bool tile_setup_band(Tile& T, double* smem, const Geo
 
 // L2 prefetch of the u rows of the tile two rows ahead in launch order (~2 ntx CTAs later):
 // (tx, ty + 2) inside the band, else the wrapped row of the next z layer.
-template <int K = 8>
+template <int K = 8, class S = double>
 __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd, const Tile& T,
-                                                  const double* __restrict__ u) {
+                                                  const S* __restrict__ u) {
   constexpr int CPL = 16 / K;
   const int ty = (T.cy - g.ty0) / CPL, tz = (T.cz - g.tz0) / CPL;
   const int b0 = T.b0;
@@ -211,18 +224,18 @@ __device__ __forceinline__ void prefetch_ahead_l2(const Geom& g, const Band& bd,
   }
   if (ny < b0 || threadIdx.x >= 256) return;
   const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
-  const double* p = u + (long long)((g.tz0 + CPL * nz) * K + z) * T.sz + (long long)((g.ty0 + CPL * ny) * K + y) * T.sy +
+  const S* p = u + (long long)((g.tz0 + CPL * nz) * K + z) * T.sz + (long long)((g.ty0 + CPL * ny) * K + y) * T.sy +
                     T.cx * K;
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 // L2 prefetch of this tile's rows of a second input (the right-hand side b the colour /
 // restriction kernels read in their z stage): DRAM latency paid during the prologue, not there.
-template <int K = 8>
-__device__ __forceinline__ void prefetch_tile_rows_l2(const Tile& T, const double* __restrict__ p0) {
+template <int K = 8, class S = double>
+__device__ __forceinline__ void prefetch_tile_rows_l2(const Tile& T, const S* __restrict__ p0) {
   if (threadIdx.x >= 256) return;
   const int y = threadIdx.x & 15, z = threadIdx.x >> 4;
-  const double* p = p0 + (long long)(T.cz * K + z) * T.sz + (long long)(T.cy * K + y) * T.sy + T.cx * K;
+  const S* p = p0 + (long long)(T.cz * K + z) * T.sz + (long long)(T.cy * K + y) * T.sy + T.cx * K;
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
@@ -260,6 +273,7 @@ struct Halo {
 };
 
 // x and y stages on the warp's two z planes (in place: U <- a <- c, B <- b <- dd)
+template <class S = double>
 __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h) {
   for (int zz = 0; zz < 2; ++zz) {
     const int z = 2 * T.warp + zz;
@@ -284,8 +298,8 @@ __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
         const int i = idxA(z, y, 8 * nb + T.c2);
-        *reinterpret_cast<double2*>(&T.sU[i]) = make_double2(ra[g8][nb][0], ra[g8][nb][1]);
-        *reinterpret_cast<double2*>(&T.sB[i]) = make_double2(rb[g8][nb][0], rb[g8][nb][1]);
+        *reinterpret_cast<double2*>(&T.sU[i]) = make_double2(rd<S>(ra[g8][nb][0]), rd<S>(ra[g8][nb][1]));
+        *reinterpret_cast<double2*>(&T.sB[i]) = make_double2(rd<S>(rb[g8][nb][0]), rd<S>(rb[g8][nb][1]));
       }
     }
     __syncwarp();
@@ -315,8 +329,8 @@ __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int j = idxC(z, 8 * nb + T.c2 + i, x);
-          T.sU[j] = ra[g8][nb][i];
-          T.sB[j] = rb[g8][nb][i];
+          T.sU[j] = rd<S>(ra[g8][nb][i]);
+          T.sB[j] = rd<S>(rb[g8][nb][i]);
         }
     }
     __syncwarp();
@@ -420,9 +434,10 @@ __device__ __forceinline__ int xs_idx(int row, int c) {
 // one (x, y) position and step only in z (or along the face normal), so each source/destination
 // is one pointer plus a constant stride instead of a fresh 64-bit index computation per element
 // (the prologue was half of the kernel's instructions).
-template <int K = 8, class OpT>
-__device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const double* __restrict__ u,
+template <int K = 8, class S = double, class OpT>
+__device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT& op, const S* __restrict__ u,
                                               const Frags& f, const double* __restrict__ ltab = nullptr) {
+  constexpr bool F32 = sizeof(S) == 4;
   const int tid = threadIdx.x;
   // optional: the L_smooth fragment table (4 kinds x 8 x 32 doubles) -> shared memory, so the
   // stage loops read it with LDS; loads issued here, stored after the trace loads are in flight
@@ -434,86 +449,78 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
   // 32-bit element strides (host guarantees 24 * sz < 2^31): one IMAD.WIDE per address
   const int sy = (int)T.sy, sz = (int)T.sz;
   const long long txy = (long long)(T.cy * K) * sy + T.cx * K;  // tile origin within a z plane
-  const double* ub = u + (long long)(T.cz * K) * sz + txy;
-  {  // tile: chunk (x2 = tid & 7, y = (tid >> 3) & 15, z = (tid >> 7) + 2i)
-    const int x2 = tid & 7, y = (tid >> 3) & 15, z0 = tid >> 7;
-    const double* src = ub + z0 * sz + y * sy + 2 * x2;
-    double* dst = &T.sU[idxU(z0, y, 2 * x2)];
+  const S* ub = u + (long long)(T.cz * K) * sz + txy;
+  // fp32 storage: tile and x-face rows are staged as floats in the still-unused B buffer by
+  // cp.async (16-byte chunks; 8-byte for K = 2, whose shifted tiles are only 8-byte aligned) and
+  // widened to fp64 after the wait; fp64 storage: cp.async straight into the tile / B buffer
+  constexpr int VEC = K == 2 ? 2 : 4, NV = 16 / VEC, LGV = NV == 4 ? 2 : 3;
+  float* stg = reinterpret_cast<float*>(T.sB);  // [0, 4096): tile z*256+y*16+x; then x rows (hi, z, y) x K
+  const int p = (tid >> 4) & 15, q = tid & 15;
+  if constexpr (F32) {
+    const int x = VEC * (tid & (NV - 1)), y = (tid >> LGV) & 15, z0 = tid >> (LGV + 4);
+    const S* src = ub + z0 * sz + y * sy + x;
+    float* dst = stg + z0 * 256 + y * 16 + x;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cp_async16(dst + i * 512, src + 2 * i * sz);
-  }
-  {  // x-neighbour layers: K/2 16-byte chunks per row (hi, z, y); chunk ch = tid % (K/2),
-     // y = (tid / (K/2)) & 15, z = zb + (32/K) k  -- every k step is 512 staged doubles
-    constexpr int KC = K / 2, LG = KC == 4 ? 2 : (KC == 2 ? 1 : 0);
-    const int ch = tid & (KC - 1), y = (tid >> LG) & 15, zb = tid >> (LG + 4);
+    for (int i = 0; i < 16 / VEC; ++i) {
+      if constexpr (VEC == 4) cp_async16(dst + (16 / NV) * i * 256, src + (16 / NV) * i * sz);
+      else cp_async8(dst + (16 / NV) * i * 256, src + (16 / NV) * i * sz);
+    }
+    // x-neighbour rows: chunk ch of row (hi, z, y); K / VEC chunks per row
+    constexpr int RC = K / VEC, LR = RC == 2 ? 1 : 0;
+    const int ch = tid & (RC - 1), yy = (tid >> LR) & 15, zb = tid >> (LR + 4);
+    constexpr int ZS = 256 / (16 * RC);  // z step per pass
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       if (!((T.nbm >> hi) & 1)) continue;
-      const double* src = ub + zb * sz + y * sy + (hi ? B : -K) + 2 * ch;
-      double* dst = &T.sB[xs_idx<K>((hi * 16 + zb) * 16 + y, ch)];
+      const S* s0 = ub + zb * sz + yy * sy + (hi ? B : -K) + VEC * ch;
+      float* d0 = stg + 4096 + ((hi * 16 + zb) * 16 + yy) * K + VEC * ch;
 #pragma unroll
-      for (int k = 0; k < KC; ++k) cp_async16(dst + k * 512, src + (32 / K) * k * sz);
+      for (int k = 0; k < 16 / ZS; ++k) {
+        if constexpr (VEC == 4) cp_async16(d0 + ZS * k * 16 * K, s0 + ZS * k * sz);
+        else cp_async8(d0 + ZS * k * 16 * K, s0 + ZS * k * sz);
+      }
+    }
+  } else {
+    {  // tile: chunk (x2 = tid & 7, y = (tid >> 3) & 15, z = (tid >> 7) + 2i)
+      const int x2 = tid & 7, y = (tid >> 3) & 15, z0 = tid >> 7;
+      const S* src = ub + z0 * sz + y * sy + 2 * x2;
+      double* dst = &T.sU[idxU(z0, y, 2 * x2)];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cp_async16(dst + i * 512, src + 2 * i * sz);
+    }
+    {  // x-neighbour layers: K/2 16-byte chunks per row (hi, z, y); chunk ch = tid % (K/2),
+       // y = (tid / (K/2)) & 15, z = zb + (32/K) k  -- every k step is 512 staged doubles
+      constexpr int KC = K / 2, LG = KC == 4 ? 2 : (KC == 2 ? 1 : 0);
+      const int ch = tid & (KC - 1), y = (tid >> LG) & 15, zb = tid >> (LG + 4);
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        if (!((T.nbm >> hi) & 1)) continue;
+        const S* src = ub + zb * sz + y * sy + (hi ? B : -K) + 2 * ch;
+        double* dst = &T.sB[xs_idx<K>((hi * 16 + zb) * 16 + y, ch)];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) cp_async16(dst + k * 512, src + (32 / K) * k * sz);
+      }
     }
   }
   // y and z faces: item (hi = j, p = (tid >> 4) & 15, q = tid & 15); K values along the normal
-  const int p = (tid >> 4) & 15, q = tid & 15;
   double w1[2][K], w2[2][K];
 #pragma unroll
   for (int hi = 0; hi < 2; ++hi) {
     if ((T.nbm >> (2 + hi)) & 1) {  // y faces: Z = p, X = q, Y = hi ? 16 : -8
-      const double* b1 = ub + p * sz + q + (hi ? B : -K) * sy;
+      const S* b1 = ub + p * sz + q + (hi ? B : -K) * sy;
 #pragma unroll
       for (int c = 0; c < K; ++c) w1[hi][c] = __ldg(b1 + c * sy);
     }
     if ((T.nbm >> (4 + hi)) & 1) {  // z faces: Y = p, X = q, Z = hi ? 16 : -8 (ghost planes past the slab)
-      const double* b2;
+      const S* b2;
       const bool inside = hi ? (T.cz + 16 / K < g.nz) : (T.cz > 0);
       if (inside) b2 = ub + (hi ? B : -K) * sz + p * sy + q;
-      else b2 = reinterpret_cast<const double*>(hi ? g.ghost_hi : g.ghost_lo) + txy + p * sy + q;
+      else b2 = reinterpret_cast<const S*>(hi ? g.ghost_hi : g.ghost_lo) + txy + p * sy + q;
 #pragma unroll
       for (int c = 0; c < K; ++c) w2[hi][c] = __ldg(b2 + c * sz);
     }
   }
-#pragma unroll
-  for (int hi = 0; hi < 2; ++hi) {
-#pragma unroll
-    for (int axis = 1; axis < 3; ++axis) {
-      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
-      const double* w = axis == 1 ? w1[hi] : w2[hi];
-      double alpha, beta = 0.0;
-      if (hi) {
-        alpha = w[0];
-#pragma unroll
-        for (int c = 1; c < K; ++c) beta = fma(op.urow[c].h, w[c], beta);
-      } else {
-        alpha = w[K - 1];
-#pragma unroll
-        for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
-      }
-      double* pl = T.tr + (2 * axis + hi) * 2 * TRP + p * TRW + q;
-      pl[0] = alpha;
-      pl[TRP] = beta;
-    }
-  }
-  if (ltab) {
-    double* dst = const_cast<double*>(T.sLf);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dst[tid + kThreads * i] = lt[i];
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  // x traces from the staged layers: item (hi, p = z, q = y) -> one staged row
-#pragma unroll
-  for (int hi = 0; hi < 2; ++hi) {
-    if (!((T.nbm >> hi) & 1)) continue;
-    const int row = (hi * 16 + p) * 16 + q;
-    double w[K];
-#pragma unroll
-    for (int ch = 0; ch < K / 2; ++ch) {
-      const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx<K>(row, ch)]);
-      w[2 * ch] = v2.x;
-      w[2 * ch + 1] = v2.y;
-    }
+  auto trace = [&](const double* w, int hi, double* pl) {
     double alpha, beta = 0.0;
     if (hi) {
       alpha = w[0];
@@ -524,9 +531,69 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
 #pragma unroll
       for (int c = 0; c < K - 1; ++c) beta = fma(op.ucol[c].h, w[c], beta);
     }
-    double* pl = T.tr + hi * 2 * TRP + p * TRW + q;
     pl[0] = alpha;
-    pl[TRP] = beta;
+    pl[TRP] = rd<S>(beta);
+  };
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+#pragma unroll
+    for (int axis = 1; axis < 3; ++axis) {
+      if (!((T.nbm >> (2 * axis + hi)) & 1)) continue;
+      trace(axis == 1 ? w1[hi] : w2[hi], hi, T.tr + (2 * axis + hi) * 2 * TRP + p * TRW + q);
+    }
+  }
+  if (ltab) {
+    double* dst = const_cast<double*>(T.sLf);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[tid + kThreads * i] = lt[i];
+  }
+  if constexpr (!F32) {
+    cp_async_wait_all();
+    __syncthreads();
+    // x traces from the staged layers: item (hi, p = z, q = y) -> one staged row
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      if (!((T.nbm >> hi) & 1)) continue;
+      const int row = (hi * 16 + p) * 16 + q;
+      double w[K];
+#pragma unroll
+      for (int ch = 0; ch < K / 2; ++ch) {
+        const double2 v2 = *reinterpret_cast<const double2*>(&T.sB[xs_idx<K>(row, ch)]);
+        w[2 * ch] = v2.x;
+        w[2 * ch + 1] = v2.y;
+      }
+      trace(w, hi, T.tr + hi * 2 * TRP + p * TRW + q);
+    }
+  } else {
+    cp_async_wait_all();
+    __syncthreads();
+    {  // widen the staged tile into the U layout
+      const int x = VEC * (tid & (NV - 1)), y = (tid >> LGV) & 15, z0 = tid >> (LGV + 4);
+#pragma unroll
+      for (int i = 0; i < 16 / VEC; ++i) {
+        const int z = z0 + (16 / NV) * i;
+        const float* src = stg + z * 256 + y * 16 + x;
+        double* dst = &T.sU[idxU(z, y, x)];
+#pragma unroll
+        for (int j = 0; j < VEC; j += 2) {
+          const float2 v2 = *reinterpret_cast<const float2*>(src + j);
+          *reinterpret_cast<double2*>(dst + j) = make_double2(v2.x, v2.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      if (!((T.nbm >> hi) & 1)) continue;
+      const float* row = stg + 4096 + ((hi * 16 + p) * 16 + q) * K;
+      double w[K];
+#pragma unroll
+      for (int c = 0; c < K; c += 2) {
+        const float2 v2 = *reinterpret_cast<const float2*>(row + c);
+        w[c] = v2.x;
+        w[c + 1] = v2.y;
+      }
+      trace(w, hi, T.tr + hi * 2 * TRP + p * TRW + q);
+    }
   }
   plane_mass_rows(T, f, 4);
   plane_mass_rows(T, f, 8);

@@ -173,19 +173,22 @@ inline void build_line_ops_host(int KK, const double* opd, const double* eigd, d
 
 // FP64 Q7 vmult on DMMA tensor cores (sf_dmma.cu); returns 0 or SF_ECUDA
 constexpr int kUseGeneric = -4;  // tensor-core launcher declines (falls back to the tile engine)
+// f32: fp32 storage on the same FP64 tensor-core kernels (operator data demoted to fp32 values,
+// stage outputs rounded to fp32); kUseGeneric if a vector is not 16-byte aligned
 int launch_vmult_dmma_line(int k_nodes, const Geom& g, const double* level_op, const void* u, void* v, int batch,
-                           cudaStream_t st);
-int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, void* v, int batch, cudaStream_t st);
+                           cudaStream_t st, bool f32 = false);
+int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, void* v, int batch, cudaStream_t st,
+                       bool f32 = false);
 // FP64 Q7 smoother colour pass on DMMA (sf_dmma.cu)
 int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* patch_eig,
-                            const void* x_old, const void* b, void* x_new, cudaStream_t st);
+                            const void* x_old, const void* b, void* x_new, cudaStream_t st, bool f32 = false);
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
-                        const void* b, void* x_new, cudaStream_t st);
+                        const void* b, void* x_new, cudaStream_t st, bool f32 = false);
 // FP64 Q7 residual + restriction on DMMA (sf_dmma.cu)
 int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* embedding,
-                                    const void* x, const void* b, void* coarse, cudaStream_t st);
+                                    const void* x, const void* b, void* coarse, cudaStream_t st, bool f32 = false);
 int launch_resid_restrict_dmma8(const Geom& g, const double* level_op, const double* embedding, const void* x,
-                                const void* b, void* coarse, cudaStream_t st);
+                                const void* b, void* coarse, cudaStream_t st, bool f32 = false);
 // FP16 / FP16-EC Q7 kernels on HMMA (sf_hmma.cu)
 int launch_resid_restrict_hmma_line(int mode, int k_nodes, const Geom& g, const double* level_op,
                                     const double* embedding, const void* x, const void* b, void* coarse,

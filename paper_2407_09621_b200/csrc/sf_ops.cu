@@ -626,9 +626,9 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
     g.tz0 = z0;
     g.ntz = (z1 - z0) / 2;
   }
-  if constexpr (K == 8 && MODE == MODE_FP64) {
+  if constexpr (K == 8 && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (!use_generic()) {
-      const int r = launch_vmult_dmma8(g, opd, u, v, batch, st);
+      const int r = launch_vmult_dmma8(g, opd, u, v, batch, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {  // (declined: local array too large for 32-bit tile offsets)
         if (r) return check_launch("sf_vmult (dmma)");
         return SF_OK;
@@ -641,9 +641,9 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
       return SF_OK;
     }
   }
-  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (!use_generic()) {
-      const int r = launch_vmult_dmma_line(K, g, opd, u, v, batch, st);
+      const int r = launch_vmult_dmma_line(K, g, opd, u, v, batch, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_vmult (dmma line)");
         return SF_OK;
@@ -691,18 +691,18 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
     return SF_OK;
   }
   bool done = false;
-  if constexpr (K == 8 && MODE == MODE_FP64) {
+  if constexpr (K == 8 && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (!use_generic()) {
-      const int r = launch_colour_dmma8(g, opd, eigd, xo, b, xn, st);
+      const int r = launch_colour_dmma8(g, opd, eigd, xo, b, xn, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_smooth_colour (dmma)");
         done = true;
       }
     }
   }
-  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (!use_generic()) {
-      const int r = launch_colour_dmma_line(K, g, opd, eigd, xo, b, xn, st);
+      const int r = launch_colour_dmma_line(K, g, opd, eigd, xo, b, xn, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_smooth_colour (dmma line)");
         done = true;
@@ -753,9 +753,9 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
   if (gr->ghost_lo || gr->ghost_hi) {
     // restriction is slab-local (aligned tiles); ghosts only feed the operator
   }
-  if constexpr ((K == 4 || K == 2) && MODE == MODE_FP64) {
+  if constexpr ((K == 4 || K == 2) && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (with_op && !use_generic()) {
-      const int r = launch_resid_restrict_dmma_line(K, g, opd, embd, x, b, coarse, st);
+      const int r = launch_resid_restrict_dmma_line(K, g, opd, embd, x, b, coarse, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_residual_restrict (dmma line)");
         return SF_OK;
@@ -771,9 +771,9 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
       }
     }
   }
-  if constexpr (K == 8 && MODE == MODE_FP64) {
+  if constexpr (K == 8 && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (with_op && !use_generic()) {
-      const int r = launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st);
+      const int r = launch_resid_restrict_dmma8(g, opd, embd, x, b, coarse, st, MODE == MODE_FP32);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_residual_restrict (dmma)");
         return SF_OK;
