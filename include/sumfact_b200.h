@@ -18,6 +18,8 @@
  * Vectors: flat lexicographic (z, y, x) arrays, x fastest, exactly the
  * reference layout (discretization.py:93-100, 135-145).  Storage dtype is
  * double for mode 0 (fp64) and float for modes 1..3 (precision.py:36-39).
+ * Vector pointers and ghost planes must be 16-byte aligned (vector loads and
+ * cp.async chunks; cudaMalloc / torch give 256); SF_EINVAL otherwise.
  * Modes: 0 fp64, 1 fp32, 2 fp16, 3 fp16_ec (precision.py:29-33, 206-230).
  * Degrees: k = 1..SF_MAX_DEGREE (K = k+1 nodes per cell and axis).
  */

@@ -1,6 +1,7 @@
 // Operator kernels (vmult, smoother colour pass, residual+restriction,
 // prolongation+add) and their C-ABI entry points.  See include/sumfact_b200.h
 // for the contract and the reference interface each entry point replaces.
+#include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 
@@ -869,6 +870,17 @@ static int check_common(int mode, int k) {
   return SF_OK;
 }
 
+// vectors are read with 16-byte vector loads / cp.async chunks: every vector pointer (and ghost plane) must be
+// 16-byte aligned (cudaMalloc and torch allocations are 256-byte aligned)
+static bool misaligned(const void* p) { return ((uintptr_t)p & 15) != 0; }
+static bool misaligned_grid(const sf_grid* g) { return g && (misaligned(g->ghost_lo) || misaligned(g->ghost_hi)); }
+#define SF_ALIGNED(...)                                                                      \
+  do {                                                                                       \
+    const void* ps_[] = {__VA_ARGS__};                                                       \
+    for (const void* p_ : ps_)                                                               \
+      if (misaligned(p_)) return fail(SF_EINVAL, "vectors must be 16-byte aligned");         \
+  } while (0)
+
 extern "C" {
 
 int sf_abi_version(void) { return SF_ABI_VERSION; }
@@ -880,6 +892,8 @@ int sf_vmult(int mode, int k, const sf_grid* grid, const double* level_op, const
   int rc = check_common(mode, k);
   if (rc) return rc;
   if (!u || !v || !level_op) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(u, v);
+  if (misaligned_grid(grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
   if (batch < 1) return fail(SF_EINVAL, "batch must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
 #define CALL(K, M) launch_vmult<K, M>(grid, level_op, u, v, batch, st)
@@ -892,6 +906,8 @@ int sf_vmult_zrange(int mode, int k, const sf_grid* grid, int z0, int z1, const 
   int rc = check_common(mode, k);
   if (rc) return rc;
   if (!u || !v || !level_op || !grid) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(u, v);
+  if (misaligned_grid(grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
   if (z0 < 0 || z1 > grid->nz || z0 >= z1 || (z0 & 1) || (z1 & 1))
     return fail(SF_EINVAL, "z range must be an even, non-empty subrange of [0, nz)");
   cudaStream_t st = (cudaStream_t)stream;
@@ -905,6 +921,8 @@ int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, con
   int rc = check_common(mode, k);
   if (rc) return rc;
   if (!shift || !x_old || !b || !x_new || !level_op || !patch_eig) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(x_old, b, x_new);
+  if (misaligned_grid(grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
   for (int i = 0; i < 3; ++i)
     if (shift[i] != 0 && shift[i] != 1) return fail(SF_EINVAL, "shift entries must be 0 or 1");
   if (x_old == x_new) return fail(SF_EINVAL, "x_old and x_new must be distinct buffers");
@@ -919,6 +937,8 @@ int sf_residual_restrict(int mode, int k, const sf_grid* fine_grid, const double
   int rc = check_common(mode, k);
   if (rc) return rc;
   if (!b || !coarse || !embedding) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(x, b, coarse);
+  if (misaligned_grid(fine_grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
   int with_op = x != nullptr;
   if (with_op && !level_op) return fail(SF_EINVAL, "level_op required with x");
   cudaStream_t st = (cudaStream_t)stream;
@@ -934,6 +954,7 @@ int sf_prolongate_add(int mode, int k, const sf_grid* coarse_grid, const double*
   int rc = check_common(mode, k);
   if (rc) return rc;
   if (!e || !fine || !embedding) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(e, fine);
   cudaStream_t st = (cudaStream_t)stream;
 #define CALL(K, M) launch_prolong_add<K, M>(coarse_grid, embedding, e, fine, st)
   SF_DISPATCH(k, mode, CALL);

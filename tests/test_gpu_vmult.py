@@ -236,3 +236,44 @@ def test_full_size_low_precision_error_levels(k, lvl):
         errs[mode] = float((v.double() - ref).norm() / ref.norm())
         del v
     assert errs[P.FP32] < 1e-5 and errs[P.FP16_EC] < 1e-5 and 1e-5 < errs[P.FP16] < 1e-2, errs
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (1, 5)])
+def test_fp32_dmma_path_matches_cuda_core_fp32(tmp_path, k, lvl):
+    """FP32 storage on the DMMA kernels (stage outputs rounded to fp32) vs the CUDA-core engine's float
+    arithmetic: both within fp32 rounding of each other and of the fp64 operator."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); import paper_2407_09621_b200 as sf; "
+            f"h = sf.build_hierarchy({lvl}, {k}); u = np.random.default_rng(11).standard_normal(h.n_dofs({lvl})); "
+            f"np.save(%r, sf.apply_operator(h, {lvl}, u, sf.PrecisionMode.FP32))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"v{flag}.npy")
+        subprocess.run([sys.executable, "-c", code % (root, path)], check=True,
+                       env=dict(os.environ, SUMFACT_B200_GENERIC=flag))
+        outs.append(np.load(path).astype(np.float64))
+    hier = sf.build_hierarchy(lvl, k)
+    ref64 = sf.apply_operator(hier, lvl, np.random.default_rng(11).standard_normal(hier.n_dofs(lvl)))
+    assert rel_l2(outs[0], outs[1]) <= 2e-6
+    assert rel_l2(outs[0], ref64) <= rel_l2(outs[1], ref64) * 2.0 + 1e-7
+
+
+def test_misaligned_vectors_are_rejected():
+    """Vectors feed 16-byte vector loads / cp.async chunks: a pointer that is not 16-byte aligned is an
+    SF_EINVAL (ValueError), not a device fault."""
+    from paper_2407_09621_b200.discretization import vmult_device
+
+    hier = sf.build_hierarchy(3, 7)
+    D = hier.n_dofs(3)
+    for mode in (P.FP32, P.FP64):
+        base = torch.randn(D + 1, dtype=mode.torch_dtype, device="cuda")
+        v = torch.empty(D, dtype=mode.torch_dtype, device="cuda")
+        with pytest.raises(ValueError, match="16-byte aligned"):
+            vmult_device(hier, 3, base[1:], v, mode)
+    torch.cuda.synchronize()  # no sticky device error
+    u = torch.randn(D, dtype=torch.float32, device="cuda")
+    assert torch.isfinite(sf.apply_operator(hier, 3, u, P.FP32)).all()
