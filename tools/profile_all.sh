@@ -14,5 +14,7 @@ run k_colour_h8 colour_q7_ec "--degree 7 --level 6 --mode fp16_ec --what colour 
 run k_colour_h8 colour_q3_ec "--degree 3 --level 7 --mode fp16_ec --what colour --reps 1"
 run k_resid_restrict vcycle_restrict_q7_fp64 "--degree 7 --level 6 --mode fp64 --what vcycle --reps 1"
 run k_prolong_add vcycle_prolong_q7_fp64 "--degree 7 --level 6 --mode fp64 --what vcycle --reps 1"
-run k_vmult fp32_vmult_q7 "--degree 7 --level 7 --mode fp32 --reps 1"
+run k_vmult_dmma8 vmult_q7_fp32 "--degree 7 --level 7 --mode fp32 --reps 1"
+run k_vmult_dmma_line vmult_q3_fp32 "--degree 3 --level 8 --mode fp32 --reps 1"
+run k_colour_dmma colour_q7_fp32 "--degree 7 --level 6 --mode fp32 --what colour --reps 1"
 echo done
