@@ -9,7 +9,8 @@ __version__ = "0.1.0"
 from .precision import PrecisionMode, relative_error  # noqa: F401
 from .core import contract_batch, contract_mode  # noqa: F401
 from .discretization import (MeshHierarchy, build_hierarchy, apply_operator, materialize_operator,  # noqa: F401
-                             assemble_rhs, interpolate, l2_error, h1_seminorm_error, sine_product_problem)
+                             assemble_rhs, interpolate, l2_error, h1_seminorm_error, sine_product_problem,
+                             save_vector, load_vector)
 from .multigrid import (MultigridPreconditioner, VCycleConfig, PatchSolver, default_ordering,  # noqa: F401
                         restrict, prolongate, patch_inverse_apply)
 from .krylov import fgmres, gmres, SolveReport  # noqa: F401

@@ -406,6 +406,39 @@ def h1_seminorm_error(hier: MeshHierarchy, level: int, u_h, grad_exact, quad_poi
     return math.sqrt(total)
 
 
+
+# ---------------------------------------------------------- serialization (discretization.py:462-488)
+
+
+def save_vector(path, u, fmt: str = "csv"):
+    """discretization.py:465-476: CSV ``index,value`` rows (17 significant digits) or flat f64 binary.
+    Accepts numpy arrays and torch tensors (CUDA tensors are read back once)."""
+    if isinstance(u, torch.Tensor):
+        u = u.detach().cpu().numpy()
+    u = np.asarray(u, dtype=np.float64).ravel()
+    if fmt == "csv":
+        with open(path, "w") as fh:
+            fh.write("index,value\n")
+            if u.size:
+                np.savetxt(fh, np.column_stack([np.arange(u.size, dtype=np.float64), u]), fmt="%d,%.17g")
+    elif fmt == "bin":
+        u.tofile(path)
+    else:
+        raise ValueError(f"unknown vector format {fmt!r}")
+
+
+def load_vector(path, fmt: str = "csv") -> np.ndarray:
+    """discretization.py:479-488: rows are put back in index order."""
+    if fmt == "csv":
+        data = np.genfromtxt(path, delimiter=",", skip_header=1)
+        if data.ndim == 1:  # single row
+            data = data.reshape(1, -1)
+        order = np.argsort(data[:, 0], kind="stable")
+        return data[order, 1].copy()
+    if fmt == "bin":
+        return np.fromfile(path, dtype=np.float64)
+    raise ValueError(f"unknown vector format {fmt!r}")
+
 @dataclass
 class ModelProblem:
     exact: callable

@@ -154,3 +154,39 @@ def test_slab_levels_property_sweep():
                 for p in per_rank:
                     sl = p[lvl]
                     assert sl.ext_dofs == sl.local_dofs + (sl.h_lo + sl.h_hi) * sl.cell_layer
+
+
+@pytest.mark.parametrize("fmt", ["csv", "bin"])
+def test_vector_serialization_roundtrip(tmp_path, fmt):
+    """tests/test_discretization.py:364-374 of the reference: exact round trip, unknown format -> ValueError."""
+    from paper_2407_09621_b200.discretization import load_vector, save_vector
+
+    u = np.random.default_rng(21).standard_normal(64)
+    path = tmp_path / f"vec.{fmt}"
+    save_vector(path, u, fmt=fmt)
+    assert np.array_equal(load_vector(path, fmt=fmt), u)
+    with pytest.raises(ValueError):
+        save_vector(path, u, fmt="hdf5")
+    with pytest.raises(ValueError):
+        load_vector(path, fmt="hdf5")
+
+
+def test_vector_csv_format_matches_reference_writer(tmp_path):
+    """Byte-identical to the reference's per-row f"{i},{v:.17g}" writer (discretization.py:470-472), and rows are
+    re-sorted by index on load."""
+    from paper_2407_09621_b200.discretization import load_vector, save_vector
+
+    u = np.concatenate([np.random.default_rng(3).standard_normal(40) * 10.0 ** np.arange(-20, 20),
+                        [0.0, -0.0, 1e308, -5e-324, 1.0 / 3.0, np.inf, -np.inf]])
+    path = tmp_path / "v.csv"
+    save_vector(path, u)
+    expect = "index,value\n" + "".join(f"{i},{v:.17g}\n" for i, v in enumerate(u))
+    assert path.read_text() == expect
+    lines = path.read_text().splitlines()
+    shuffled = tmp_path / "s.csv"
+    shuffled.write_text("\n".join([lines[0]] + lines[1:][::-1]) + "\n")
+    got = load_vector(shuffled)
+    assert np.array_equal(got, u)
+    one = tmp_path / "one.csv"
+    save_vector(one, u[:1])
+    assert np.array_equal(load_vector(one), u[:1])
