@@ -125,6 +125,27 @@ int sf_axpby(long long n, double alpha, const double* x, double beta, double* y,
 /* float variant used inside low-precision V-cycles: y = alpha * x + beta * y (fp32). */
 int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream);
 
+/* ---- binary16 primitives of the precision semantics (precision.py:60-197), same cvt as the FP16 kernels ---- */
+
+/* fp32 -> binary16 bit patterns, round to nearest even, subnormals exact, overflow to inf, NaN -> 0x7E00|sign.
+ * Replaces precision.to_half                                    precision.py:60-113. */
+int sf_to_half(long long n, const float* x, unsigned short* bits, void* stream);
+/* binary16 bit patterns -> exact fp32 (NaN -> 0x7FC00000 whatever its sign, as the reference's sign * nan).
+ * Replaces precision.from_half                                  precision.py:116-127. */
+int sf_from_half(long long n, const unsigned short* bits, float* x, void* stream);
+/* fp32 -> binary16 -> fp32 (numpy's float16 cast, NaN payload top bits kept).
+ * Replaces precision.demote16                                   precision.py:130-137. */
+int sf_demote16(long long n, const float* x, float* out, void* stream);
+/* main = to_half(x), residual = to_half((x - from_half(main)) * 2^11); *range_flag_dev |= 1 when some |x| > 65504
+ * or x is not finite (the caller raises HalfRangeError).  Replaces precision.ec_split   precision.py:160-167. */
+int sf_ec_split(long long n, const float* x, unsigned short* main_bits, unsigned short* resid_bits, int* range_flag_dev,
+                void* stream);
+/* out (m x n, row-major f32) = A_h B_h + corr / 2^11, corr = A_d B_h (refine 0 both / 1 left) + A_h B_d (0 both /
+ * 2 right); A (m x k), B (k x n) given as row-major main / residual half bit patterns, fp32 accumulation.
+ * Replaces precision.ec_matmul                                  precision.py:178-197. */
+int sf_ec_matmul(int m, int k, int n, const unsigned short* a_main, const unsigned short* a_resid,
+                 const unsigned short* b_main, const unsigned short* b_resid, int refine, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,8 @@ run_solve).  All compute runs in libsumfact_b200.so; there is no CPU fallback.
 """
 __version__ = "0.1.0"
 
-from .precision import PrecisionMode, relative_error  # noqa: F401
+from .precision import (PrecisionMode, relative_error, HalfRangeError, EcPair, to_half, from_half,  # noqa: F401
+                        demote16, ec_split, ec_matmul)
 from .core import contract_batch, contract_mode  # noqa: F401
 from .discretization import (MeshHierarchy, build_hierarchy, apply_operator, materialize_operator,  # noqa: F401
                              assemble_rhs, interpolate, l2_error, h1_seminorm_error, sine_product_problem,

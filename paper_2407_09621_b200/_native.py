@@ -60,6 +60,12 @@ def lib():
             "sf_axpby_f32": ([c_ll, c_f, c_p, c_f, c_p, c_p], c_i),
             "sf_contract": ([c_i, c_ll, c_i, c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_contract_last_error": ([], ctypes.c_char_p),
+            "sf_half_last_error": ([], ctypes.c_char_p),
+            "sf_to_half": ([c_ll, c_p, c_p, c_p], c_i),
+            "sf_from_half": ([c_ll, c_p, c_p, c_p], c_i),
+            "sf_demote16": ([c_ll, c_p, c_p, c_p], c_i),
+            "sf_ec_split": ([c_ll, c_p, c_p, c_p, c_p, c_p], c_i),
+            "sf_ec_matmul": ([c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_i, c_p, c_p], c_i),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -73,7 +79,7 @@ def lib():
 
 EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "sf_smooth_colour", "sf_residual_restrict",
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
-            "sf_contract")
+            "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul")
 
 
 def check(rc: int, what: str):
@@ -81,7 +87,7 @@ def check(rc: int, what: str):
         return
     L = lib()
     msg = ((L.sf_last_error() or b"").decode() or (L.sf_vec_last_error() or b"").decode()
-           or (L.sf_contract_last_error() or b"").decode())
+           or (L.sf_contract_last_error() or b"").decode() or (L.sf_half_last_error() or b"").decode())
     if rc == SF_EINVAL:
         raise ValueError(f"{what}: {msg}")
     if rc == SF_EUNSUPPORTED:

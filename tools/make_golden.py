@@ -139,6 +139,35 @@ def half():
     save("half", x=x, demoted=demote16(x))
 
 
+def softfloat():
+    """precision.py:60-197 through the reference itself: its binary16 fixture (tests/data/half_reference.txt,
+    fp32 bits -> fp16 bits), to_half on NaN payloads / edge values, from_half of all 65536 patterns, ec_split
+    and ec_matmul (all three refine choices)."""
+    from sumfact.precision import ec_matmul, ec_split, from_half, to_half
+
+    lines = open("/root/reference/pkg/tests/data/half_reference.txt").read().splitlines()
+    pairs = [ln.split() for ln in lines if not ln.startswith("#")]
+    fix_x = np.array([int(a, 16) for a, _ in pairs], dtype=np.uint32)
+    fix_h = np.array([int(b, 16) for _, b in pairs], dtype=np.uint16)
+    nan_bits = np.array([0x7FC00000, 0xFFC00000, 0x7F800001, 0xFF800001, 0x7FA00000, 0x7F802000, 0x7FFFFFFF,
+                         0x00000001, 0x80000001, 0x007FFFFF, 0x33000000, 0x33000001, 0x33800000, 0x477FEFFF,
+                         0x477FF000, 0x7F7FFFFF], dtype=np.uint32)
+    edge_x = np.concatenate([nan_bits, fix_x[:64]]).view(np.float32)
+    all_h = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    rng = np.random.default_rng(9)
+    ec_x = np.concatenate([(rng.standard_normal(3000) * 10.0 ** rng.uniform(-6, 4, 3000)).astype(np.float32),
+                           np.array([65504.0, -65504.0, 0.0, -0.0, 6e-8, 1.0 / 3.0], dtype=np.float32)])
+    pr = ec_split(ec_x)
+    A = (rng.standard_normal((19, 23)) * 3).astype(np.float32)
+    B = (rng.standard_normal((23, 17)) * 0.1).astype(np.float32)
+    ea, eb = ec_split(A.ravel()), ec_split(B.ravel())
+    ea = type(ea)(main=ea.main.reshape(A.shape), residual=ea.residual.reshape(A.shape))
+    eb = type(eb)(main=eb.main.reshape(B.shape), residual=eb.residual.reshape(B.shape))
+    save("softfloat", fix_x=fix_x, fix_h=fix_h, edge_x=edge_x, edge_h=to_half(edge_x),
+         from_half_all=from_half(all_h).view(np.uint32), ec_x=ec_x, ec_main=pr.main, ec_resid=pr.residual,
+         mm_a=A, mm_b=B, **{f"mm_{r}": ec_matmul(ea, eb, refine=r) for r in ("both", "left", "right")})
+
+
 def error_profiles():
     """Reference experiments.error_profile(7, 4, (fp32, fp16, fp16_ec), seed=0) -> JSON rows
     (acceptance criterion 9 inputs, tests/test_gpu_acceptance.py)."""
@@ -160,6 +189,6 @@ if __name__ == "__main__" and len(sys.argv) > 1:
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     print("reference sumfact", sumfact.__version__, "compiled core:", sumfact.HAVE_COMPILED)
-    which = sys.argv[1:] or ["matrices", "vmult", "dense", "smoother_transfers", "vcycles", "half", "solves"]
+    which = sys.argv[1:] or ["matrices", "vmult", "dense", "smoother_transfers", "vcycles", "half", "solves", "softfloat"]
     for w in which:
         globals()[w]()
