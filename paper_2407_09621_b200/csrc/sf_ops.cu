@@ -396,23 +396,38 @@ __global__ void __launch_bounds__(kThreads) k_prolong_add(const typename MT<MODE
   }
   __syncthreads();
   const C back = kHalf ? (C)pow2f(-ee) : C(1);
-  // z lines: (t, y, x) K -> B, added into the fine vector
-  for (int j2 = threadIdx.x; j2 < TPC * B * B; j2 += blockDim.x) {
-    int xf = j2 % B, yf = (j2 / B) % B, t = j2 / (B * B);
+  // z lines: (t, y, x) K -> B, added into the fine vector; one work item per (column, group of HB outputs).
+  // An item's HB fine values are all in flight before its first store (a read-modify-write loop would serialise
+  // into dependent DRAM round trips: the compiler cannot hoist a load above a store to the same array).  fp64
+  // takes all B per item (measured fastest); the fp32-storage modes split the column in two (register budget).
+  constexpr int HB = MODE == MODE_FP64 ? B : K, NH = B / HB;
+  for (int j2 = threadIdx.x; j2 < NH * TPC * B * B; j2 += blockDim.x) {
+    const int h = j2 / (TPC * B * B);
+    const int jj = j2 - h * (TPC * B * B);
+    int xf = jj % B, yf = (jj / B) % B, t = jj / (B * B);
     int ax, ay, az;
     if (!cell(t, ax, ay, az)) continue;
     const C* col = s + t * VOL + yf * P + xf;
     Op<MODE> w[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) w[j] = prep<MODE>(col[j * B * P]);
-    S* out = fine + (long long)(2 * az * K) * szf + (long long)(2 * ay * K + yf) * syf + (2 * ax * K + xf);
+    S* out = fine + (long long)(2 * az * K + h * HB) * szf + (long long)(2 * ay * K + yf) * syf + (2 * ax * K + xf);
+    auto group = [&](auto O0) {  // compile-time output offset: constant indices into the embedding
+      constexpr int oc = decltype(O0)::value;
+      C old[HB];
 #pragma unroll
-    for (int o = 0; o < B; ++o) {
-      Acc<MODE> a;
+      for (int o = 0; o < HB; ++o) old[o] = (C)out[o * szf];
 #pragma unroll
-      for (int j = 0; j < K; ++j) a.fma(emb.P[o][j], w[j]);
-      out[o * szf] = (S)((C)out[o * szf] + a.result() * back);
-    }
+      for (int o = 0; o < HB; ++o) {
+        Acc<MODE> a;
+#pragma unroll
+        for (int j = 0; j < K; ++j) a.fma(emb.P[oc + o][j], w[j]);
+        out[o * szf] = (S)(old[o] + a.result() * back);
+      }
+    };
+    if constexpr (NH == 1) group(std::integral_constant<int, 0>{});
+    else if (h == 0) group(std::integral_constant<int, 0>{});
+    else group(std::integral_constant<int, B - HB>{});
   }
 }
 
