@@ -119,6 +119,16 @@ int sf_dot(long long n, const double* x, const double* y, double* out_dev, doubl
  * Replaces `w = w - H[i, j] * V[i]`                          krylov.py:76,83. */
 int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream);
 
+/* Fused modified-Gram-Schmidt step: w += sign * (*coef_dev) * x (as sf_axpy_dev), then *out_dev = y . w_new
+ * (y == NULL: w_new . w_new), bitwise equal to the separate sf_axpy_dev + sf_dot; one pass over w.
+ * Replaces `w = w - H[i, j] * V[i]; H[i + 1, j] = V[i + 1] @ w`     krylov.py:73-84. */
+int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* x, double* w, const double* y,
+                double* out_dev, double* scratch_dev, void* stream);
+/* *out1_dev = x1 . y and *out2_dev = x2 . y in one pass over y, each bitwise equal to sf_dot;
+ * scratch_dev: 2 * SF_DOT_SCRATCH doubles. */
+int sf_dot2(long long n, const double* x1, const double* x2, const double* y, double* out1_dev, double* out2_dev,
+            double* scratch_dev, void* stream);
+
 /* y = alpha * x + beta * y (host scalars; y may alias nothing).  Replaces b / beta, w / h_next, x += y_i Z_i. */
 int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream);
 

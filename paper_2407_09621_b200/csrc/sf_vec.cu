@@ -48,6 +48,72 @@ __global__ void k_dot_partial(long long n, const double* __restrict__ x, const d
   if (threadIdx.x == 0) part[blockIdx.x] = s[0];
 }
 
+// Fused MGS step (krylov.py:73-84): w -= coef * x elementwise exactly as k_axpy_dev, and the partial sums of
+// <y, w_new> (y = w when y == nullptr: the closing norm) in exactly k_dot_partial's element -> thread ->
+// accumulator assignment, so the reduced value is bitwise the separate dot's.  One pass over w instead of two.
+__global__ void k_axpy_dot_partial(long long n, double sign, const double* __restrict__ coef,
+                                   const double* __restrict__ x, double* __restrict__ w, const double* __restrict__ y,
+                                   double* __restrict__ part) {
+  __shared__ double s[kThreads];
+  const double a = sign * (*coef);
+  double acc = 0.0, acc2 = 0.0;
+  const long long stride = (long long)kDotBlocks * kThreads;
+  long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  for (; i + stride < n; i += 2 * stride) {
+    const double w0 = fma(a, x[i], w[i]), w1 = fma(a, x[i + stride], w[i + stride]);
+    w[i] = w0;
+    w[i + stride] = w1;
+    acc = fma(y ? y[i] : w0, w0, acc);
+    acc2 = fma(y ? y[i + stride] : w1, w1, acc2);
+  }
+  if (i < n) {
+    const double w0 = fma(a, x[i], w[i]);
+    w[i] = w0;
+    acc = fma(y ? y[i] : w0, w0, acc);
+  }
+  s[threadIdx.x] = acc + acc2;
+  __syncthreads();
+  for (int t = kThreads / 2; t > 0; t >>= 1) {
+    if (threadIdx.x < t) s[threadIdx.x] += s[threadIdx.x + t];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+// Two dots sharing the right operand in one pass: <x1, y> and <x2, y>, each with k_dot_partial's order.
+__global__ void k_dot2_partial(long long n, const double* __restrict__ x1, const double* __restrict__ x2,
+                               const double* __restrict__ y, double* __restrict__ part1, double* __restrict__ part2) {
+  __shared__ double s1[kThreads], s2[kThreads];
+  double a1 = 0.0, a1b = 0.0, a2 = 0.0, a2b = 0.0;
+  const long long stride = (long long)kDotBlocks * kThreads;
+  long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  for (; i + stride < n; i += 2 * stride) {
+    const double y0 = y[i], y1 = y[i + stride];
+    a1 = fma(x1[i], y0, a1);
+    a1b = fma(x1[i + stride], y1, a1b);
+    a2 = fma(x2[i], y0, a2);
+    a2b = fma(x2[i + stride], y1, a2b);
+  }
+  if (i < n) {
+    a1 = fma(x1[i], y[i], a1);
+    a2 = fma(x2[i], y[i], a2);
+  }
+  s1[threadIdx.x] = a1 + a1b;
+  s2[threadIdx.x] = a2 + a2b;
+  __syncthreads();
+  for (int t = kThreads / 2; t > 0; t >>= 1) {
+    if (threadIdx.x < t) {
+      s1[threadIdx.x] += s1[threadIdx.x + t];
+      s2[threadIdx.x] += s2[threadIdx.x + t];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part1[blockIdx.x] = s1[0];
+    part2[blockIdx.x] = s2[0];
+  }
+}
+
 __global__ void k_dot_final(const double* __restrict__ part, double* __restrict__ out) {
   __shared__ double s[kDotBlocks];
   for (int i = threadIdx.x; i < kDotBlocks; i += blockDim.x) s[i] = part[i];
@@ -113,6 +179,25 @@ int sf_dot(long long n, const double* x, const double* y, double* out_dev, doubl
   k_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(n, x, y, scratch);
   k_dot_final<<<1, 1024, 0, st>>>(scratch, out_dev);
   return launched("sf_dot");
+}
+
+int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* x, double* w, const double* y,
+                double* out_dev, double* scratch, void* stream) {
+  if (n < 0 || !coef_dev || !out_dev || !scratch || (n && (!x || !w))) return SF_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_axpy_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(n, sign, coef_dev, x, w, y, scratch);
+  k_dot_final<<<1, 1024, 0, st>>>(scratch, out_dev);
+  return launched("sf_axpy_dot");
+}
+
+int sf_dot2(long long n, const double* x1, const double* x2, const double* y, double* out1_dev, double* out2_dev,
+            double* scratch2, void* stream) {
+  if (n < 0 || !out1_dev || !out2_dev || !scratch2 || (n && (!x1 || !x2 || !y))) return SF_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_dot2_partial<<<kDotBlocks, kThreads, 0, st>>>(n, x1, x2, y, scratch2, scratch2 + kDotBlocks);
+  k_dot_final<<<1, 1024, 0, st>>>(scratch2, out1_dev);
+  k_dot_final<<<1, 1024, 0, st>>>(scratch2 + kDotBlocks, out2_dev);
+  return launched("sf_dot2");
 }
 
 int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream) {

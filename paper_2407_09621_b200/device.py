@@ -63,7 +63,7 @@ class Scratch:
         key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
         buf = cls._buf.get(key)
         if buf is None:
-            buf = torch.empty(_native.SF_DOT_SCRATCH, dtype=torch.float64, device="cuda")
+            buf = torch.empty(2 * _native.SF_DOT_SCRATCH, dtype=torch.float64, device="cuda")
             cls._buf[key] = buf
         return buf
 
@@ -75,6 +75,21 @@ def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> to
     _native.check(_native.lib().sf_dot(x.numel(), ptr(x), ptr(y), out.data_ptr(), ptr(Scratch.dot()), stream_ptr()),
                   "sf_dot")
     return out
+
+
+def axpy_dot(sign: float, coef: torch.Tensor, x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None,
+             out: torch.Tensor) -> torch.Tensor:
+    """w += sign * coef[0] * x, then out[0] = y . w (w . w when y is None) -- one pass, bitwise the separate ops."""
+    _native.check(_native.lib().sf_axpy_dot(x.numel(), sign, coef.data_ptr(), ptr(x), ptr(w),
+                                            ptr(y) if y is not None else None, out.data_ptr(), ptr(Scratch.dot()),
+                                            stream_ptr()), "sf_axpy_dot")
+    return out
+
+
+def dot2(x1: torch.Tensor, x2: torch.Tensor, y: torch.Tensor, out1: torch.Tensor, out2: torch.Tensor):
+    """out1[0] = x1 . y, out2[0] = x2 . y in one pass over y (each bitwise sf_dot)."""
+    _native.check(_native.lib().sf_dot2(y.numel(), ptr(x1), ptr(x2), ptr(y), out1.data_ptr(), out2.data_ptr(),
+                                        ptr(Scratch.dot()), stream_ptr()), "sf_dot2")
 
 
 def axpy_dev(sign: float, coef: torch.Tensor, x: torch.Tensor, y: torch.Tensor):

@@ -86,3 +86,25 @@ def test_criterion_09_error_profile_ordering_and_reference_values():
         assert (r["level"], r["mode"]) == (g["level"], g["mode"])
         # same inputs, same per-contraction demotion: errors agree to within a factor 2
         assert 0.5 * g["relative_error"] <= r["relative_error"] <= 2.0 * g["relative_error"], (r, g)
+
+
+def test_fused_gram_schmidt_is_bitwise_the_separate_one():
+    """sf_axpy_dot / sf_dot2 (one pass over w per MGS step) reproduce the separate sf_dot + sf_axpy_dev sweep
+    bit for bit: same iterates, residual history and solution."""
+    from paper_2407_09621_b200 import krylov
+
+    hier = sf.build_hierarchy(4, 3)
+    b = np.random.default_rng(7).standard_normal(hier.n_dofs(4))
+    mg = sf.MultigridPreconditioner(hier)
+    A = lambda v: sf.apply_operator(hier, 4, v)
+    M = lambda v: mg.apply(v, 4)
+    outs = []
+    for fused in (True, False):
+        krylov.FUSED_MGS = fused
+        try:
+            outs.append(sf.fgmres(A, M, b, tol=1e-10, maxit=40))
+        finally:
+            krylov.FUSED_MGS = True
+    (x1, r1), (x2, r2) = outs
+    assert r1.iterations == r2.iterations and r1.residual_history == r2.residual_history
+    assert np.array_equal(x1, x2)
