@@ -129,6 +129,11 @@ int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* 
 int sf_dot2(long long n, const double* x1, const double* x2, const double* y, double* out1_dev, double* out2_dev,
             double* scratch_dev, void* stream);
 
+/* out = sum_{t < m} coefs[t] * vecs[t] (m <= 128 device vectors, host pointer/coefficient arrays), accumulated in
+ * term order as m successive sf_axpby(coefs[t], vecs[t], 1.0, out) from out = 0 -- bitwise -- in one pass.
+ * Replaces the FGMRES solution update x = sum_i y_i Z_i        krylov.py:120-124. */
+int sf_lincomb(long long n, int m, const double* const* vecs, const double* coefs, double* out, void* stream);
+
 /* y = alpha * x + beta * y (host scalars; y may alias nothing).  Replaces b / beta, w / h_next, x += y_i Z_i. */
 int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream);
 

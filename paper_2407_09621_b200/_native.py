@@ -58,6 +58,7 @@ def lib():
             "sf_axpy_dev": ([c_ll, c_d, c_p, c_p, c_p, c_p], c_i),
             "sf_axpy_dot": ([c_ll, c_d, c_p, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_dot2": ([c_ll, c_p, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
+            "sf_lincomb": ([c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_axpby": ([c_ll, c_d, c_p, c_d, c_p, c_p], c_i),
             "sf_axpby_f32": ([c_ll, c_f, c_p, c_f, c_p, c_p], c_i),
             "sf_contract": ([c_i, c_ll, c_i, c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
@@ -81,7 +82,7 @@ def lib():
 
 EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "sf_smooth_colour", "sf_residual_restrict",
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
-            "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2")
+            "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2", "sf_lincomb")
 
 
 def check(rc: int, what: str):

@@ -135,7 +135,23 @@ __global__ void k_axpy_dev(long long n, double sign, const double* __restrict__ 
 template <typename T>
 __global__ void k_axpby(long long n, T alpha, const T* __restrict__ x, T beta, T* __restrict__ y) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = beta == T(0) ? alpha * x[i] : alpha * x[i] + beta * y[i];  // beta = 0 never reads y
+    y[i] = beta == T(0) ? alpha * x[i] : fma(alpha, x[i], beta * y[i]);  // beta = 0 never reads y
+}
+
+// x = sum_i c_i v_i accumulated in term order exactly as x = 0; x = fma(c_i, v_i, 1.0 * x) (k_axpby with beta = 1),
+// in one pass: reads the m vectors once and writes x once (krylov.py:120-124, the FGMRES solution update)
+constexpr int kMaxTerms = 128;
+struct LinComb {
+  const double* v[kMaxTerms];
+  double c[kMaxTerms];
+};
+
+__global__ void k_lincomb(long long n, int m, const LinComb lc, double* __restrict__ x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < m; ++t) acc = fma(lc.c[t], lc.v[t][i], 1.0 * acc);
+    x[i] = acc;
+  }
 }
 
 thread_local char g_err[256] = "";
@@ -198,6 +214,19 @@ int sf_dot2(long long n, const double* x1, const double* x2, const double* y, do
   k_dot_final<<<1, 1024, 0, st>>>(scratch2, out1_dev);
   k_dot_final<<<1, 1024, 0, st>>>(scratch2 + kDotBlocks, out2_dev);
   return launched("sf_dot2");
+}
+
+int sf_lincomb(long long n, int m, const double* const* vecs, const double* coefs, double* out, void* stream) {
+  if (n < 0 || m < 0 || m > kMaxTerms || !out || (m && (!vecs || !coefs))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  LinComb lc;
+  for (int t = 0; t < m; ++t) {
+    if (!vecs[t]) return SF_EINVAL;
+    lc.v[t] = vecs[t];
+    lc.c[t] = coefs[t];
+  }
+  k_lincomb<<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, m, lc, out);
+  return launched("sf_lincomb");
 }
 
 int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream) {

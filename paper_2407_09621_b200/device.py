@@ -92,6 +92,18 @@ def dot2(x1: torch.Tensor, x2: torch.Tensor, y: torch.Tensor, out1: torch.Tensor
                                         ptr(Scratch.dot()), stream_ptr()), "sf_dot2")
 
 
+def lincomb(vecs, coefs, out: torch.Tensor) -> torch.Tensor:
+    """out = sum_t coefs[t] vecs[t] in one pass (bitwise the axpby chain from zero)."""
+    import ctypes
+
+    m = len(vecs)
+    P = (ctypes.c_void_p * max(m, 1))(*[ptr(v) for v in vecs])
+    C = (ctypes.c_double * max(m, 1))(*[float(c) for c in coefs])
+    _native.check(_native.lib().sf_lincomb(out.numel(), m, ctypes.cast(P, ctypes.c_void_p),
+                                           ctypes.cast(C, ctypes.c_void_p), ptr(out), stream_ptr()), "sf_lincomb")
+    return out
+
+
 def axpy_dev(sign: float, coef: torch.Tensor, x: torch.Tensor, y: torch.Tensor):
     """y += sign * coef[0] * x, coef on the device."""
     _native.check(_native.lib().sf_axpy_dev(x.numel(), sign, coef.data_ptr(), ptr(x), ptr(y), stream_ptr()),
