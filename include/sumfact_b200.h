@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 1
+#define SF_ABI_VERSION 2  /* 2: sf_div, SF_LINCOMB_MAX_TERMS */
 #define SF_MAX_DEGREE 7
 
 #define SF_OK 0
@@ -129,12 +129,18 @@ int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* 
 int sf_dot2(long long n, const double* x1, const double* x2, const double* y, double* out1_dev, double* out2_dev,
             double* scratch_dev, void* stream);
 
-/* out = sum_{t < m} coefs[t] * vecs[t] (m <= 128 device vectors, host pointer/coefficient arrays), accumulated in
+/* Largest term count sf_lincomb accepts (larger FGMRES bases fall back to the sf_axpby chain). */
+#define SF_LINCOMB_MAX_TERMS 128
+/* out = sum_{t < m} coefs[t] * vecs[t] (m <= SF_LINCOMB_MAX_TERMS device vectors, host pointer/coefficient arrays), accumulated in
  * term order as m successive sf_axpby(coefs[t], vecs[t], 1.0, out) from out = 0 -- bitwise -- in one pass.
  * Replaces the FGMRES solution update x = sum_i y_i Z_i        krylov.py:120-124. */
 int sf_lincomb(long long n, int m, const double* const* vecs, const double* coefs, double* out, void* stream);
 
-/* y = alpha * x + beta * y (host scalars; y may alias nothing).  Replaces b / beta, w / h_next, x += y_i Z_i. */
+/* y = x / d elementwise (IEEE division, the reference's rounding).  Replaces V = [b / beta] and
+ * V.append(w / h_next)                                        krylov.py:57,106. */
+int sf_div(long long n, const double* x, double d, double* y, void* stream);
+
+/* y = alpha * x + beta * y (host scalars; y may alias nothing).  Replaces x += y_i Z_i (chain form). */
 int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream);
 
 /* float variant used inside low-precision V-cycles: y = alpha * x + beta * y (fp32). */

@@ -18,6 +18,8 @@ SF_EINVAL = -1
 SF_EUNSUPPORTED = -2
 SF_ECUDA = -3
 SF_DOT_SCRATCH = 1024
+SF_LINCOMB_MAX_TERMS = 128  # include/sumfact_b200.h
+ABI_VERSION = 2
 MAX_DEGREE = 7
 
 
@@ -60,6 +62,7 @@ def lib():
             "sf_dot2": ([c_ll, c_p, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_lincomb": ([c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_axpby": ([c_ll, c_d, c_p, c_d, c_p, c_p], c_i),
+            "sf_div": ([c_ll, c_p, c_d, c_p, c_p], c_i),
             "sf_axpby_f32": ([c_ll, c_f, c_p, c_f, c_p, c_p], c_i),
             "sf_contract": ([c_i, c_ll, c_i, c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_contract_last_error": ([], ctypes.c_char_p),
@@ -70,27 +73,48 @@ def lib():
             "sf_ec_split": ([c_ll, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_ec_matmul": ([c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_i, c_p, c_p], c_i),
         }
-        for name, (args, res) in sigs.items():
-            fn = getattr(L, name)
-            fn.argtypes = args
-            fn.restype = res
-        if L.sf_abi_version() != 1:
-            raise ImportError("libsumfact_b200.so ABI mismatch; rebuild")
+        try:
+            version = L.sf_abi_version()
+            for name, (args, res) in sigs.items():
+                fn = getattr(L, name)
+                fn.argtypes = args
+                fn.restype = res
+        except AttributeError as e:  # a library built before an entry point was added
+            raise ImportError(f"libsumfact_b200.so ABI mismatch ({e}); rebuild") from e
+        if version != ABI_VERSION:
+            raise ImportError(f"libsumfact_b200.so ABI {version} != {ABI_VERSION}; rebuild")
         _lib = L
     return _lib
 
 
 EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "sf_smooth_colour", "sf_residual_restrict",
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
-            "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2", "sf_lincomb")
+            "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_div")
+
+# which thread-local error buffer each entry point writes (each module clears its own on entry)
+_VEC = {"sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_axpby", "sf_axpby_f32",
+        "sf_div"}
+_HALF = {"sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul"}
+
+
+def _error_message(what: str) -> str:
+    L = lib()
+    name = what.split()[0]
+    if name in _VEC:
+        getter = L.sf_vec_last_error
+    elif name in _HALF:
+        getter = L.sf_half_last_error
+    elif name == "sf_contract":
+        getter = L.sf_contract_last_error
+    else:
+        getter = L.sf_last_error
+    return (getter() or b"").decode()
 
 
 def check(rc: int, what: str):
     if rc == SF_OK:
         return
-    L = lib()
-    msg = ((L.sf_last_error() or b"").decode() or (L.sf_vec_last_error() or b"").decode()
-           or (L.sf_contract_last_error() or b"").decode() or (L.sf_half_last_error() or b"").decode())
+    msg = _error_message(what)
     if rc == SF_EINVAL:
         raise ValueError(f"{what}: {msg}")
     if rc == SF_EUNSUPPORTED:

@@ -79,11 +79,16 @@ const char* sf_contract_last_error(void) { return g_err; }
 
 int sf_contract(int mode, long long outer, int n, long long inner, int rows, const void* m, const void* u, void* out,
                 void* stream) {
-  if (mode < 0 || mode > 3) return SF_EINVAL;
-  if (outer < 0 || inner < 0 || n < 0 || rows < 0) return SF_EINVAL;
+  g_err[0] = 0;
+  auto invalid = [](const char* why) {
+    snprintf(g_err, sizeof(g_err), "sf_contract: %s", why);
+    return SF_EINVAL;
+  };
+  if (mode < 0 || mode > 3) return invalid("mode must be 0..3");
+  if (outer < 0 || inner < 0 || n < 0 || rows < 0) return invalid("negative extent");
   const long long total = outer * rows * inner;
   if (total == 0) return SF_OK;
-  if (!m || !u || !out) return SF_EINVAL;
+  if (!m || !u || !out) return invalid("null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;

@@ -109,22 +109,30 @@ extern "C" {
 
 const char* sf_half_last_error(void) { return g_err; }
 
+static int invalid(const char* what) {
+  snprintf(g_err, sizeof(g_err), "%s: negative size, bad refine flag or null pointer", what);
+  return SF_EINVAL;
+}
+
 int sf_to_half(long long n, const float* x, unsigned short* bits, void* stream) {
-  if (n < 0 || (n && (!x || !bits))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !bits))) return invalid("sf_to_half");
   if (n == 0) return SF_OK;
   k_to_half<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, bits);
   return launched("sf_to_half");
 }
 
 int sf_from_half(long long n, const unsigned short* bits, float* x, void* stream) {
-  if (n < 0 || (n && (!x || !bits))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !bits))) return invalid("sf_from_half");
   if (n == 0) return SF_OK;
   k_from_half<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, bits, x);
   return launched("sf_from_half");
 }
 
 int sf_demote16(long long n, const float* x, float* out, void* stream) {
-  if (n < 0 || (n && (!x || !out))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !out))) return invalid("sf_demote16");
   if (n == 0) return SF_OK;
   k_demote16<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, out);
   return launched("sf_demote16");
@@ -132,7 +140,8 @@ int sf_demote16(long long n, const float* x, float* out, void* stream) {
 
 int sf_ec_split(long long n, const float* x, unsigned short* main_bits, unsigned short* resid_bits, int* range_flag_dev,
                 void* stream) {
-  if (n < 0 || !range_flag_dev || (n && (!x || !main_bits || !resid_bits))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !range_flag_dev || (n && (!x || !main_bits || !resid_bits))) return invalid("sf_ec_split");
   if (n == 0) return SF_OK;
   k_ec_split<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, main_bits, resid_bits, range_flag_dev);
   return launched("sf_ec_split");
@@ -140,9 +149,10 @@ int sf_ec_split(long long n, const float* x, unsigned short* main_bits, unsigned
 
 int sf_ec_matmul(int m, int k, int n, const unsigned short* a_main, const unsigned short* a_resid,
                  const unsigned short* b_main, const unsigned short* b_resid, int refine, float* out, void* stream) {
-  if (m < 0 || k < 0 || n < 0 || refine < 0 || refine > 2) return SF_EINVAL;
+  g_err[0] = 0;
+  if (m < 0 || k < 0 || n < 0 || refine < 0 || refine > 2) return invalid("sf_ec_matmul");
   if ((long long)m * n == 0) return SF_OK;
-  if (!a_main || !a_resid || !b_main || !b_resid || !out) return SF_EINVAL;
+  if (!a_main || !a_resid || !b_main || !b_resid || !out) return invalid("sf_ec_matmul");
   const long long total = (long long)m * n;
   const int left = refine != 2, right = refine != 1;  // 0 both, 1 left, 2 right
   k_ec_matmul<<<(int)((total + kThreads - 1) / kThreads), kThreads, 0, (cudaStream_t)stream>>>(

@@ -880,6 +880,7 @@ using namespace sf;
   } while (0)
 
 static int check_common(int mode, int k) {
+  g_err[0] = 0;  // every entry point starts here: no stale message survives a later failure
   if (mode < 0 || mode > 3) return fail(SF_EINVAL, "mode must be 0..3 (fp64, fp32, fp16, fp16_ec)");
   if (k < 1 || k > SF_MAX_DEGREE) return fail(SF_EUNSUPPORTED, "degree k must be in 1..7");
   return SF_OK;

@@ -125,6 +125,12 @@ __global__ void k_dot_final(const double* __restrict__ part, double* __restrict_
   if (threadIdx.x == 0) *out = s[0];
 }
 
+// y = x / d elementwise (IEEE division, as the reference's V = [b / beta], w / h_next, krylov.py:57,106)
+__global__ void k_div(long long n, const double* __restrict__ x, double d, double* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+
 __global__ void k_axpy_dev(long long n, double sign, const double* __restrict__ coef, const double* __restrict__ x,
                            double* __restrict__ y) {
   const double a = sign * (*coef);
@@ -140,7 +146,7 @@ __global__ void k_axpby(long long n, T alpha, const T* __restrict__ x, T beta, T
 
 // x = sum_i c_i v_i accumulated in term order exactly as x = 0; x = fma(c_i, v_i, 1.0 * x) (k_axpby with beta = 1),
 // in one pass: reads the m vectors once and writes x once (krylov.py:120-124, the FGMRES solution update)
-constexpr int kMaxTerms = 128;
+constexpr int kMaxTerms = SF_LINCOMB_MAX_TERMS;
 struct LinComb {
   const double* v[kMaxTerms];
   double c[kMaxTerms];
@@ -155,6 +161,12 @@ __global__ void k_lincomb(long long n, int m, const LinComb lc, double* __restri
 }
 
 thread_local char g_err[256] = "";
+
+// every entry point clears the buffer first, and every SF_EINVAL carries a message
+int invalid(const char* what, const char* why) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, why);
+  return SF_EINVAL;
+}
 
 int launched(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -172,7 +184,8 @@ extern "C" {
 const char* sf_vec_last_error(void) { return g_err; }
 
 int sf_convert(long long n, const void* in, int in_dtype, void* out, int out_dtype, void* stream) {
-  if (n < 0 || (!in && n) || (!out && n)) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (!in && n) || (!out && n)) return invalid("sf_convert", "negative length or null vector");
   if (n == 0) return SF_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int g = grid_for(n, 4);
@@ -185,12 +198,13 @@ int sf_convert(long long n, const void* in, int in_dtype, void* out, int out_dty
   else if (in_dtype == 1 && out_dtype == 1)
     k_convert<float, float><<<g, kThreads, 0, st>>>(n, (const float*)in, (float*)out);
   else
-    return SF_EINVAL;
+    return invalid("sf_convert", "dtype codes must be 0 (f64) or 1 (f32)");
   return launched("sf_convert");
 }
 
 int sf_dot(long long n, const double* x, const double* y, double* out_dev, double* scratch, void* stream) {
-  if (n < 0 || !out_dev || !scratch || (n && (!x || !y))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !out_dev || !scratch || (n && (!x || !y))) return invalid("sf_dot", "negative length or null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   k_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(n, x, y, scratch);
   k_dot_final<<<1, 1024, 0, st>>>(scratch, out_dev);
@@ -199,7 +213,9 @@ int sf_dot(long long n, const double* x, const double* y, double* out_dev, doubl
 
 int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* x, double* w, const double* y,
                 double* out_dev, double* scratch, void* stream) {
-  if (n < 0 || !coef_dev || !out_dev || !scratch || (n && (!x || !w))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !coef_dev || !out_dev || !scratch || (n && (!x || !w)))
+    return invalid("sf_axpy_dot", "negative length or null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   k_axpy_dot_partial<<<kDotBlocks, kThreads, 0, st>>>(n, sign, coef_dev, x, w, y, scratch);
   k_dot_final<<<1, 1024, 0, st>>>(scratch, out_dev);
@@ -208,7 +224,9 @@ int sf_axpy_dot(long long n, double sign, const double* coef_dev, const double* 
 
 int sf_dot2(long long n, const double* x1, const double* x2, const double* y, double* out1_dev, double* out2_dev,
             double* scratch2, void* stream) {
-  if (n < 0 || !out1_dev || !out2_dev || !scratch2 || (n && (!x1 || !x2 || !y))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !out1_dev || !out2_dev || !scratch2 || (n && (!x1 || !x2 || !y)))
+    return invalid("sf_dot2", "negative length or null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   k_dot2_partial<<<kDotBlocks, kThreads, 0, st>>>(n, x1, x2, y, scratch2, scratch2 + kDotBlocks);
   k_dot_final<<<1, 1024, 0, st>>>(scratch2, out1_dev);
@@ -217,11 +235,14 @@ int sf_dot2(long long n, const double* x1, const double* x2, const double* y, do
 }
 
 int sf_lincomb(long long n, int m, const double* const* vecs, const double* coefs, double* out, void* stream) {
-  if (n < 0 || m < 0 || m > kMaxTerms || !out || (m && (!vecs || !coefs))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !out) return invalid("sf_lincomb", "negative length or null output");
+  if (m < 0 || m > kMaxTerms) return invalid("sf_lincomb", "term count must lie in [0, SF_LINCOMB_MAX_TERMS]");
+  if (m && (!vecs || !coefs)) return invalid("sf_lincomb", "null term arrays");
   if (n == 0) return SF_OK;
   LinComb lc;
   for (int t = 0; t < m; ++t) {
-    if (!vecs[t]) return SF_EINVAL;
+    if (!vecs[t]) return invalid("sf_lincomb", "null term vector");
     lc.v[t] = vecs[t];
     lc.c[t] = coefs[t];
   }
@@ -230,24 +251,35 @@ int sf_lincomb(long long n, int m, const double* const* vecs, const double* coef
 }
 
 int sf_axpy_dev(long long n, double sign, const double* coef_dev, const double* x, double* y, void* stream) {
-  if (n < 0 || !coef_dev || (n && (!x || !y))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || !coef_dev || (n && (!x || !y))) return invalid("sf_axpy_dev", "negative length or null pointer");
   if (n == 0) return SF_OK;
   k_axpy_dev<<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, sign, coef_dev, x, y);
   return launched("sf_axpy_dev");
 }
 
 int sf_axpby(long long n, double alpha, const double* x, double beta, double* y, void* stream) {
-  if (n < 0 || (n && (!x || !y))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !y))) return invalid("sf_axpby", "negative length or null vector");
   if (n == 0) return SF_OK;
   k_axpby<double><<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
   return launched("sf_axpby");
 }
 
 int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream) {
-  if (n < 0 || (n && (!x || !y))) return SF_EINVAL;
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !y))) return invalid("sf_axpby_f32", "negative length or null vector");
   if (n == 0) return SF_OK;
   k_axpby<float><<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
   return launched("sf_axpby_f32");
+}
+
+int sf_div(long long n, const double* x, double d, double* y, void* stream) {
+  g_err[0] = 0;
+  if (n < 0 || (n && (!x || !y))) return invalid("sf_div", "negative length or null vector");
+  if (n == 0) return SF_OK;
+  k_div<<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, x, d, y);
+  return launched("sf_div");
 }
 
 }  // extern "C"

@@ -120,6 +120,11 @@ def axpby(alpha: float, x: torch.Tensor, beta: float, y: torch.Tensor):
     _native.check(rc, "sf_axpby")
 
 
+def div(x: torch.Tensor, d: float, y: torch.Tensor):
+    """y = x / d (fp64, IEEE division: the reference's normalisation rounding)."""
+    _native.check(_native.lib().sf_div(x.numel(), ptr(x), float(d), ptr(y), stream_ptr()), "sf_div")
+
+
 def convert(src: torch.Tensor, dst: torch.Tensor):
     code = {torch.float64: 0, torch.float32: 1}
     _native.check(_native.lib().sf_convert(src.numel(), ptr(src), code[src.dtype], ptr(dst), code[dst.dtype],

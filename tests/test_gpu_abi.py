@@ -67,3 +67,92 @@ def test_batched_vmult_equals_single_vmults():
     vmult_device(hier, 2, U, V, sf.PrecisionMode.FP64, batch=5)
     for i in range(5):
         assert torch.equal(V[i], sf.apply_operator(hier, 2, U[i].contiguous()))
+
+
+def _chain(vecs, coefs, n):
+    out = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for v, c in zip(vecs, coefs):
+        device.axpby(float(c), v, 1.0, out)
+    return out
+
+
+@pytest.mark.parametrize("m", [0, 1, 7, _native.SF_LINCOMB_MAX_TERMS])
+def test_lincomb_is_bitwise_the_axpby_chain(m):
+    n = 100_003
+    g = torch.Generator(device="cuda")
+    g.manual_seed(m)
+    vecs = [torch.randn(n, dtype=torch.float64, device="cuda", generator=g) for _ in range(m)]
+    coefs = np.random.default_rng(m).standard_normal(m)
+    out = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+    device.lincomb(vecs, coefs, out)
+    assert torch.equal(out, _chain(vecs, coefs, n))  # m = 0 writes zeros
+
+
+def test_lincomb_rejects_more_terms_than_the_limit():
+    n = 64
+    vecs = [torch.ones(n, dtype=torch.float64, device="cuda")] * (_native.SF_LINCOMB_MAX_TERMS + 1)
+    with pytest.raises(ValueError, match="term count"):
+        device.lincomb(vecs, np.ones(len(vecs)), torch.empty(n, dtype=torch.float64, device="cuda"))
+
+
+def test_axpy_dot_norm_form_and_dot2_are_bitwise_the_separate_ops():
+    n = 300_001
+    x, w, y = (torch.randn(n, dtype=torch.float64, device="cuda") for _ in range(3))
+    coef = torch.tensor([0.37], dtype=torch.float64, device="cuda")
+    for yy in (y, None):
+        w1, w2 = w.clone(), w.clone()
+        o1 = torch.empty(1, dtype=torch.float64, device="cuda")
+        o2 = torch.empty(1, dtype=torch.float64, device="cuda")
+        device.axpy_dot(-1.0, coef, x, w1, yy, o1)
+        device.axpy_dev(-1.0, coef, x, w2)
+        device.dot(yy if yy is not None else w2, w2, o2)
+        assert torch.equal(w1, w2) and torch.equal(o1, o2)
+    a1, a2, b1, b2 = (torch.empty(1, dtype=torch.float64, device="cuda") for _ in range(4))
+    device.dot2(x, w, y, a1, a2)
+    device.dot(x, y, b1)
+    device.dot(w, y, b2)
+    assert torch.equal(a1, b1) and torch.equal(a2, b2)
+
+
+def test_div_rounds_like_the_reference_division():
+    x = torch.randn(10_007, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    d = 3.000000000000001
+    device.div(x, d, y)
+    assert np.array_equal(y.cpu().numpy(), x.cpu().numpy() / d)  # numpy's IEEE division, bitwise
+
+
+def test_krylov_solution_update_fallback_beyond_the_lincomb_limit(monkeypatch):
+    """m > SF_LINCOMB_MAX_TERMS takes the axpby chain; with a lowered limit the two paths agree bitwise."""
+    from paper_2407_09621_b200 import krylov
+
+    rng = np.random.default_rng(5)
+    Q, _ = np.linalg.qr(rng.standard_normal((60, 60)))
+    A = Q @ np.diag(np.geomspace(1, 1e3, 60)) @ Q.T
+    b = rng.standard_normal(60)
+    At = torch.from_numpy(A).cuda()
+    apply = lambda v: At @ v
+    bt = torch.from_numpy(b).cuda()
+    x1, r1 = sf.fgmres(apply, None, bt, tol=1e-12, maxit=60)
+    monkeypatch.setattr(_native, "SF_LINCOMB_MAX_TERMS", 3)
+    x2, r2 = sf.fgmres(apply, None, bt, tol=1e-12, maxit=60)
+    assert r1.iterations == r2.iterations > 3
+    assert torch.equal(x1, x2)
+
+
+@pytest.mark.parametrize("solver", ["fgmres", "gmres"])
+def test_fused_mgs_toggle_is_bitwise_for_both_solvers(monkeypatch, solver):
+    from paper_2407_09621_b200 import krylov
+
+    hier = sf.build_hierarchy(3, 3)
+    mg = sf.MultigridPreconditioner(hier)
+    b = torch.randn(hier.n_dofs(3), dtype=torch.float64, device="cuda")
+    A = lambda v: sf.apply_operator(hier, 3, v)
+    M = lambda v: mg.apply(v, 3)
+    run = getattr(sf, solver)
+    xa, ra = run(A, M, b, tol=1e-9, maxit=30)
+    monkeypatch.setattr(krylov, "FUSED_MGS", False)
+    xb, rb = run(A, M, b, tol=1e-9, maxit=30)
+    assert ra.iterations == rb.iterations
+    assert ra.residual_history == rb.residual_history
+    assert torch.equal(xa, xb)
