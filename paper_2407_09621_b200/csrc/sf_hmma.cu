@@ -446,7 +446,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
     const int i = threadIdx.x + k2 * kThreads;
     const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
-    q4[k2] = __ldg(reinterpret_cast<const float4*>(ub + z * T.sz + y * T.sy + x4));
+    const float* src = ub + z * T.sz + y * T.sy + x4;
+    if constexpr (KK == 2) {  // shifted colours start at an odd cell: only 8-byte alignment
+      const float2 lo = __ldg(reinterpret_cast<const float2*>(src)), hi = __ldg(reinterpret_cast<const float2*>(src + 2));
+      q4[k2] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    } else {
+      q4[k2] = __ldg(reinterpret_cast<const float4*>(src));
+    }
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q4[k2].x), fabsf(q4[k2].y)), fmaxf(fabsf(q4[k2].z), fabsf(q4[k2].w))));
   }
   smax(&T.s_exp[0], mx);
