@@ -1,21 +1,32 @@
-// FP16 / FP16-EC tensor-core kernels for Q7 (K = 8): vmult and smoother colour
-// pass with mma.sync.m16n8k16 (f16 x f16 -> f32), ldmatrix/stmatrix operand
-// staging and the reference's per-contraction demotion semantics
-// (precision.py:206-230):
-//   fp16    : every contraction's input tensor and matrix are binary16 (RNE,
-//             subnormals kept); products are exact in f32; f32 accumulation.
-//   fp16_ec : main = A_h B_h, corr = A_d B_h + A_h B_d with the 2^11-scaled
-//             residual halves d; result = main + corr / 2048.
-// Intermediate tensors therefore live in shared memory as binary16 (plus the
-// residual half for EC): demotion happens exactly once, where the reference's
-// next contraction would demote them.
+// FP16 / FP16-EC tensor-core kernels: vmult, smoother colour pass and fused residual +
+// restriction on 16^3-point tiles (Q7: one 2x2x2-cell vertex patch; Q3 / Q1: 16-point
+// lines of 4 / 8 cells), mma.sync f16 x f16 -> f32 with ldmatrix / stmatrix staging and
+// the reference's per-contraction demotion semantics (precision.py:206-230):
+//   fp16    : every contraction's input tensor and matrix are binary16 (RNE, subnormals
+//             kept); products exact in f32; f32 accumulation.
+//   fp16_ec : main = A_h B_h, corr = A_d B_h + A_h B_d with the 2^11-scaled residual
+//             halves d; result = main + corr / 2048.
+// Intermediate tensors live in shared memory as binary16 (plus the residual half for
+// EC): demotion happens exactly once, where the reference's next contraction would
+// demote them.
 //
-// Tile = 2x2x2 cells = 16^3 dofs, 4 warps, f32 vectors in HBM (fp32 storage).
-// One 16-line group is one m16 MMA tile; a 16 -> 16 line operator is two
-// m16n8k16 MMAs.  Same cell-wise schedule as the FP64 path (sf_dmma.cuh):
+// Schedule per tile (same cell-wise form as the FP64 path, sf_dmma.cuh):
 //   x: a = Mx u, b = Lx u (+halo) | y: c = My a, dd = Ly a (+halo) + My b | z: v = Lz c (+halo) + Mz dd
-// The accumulator fragment of m16n8k16 is the A fragment of the next MMA, so
-// contractions along the same axis chain in registers (smoother: z fwd, x fwd/bwd).
+// CTA = 4 warps; warp w owns z planes 4w..4w+3 in the x / y stages and y rows 4w..4w+3 in the z
+// stages.  A 16-line group is one m16 MMA tile; a 16 -> 16 line operator is two n8 tiles.
+//
+// Instruction budget (this kernel family is issue- and HMMA-bound, profiles/r02_hmma.md):
+//  * B operands: per-lane 32-byte table rows (two 128-bit loads per operator), loaded once
+//    per tile, not per plane;
+//  * block-diagonal operators (M, and the Q3 / Q1 patch transforms): the EC correction of an
+//    n8 tile needs only its own 8 inputs, so A_h B_d + A_d B_h is ONE k16 MMA with the
+//    (h, d) fragment halves stacked along k -- 4 instead of 6 HMMA per 16 x 16 operator;
+//  * the rank-2 face coupling to the neighbour tiles (alpha, beta traces) is a k8 MMA on
+//    pre-split halo words (no per-line branches or FFMA chains);
+//  * the EC split h = half(x), d = half(2048 (x - h)) runs as one packed cvt, one mixed
+//    f16*f16+f32 FHFMA and one FMUL per element;
+//  * the patch eigenvalue division uses a per-level table of the f32 denominators and their
+//    reciprocals (correctly rounded quotient via Markstein's fma correction).
 // Shared layout (halves): z*264 + y*16 + 8*((x>>3) ^ ((y>>2)&1)) + (x&7): every
 // ldmatrix/stmatrix 8x8 access (rows along y or z) is bank-conflict free.
 #include <cuda_fp16.h>
@@ -33,11 +44,22 @@
 namespace sf {
 namespace hm {
 
-constexpr int K = 8, B = 16;
+constexpr int K = 8;
 constexpr int PZ = 264;            // halves per z plane (256 + 8 pad)
 constexpr int TVOL = 16 * PZ;      // halves per tile tensor
 constexpr int kThreads = 128;      // 4 warps
 constexpr float kEc = 2048.0f;
+constexpr float kInvEc = 1.0f / 2048.0f;
+
+// shared memory map (bytes): U_h | U_d | B_h | B_d | halo words | exponent words.
+// During the prologue the B region holds the f32 face-trace planes (and, for EC, the
+// staged x-neighbour cell layers).
+constexpr int SM_UH = 0, SM_UD = 2 * TVOL, SM_BH = 4 * TVOL, SM_BD = 6 * TVOL;
+constexpr int SM_HALO = 8 * TVOL;                 // [axis][p 16][q 16] x 16 B
+constexpr int SM_EXP = SM_HALO + 3 * 256 * 16;
+constexpr int kSmem = SM_EXP + 16;
+constexpr int PLP = 17;                           // f32 trace plane pitch
+constexpr int PLS = 16 * PLP;                     // floats per trace plane
 
 __device__ __forceinline__ int hidx(int z, int y, int x) {
   return z * PZ + y * 16 + ((((x >> 3) ^ (y >> 2)) & 1) << 3) + (x & 7);
@@ -50,47 +72,60 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-__device__ __forceinline__ void ldsm4(unsigned (&r)[4], const __half* p) {
+__device__ __forceinline__ void ldsm4(unsigned (&r)[4], unsigned addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(p)));
+               : "r"(addr));
 }
-__device__ __forceinline__ void ldsm4t(unsigned (&r)[4], const __half* p) {
+__device__ __forceinline__ void ldsm4t(unsigned (&r)[4], unsigned addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(p)));
+               : "r"(addr));
 }
-__device__ __forceinline__ void stsm4(__half* p, const unsigned (&r)[4]) {
-  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(smem_u32(p)), "r"(r[0]),
-               "r"(r[1]), "r"(r[2]), "r"(r[3])
+__device__ __forceinline__ void stsm4(unsigned addr, const unsigned (&r)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
                : "memory");
 }
-__device__ __forceinline__ void stsm4t(__half* p, const unsigned (&r)[4]) {
-  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(smem_u32(p)),
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+__device__ __forceinline__ void stsm4t(unsigned addr, const unsigned (&r)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
                : "memory");
 }
 
 // D(16x8,f32) += A(16x16,f16) B(16x8,f16)
-__device__ __forceinline__ void hmma(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+__device__ __forceinline__ void hmma16(float (&d)[4], unsigned a0, unsigned a1, unsigned a2, unsigned a3, unsigned b0,
+                                       unsigned b1) {
   asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// D(16x8,f32) += A(16x8,f16) B(8x8,f16)
+__device__ __forceinline__ void hmma8(float (&d)[4], unsigned a0, unsigned a1, unsigned b0) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
 }
 
-__device__ __forceinline__ unsigned pack2(float lo, float hi) {
-  __half2 h = __halves2half2(__float2half_rn(lo), __float2half_rn(hi));
-  return *reinterpret_cast<unsigned*>(&h);
-}
-__device__ __forceinline__ float2 unpack2(unsigned u) {
-  __half2 h = *reinterpret_cast<__half2*>(&u);
-  return __half22float2(h);
-}
-
-// A 16-line x 16-output accumulator: two n8 tiles, f32; EC keeps main and corr.
+// (x0, x1) -> packed binary16 main halves h (and for EC the packed residual halves
+// d = half(2048 (x - h))).  x - h is exact in f32 (one mixed-precision FHFMA per element).
 template <int MODE>
-struct Acc16 {
+__device__ __forceinline__ void demote_pair(float x0, float x1, unsigned& h, unsigned& d) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(h) : "f"(x1), "f"(x0));
+  if constexpr (MODE == MODE_FP16_EC) {
+    float r0, r1;
+    asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n"
+        " fma.rn.f32.f16 %0, lo, %5, %3;\n fma.rn.f32.f16 %1, hi, %5, %4;\n}\n"
+        : "=f"(r0), "=f"(r1)
+        : "r"(h), "f"(x0), "f"(x1), "h"((unsigned short)0xBC00));  // -1.0 in binary16
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(d) : "f"(r1 * kEc), "f"(r0 * kEc));
+  }
+}
+
+// A 16-line x 16-output accumulator: two n8 tiles; EC keeps main and corr.
+template <int MODE>
+struct HAcc {
   float m[2][4];
   float c[2][4];
   __device__ __forceinline__ void zero() {
@@ -99,63 +134,75 @@ struct Acc16 {
 #pragma unroll
       for (int i = 0; i < 4; ++i) m[nt][i] = c[nt][i] = 0.f;
   }
-  // output value (nt, i) after the contraction: main (+ corr/2048 for EC)
   __device__ __forceinline__ float val(int nt, int i) const {
-    if constexpr (MODE == MODE_FP16_EC) return m[nt][i] + c[nt][i] / kEc;
+    if constexpr (MODE == MODE_FP16_EC) return fmaf(c[nt][i], kInvEc, m[nt][i]);
     return m[nt][i];
+  }
+  __device__ __forceinline__ void vals(float (&v)[2][4]) const {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[nt][i] = val(nt, i);
   }
 };
 
-// A fragment of one operand tensor: main halves (+ EC residual halves)
-template <int MODE>
-struct AFrag {
+// A fragment (16 lines x 16 k) of one operand tensor: main halves (+ EC residual halves)
+struct HFrag {
   unsigned h[4];
   unsigned d[4];
 };
 
-// B fragments of one 16x16 operator: [nt][reg] (+ EC residual)
-template <int MODE>
-struct BFrag {
-  unsigned h[2][2];
-  unsigned d[2][2];
+// B fragments of one 16x16 operator for this lane: word nt*2 + j = rows 2t+8j (+1), column 8nt+g
+struct HOpFrag {
+  unsigned h[4];
+  unsigned d[4];
 };
 
+// dense 16 -> 16 operator: 2 (fp16) / 6 (EC) HMMA
 template <int MODE>
-__device__ __forceinline__ void mma16(Acc16<MODE>& acc, const AFrag<MODE>& a, const BFrag<MODE>& b) {
+__device__ __forceinline__ void mma_dense(HAcc<MODE>& acc, const HFrag& a, const HOpFrag& b) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
-    hmma(acc.m[nt], a.h, b.h[nt][0], b.h[nt][1]);
+    hmma16(acc.m[nt], a.h[0], a.h[1], a.h[2], a.h[3], b.h[2 * nt], b.h[2 * nt + 1]);
     if constexpr (MODE == MODE_FP16_EC) {
-      hmma(acc.c[nt], a.h, b.d[nt][0], b.d[nt][1]);  // c(mh, du) part: A_h B_d ...
-      hmma(acc.c[nt], a.d, b.h[nt][0], b.h[nt][1]);  // ... and A_d B_h
+      hmma16(acc.c[nt], a.h[0], a.h[1], a.h[2], a.h[3], b.d[2 * nt], b.d[2 * nt + 1]);
+      hmma16(acc.c[nt], a.d[0], a.d[1], a.d[2], a.d[3], b.h[2 * nt], b.h[2 * nt + 1]);
     }
   }
 }
 
-// split an f32 value into the operand halves of the mode
+// block-diagonal operator (two 8 x 8 blocks): n tile nt only reads inputs 8nt..8nt+7, so the
+// EC correction A_h B_d + A_d B_h of a tile is one k16 MMA over the stacked (h | d) halves.
 template <int MODE>
-__device__ __forceinline__ void split(float x, float& h, float& d) {
-  h = __half2float(__float2half_rn(x));
-  d = (MODE == MODE_FP16_EC) ? __half2float(__float2half_rn((x - h) * kEc)) : 0.f;
-}
-
-// accumulator fragment -> A fragment of the next MMA (same axis), with demotion.
-// Pairs are rounded with one packed cvt (cvt.rn.f16x2.f32) and the EC residual is formed from
-// the packed halves directly -- the same values as split() + pack2() with ~40 % fewer
-// instructions (the F2FP/HADD2 chain was the largest instruction class, profiles/r01_smoother_fp16.md).
-template <int MODE>
-__device__ __forceinline__ void demote_pair(float x0, float x1, unsigned& h, unsigned& d) {
-  const __half2 hh = __floats2half2_rn(x0, x1);
-  h = *reinterpret_cast<const unsigned*>(&hh);
+__device__ __forceinline__ void mma_bd(HAcc<MODE>& acc, const HFrag& a, const HOpFrag& b) {
+  hmma8(acc.m[0], a.h[0], a.h[1], b.h[0]);
+  hmma8(acc.m[1], a.h[2], a.h[3], b.h[3]);
   if constexpr (MODE == MODE_FP16_EC) {
-    const float2 hf = __half22float2(hh);
-    const __half2 dd = __floats2half2_rn((x0 - hf.x) * kEc, (x1 - hf.y) * kEc);
-    d = *reinterpret_cast<const unsigned*>(&dd);
+    hmma16(acc.c[0], a.h[0], a.h[1], a.d[0], a.d[1], b.d[0], b.h[0]);
+    hmma16(acc.c[1], a.h[2], a.h[3], a.d[2], a.d[3], b.d[3], b.h[3]);
   }
 }
 
+template <int MODE, bool BD>
+__device__ __forceinline__ void mma_op(HAcc<MODE>& acc, const HFrag& a, const HOpFrag& b) {
+  if constexpr (BD) mma_bd<MODE>(acc, a, b); else mma_dense<MODE>(acc, a, b);
+}
+
+// rank-2 face coupling of a stiffness accumulator: k8 A = the lines' halo words
+// (t = 0: alpha_h lo|hi, 1: beta_h, 2: alpha_d, 3: beta_d), B = hb (main nt0, nt1, corr nt0, nt1)
 template <int MODE>
-__device__ __forceinline__ void acc_to_a(const float (&v)[2][4], AFrag<MODE>& a) {
+__device__ __forceinline__ void mma_halo(HAcc<MODE>& acc, unsigned w0, unsigned w1, const unsigned (&hb)[4]) {
+  hmma8(acc.m[0], w0, w1, hb[0]);
+  hmma8(acc.m[1], w0, w1, hb[1]);
+  if constexpr (MODE == MODE_FP16_EC) {
+    hmma8(acc.c[0], w0, w1, hb[2]);
+    hmma8(acc.c[1], w0, w1, hb[3]);
+  }
+}
+
+// accumulator values -> A fragment of the next MMA along the same axis (with demotion)
+template <int MODE>
+__device__ __forceinline__ void to_frag(const float (&v)[2][4], HFrag& a) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     demote_pair<MODE>(v[nt][0], v[nt][1], a.h[2 * nt], a.d[2 * nt]);
@@ -164,63 +211,66 @@ __device__ __forceinline__ void acc_to_a(const float (&v)[2][4], AFrag<MODE>& a)
 }
 
 // ---------------------------------------------------------------- tables
-// B fragment of Op (16 out x 16 in) for lane ln, n tile nt, register j:
-//   (Op[8nt + (ln>>2)][2(ln&3) + 8j], Op[...][... + 1]) as half2 (+ EC residual half2)
+// Per-lane operator rows: w[lane][0] = h words, w[lane][1] = d words (uint4 each).
+struct HOp {
+  uint4 w[32][2];
+};
 struct HTables {
-  unsigned M[2][2][2][32];      // [h/d][nt][j][lane]  M_patch
-  unsigned L[4][2][2][2][32];   // [kind][h/d][nt][j][lane]  L_smooth[kind]
-  unsigned Vf[4][2][2][2][32];  // Op = V^T
-  unsigned Vb[4][2][2][2][32];  // Op = V
+  HOp M;          // M_line (block diagonal)
+  HOp L[4];       // L_line[kind]
+  HOp Vf[4];      // Op = V^T
+  HOp Vb[4];      // Op = V
+  uint4 halo[32];  // halo B words: main nt0, main nt1, corr nt0, corr nt1
   double lam[4][16];
-  float ucol[2][K], urow[2][K];  // [h/d] demoted halo vectors
+};
+// f32 eigenvalue-sum denominators and reciprocals for one kind combination, in the V_x^T
+// accumulator order: [z][lane][nt*4+i] (row y = g + 8(i>>1), column x = 8nt + 2t + (i&1))
+struct DenTab {
+  float d[16][32][8];
+  float r[16][32][8];
 };
 
-template <int MODE>
-__device__ __forceinline__ void load_b(BFrag<MODE>& b, const unsigned* t /* [2][2][2][32] */, int lane) {
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      b.h[nt][j] = __ldg(t + (0 * 4 + nt * 2 + j) * 32 + lane);
-      if constexpr (MODE == MODE_FP16_EC) b.d[nt][j] = __ldg(t + (1 * 4 + nt * 2 + j) * 32 + lane);
-    }
+__device__ __forceinline__ void ld_op(HOpFrag& b, const HOp& op, int lane) {
+  const uint4 h = __ldg(&op.w[lane][0]), d = __ldg(&op.w[lane][1]);
+  b.h[0] = h.x; b.h[1] = h.y; b.h[2] = h.z; b.h[3] = h.w;
+  b.d[0] = d.x; b.d[1] = d.y; b.d[2] = d.z; b.d[3] = d.w;
 }
 
 // ---------------------------------------------------------------- tile
 template <int MODE>
 struct HTile {
-  __half* uh;  // tensor U (h) ; EC residual at uh + 2*TVOL
-  __half* bh;  // tensor B (h) ; EC residual at bh + 2*TVOL
-  float* tr;   // V1 trace planes (12 x 16 x 17 f32)
-  int* s_exp;  // block-exponent words ([0] input, [1] residual)
-  int eu;      // input block exponent: u^ = 2^eu u
+  char* sm;
+  unsigned s0;  // shared-window address of the smem base
+  int* s_exp;   // block-exponent words ([0] input, [1] residual)
+  int eu;       // input block exponent: u^ = 2^eu u
   int cx, cy, cz;
   long long sy, sz;
   unsigned nbm;
   int kind[3];
-  int lane, warp, g, t;
-  float hur[2][2], huc[2][2];  // [h/d][i]: urow / ucol at output n = 2t + i of this lane (halo16)
-  int skip[3];                 // line tiles: leading points per axis owned by the previous tile
-  __device__ __forceinline__ __half* ud() const { return uh + 2 * TVOL; }
-  __device__ __forceinline__ __half* bd() const { return bh + 2 * TVOL; }
+  int lane, warp, g, t, q, j;
+  int skip[3];  // line tiles: leading points per axis owned by the previous tile
+  unsigned hb[4];  // halo B words of this lane
+  __device__ __forceinline__ unsigned UH() const { return s0 + SM_UH; }
+  __device__ __forceinline__ unsigned UD() const { return s0 + SM_UD; }
+  __device__ __forceinline__ unsigned BH() const { return s0 + SM_BH; }
+  __device__ __forceinline__ unsigned BD() const { return s0 + SM_BD; }
+  // ldmatrix / stmatrix lane offsets (bytes):
+  //  x stage (rows = y lines, k = x; non-trans): line j + 8(q&1), k0 = 8(q>>1)
+  __device__ __forceinline__ unsigned ox(int z) const { return 2u * hidx(z, j + 8 * (q & 1), 8 * (q >> 1)); }
+  //  y stage (rows = x lines, k = y; trans): krow = j + 8(q>>1), line0 = 8(q&1)
+  __device__ __forceinline__ unsigned oy(int z) const { return 2u * hidx(z, j + 8 * (q >> 1), 8 * (q & 1)); }
+  //  z stage (rows = x lines, k = z; trans) at row y
+  __device__ __forceinline__ unsigned oz(int y) const { return 2u * hidx(j + 8 * (q >> 1), y, 8 * (q & 1)); }
+  // this lane's halo words for plane p, lines g and g + 8 of an axis
+  __device__ __forceinline__ void halo(int axis, int p, unsigned& w0, unsigned& w1) const {
+    const unsigned* hw = reinterpret_cast<const unsigned*>(sm + SM_HALO) + ((axis * 16 + p) * 16) * 4 + t;
+    w0 = hw[g * 4];
+    w1 = hw[(g + 8) * 4];
+  }
 };
 
 template <int MODE>
-constexpr size_t smem_bytes() {
-  return sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL + sizeof(float) * 12 * 16 * 17 + 16;
-}
-
-// store a value into (h, d) tensors at half index i
-template <int MODE>
-__device__ __forceinline__ void put(__half* h, __half* d, int i, float x) {
-  float hh, dd;
-  split<MODE>(x, hh, dd);
-  h[i] = __float2half_rn(hh);
-  if constexpr (MODE == MODE_FP16_EC) d[i] = __float2half_rn(dd);
-}
-
-template <int MODE>
-__device__ __forceinline__ void ld_a(AFrag<MODE>& a, const __half* h, const __half* d, int off, bool trans) {
+__device__ __forceinline__ void ld_a(HFrag& a, unsigned h, unsigned d, unsigned off, bool trans) {
   if (trans) {
     ldsm4t(a.h, h + off);
     if constexpr (MODE == MODE_FP16_EC) ldsm4t(a.d, d + off);
@@ -229,14 +279,8 @@ __device__ __forceinline__ void ld_a(AFrag<MODE>& a, const __half* h, const __ha
     if constexpr (MODE == MODE_FP16_EC) ldsm4(a.d, d + off);
   }
 }
-
-// store accumulator values (already final f32) via stmatrix as (h, d)
 template <int MODE>
-__device__ __forceinline__ void st_acc(__half* h, __half* d, int off, const float (&v)[2][4], bool trans) {
-  AFrag<MODE> a;
-  acc_to_a<MODE>(v, a);
-  // A fragment regs (0: rows 0-7 k 0-7, 1: rows 8-15 k 0-7, 2: rows 0-7 k 8-15, 3: rows 8-15 k 8-15)
-  // map onto stmatrix matrices in the same order as the ldmatrix addressing used here.
+__device__ __forceinline__ void st_a(unsigned h, unsigned d, unsigned off, const HFrag& a, bool trans) {
   if (trans) {
     stsm4t(h + off, a.h);
     if constexpr (MODE == MODE_FP16_EC) stsm4t(d + off, a.d);
@@ -246,76 +290,23 @@ __device__ __forceinline__ void st_acc(__half* h, __half* d, int off, const floa
   }
 }
 
+// split f32 alpha / beta trace values into one 16-byte halo word (see mma_halo)
 template <int MODE>
-__device__ __forceinline__ void finals(const Acc16<MODE>& acc, float (&v)[2][4]) {
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[nt][i] = acc.val(nt, i);
+__device__ __forceinline__ void put_halo(char* sm, int axis, int p, int q, float al, float ah, float bl, float bh) {
+  unsigned ah2, ad2, bh2, bd2;
+  demote_pair<MODE_FP16_EC>(al, ah, ah2, ad2);
+  demote_pair<MODE_FP16_EC>(bl, bh, bh2, bd2);
+  if constexpr (MODE != MODE_FP16_EC) ad2 = 0;  // fp16: alpha is a demoted operand; beta keeps its residual
+  *reinterpret_cast<uint4*>(sm + SM_HALO + ((axis * 16 + p) * 16 + q) * 16) = make_uint4(ah2, bh2, ad2, bd2);
 }
 
-// ldmatrix / stmatrix lane address for a 16x16 operand:
-//   non-trans (rows along the "line" axis a1, k along x):  line = j + 8(q&1), k0 = 8(q>>1)
-//   trans     (memory rows along the k axis):                krow = j + 8(q>>1), line0 = 8(q&1)
-__device__ __forceinline__ void lane_qj(int lane, int& q, int& j) {
-  q = lane >> 3;
-  j = lane & 7;
-}
-
-// halo update on a stiffness accumulator of 16 lines; alpha/beta per line from the trace plane
+// Tangential mass of a y-face (Mx along q) or z-face (My along p) trace plane on the tensor cores:
+// plane = 16 x 16 f32 (pitch 17), A fragment gathered from f32 shared memory with demotion, in place.
 template <int MODE>
-__device__ __forceinline__ void halo16(const HTile<MODE>& T, Acc16<MODE>& acc, const HTables* tab, int axis,
-                                       const float* tr_lo_a, const float* tr_lo_b, const float* tr_hi_a,
-                                       const float* tr_hi_b) {
-  // lines g and g+8 (rows of the accumulator), outputs n = 8nt + 2t + {0,1}
-  const int g = T.g, t2 = 2 * T.t;
-#pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int line = g + 8 * rr;
-    if ((T.nbm >> (2 * axis)) & 1) {  // lo neighbour -> cell 0 outputs (nt = 0)
-      float ah, ad;
-      split<MODE>(tr_lo_a[line], ah, ad);
-      const float bet = tr_lo_b[line];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        acc.m[0][2 * rr + i] = fmaf(T.hur[0][i], ah, acc.m[0][2 * rr + i]);
-        if constexpr (MODE == MODE_FP16_EC) {
-          acc.c[0][2 * rr + i] = fmaf(T.hur[1][i], ah, acc.c[0][2 * rr + i]);
-          acc.c[0][2 * rr + i] = fmaf(T.hur[0][i], ad, acc.c[0][2 * rr + i]);
-        }
-      }
-      if (t2 == 0) acc.m[0][2 * rr] += bet;
-    }
-    if ((T.nbm >> (2 * axis + 1)) & 1) {  // hi neighbour -> cell 1 outputs (nt = 1)
-      float ah, ad;
-      split<MODE>(tr_hi_a[line], ah, ad);
-      const float bet = tr_hi_b[line];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        acc.m[1][2 * rr + i] = fmaf(T.huc[0][i], ah, acc.m[1][2 * rr + i]);
-        if constexpr (MODE == MODE_FP16_EC) {
-          acc.c[1][2 * rr + i] = fmaf(T.huc[1][i], ah, acc.c[1][2 * rr + i]);
-          acc.c[1][2 * rr + i] = fmaf(T.huc[0][i], ad, acc.c[1][2 * rr + i]);
-        }
-      }
-      if (t2 + 1 == K - 1) acc.m[1][2 * rr + 1] += bet;
-    }
-  }
-}
-
-template <int MODE>
-__device__ __forceinline__ const float* trp(const HTile<MODE>& T, int face, int plane) {
-  return T.tr + (face * 2 + plane) * (16 * 17);
-}
-
-// Tangential masses of the y-face (Mx along q) and z-face (Mx along q, then My
-// along p) trace planes on the tensor cores: plane = 16 x 16 f32 (pitch 17),
-// A fragment gathered from f32 shared memory with demotion, in place.
-template <int MODE>
-__device__ __forceinline__ void plane_mass(float* P, bool along_p, const BFrag<MODE>& bm, int g, int t) {
+__device__ __forceinline__ void plane_mass(float* P, bool along_p, const HOpFrag& bm, int g, int t) {
   float v[2][4];
   // A[row][k]: along q: row = p, k = q;  along p: row = q, k = p
-  auto at = [&](int row, int k) -> float { return along_p ? P[k * 17 + row] : P[row * 17 + k]; };
+  auto at = [&](int row, int k) -> float { return along_p ? P[k * PLP + row] : P[row * PLP + k]; };
 #pragma unroll
   for (int kb = 0; kb < 2; ++kb) {
     v[kb][0] = at(g, 8 * kb + 2 * t);
@@ -323,37 +314,19 @@ __device__ __forceinline__ void plane_mass(float* P, bool along_p, const BFrag<M
     v[kb][2] = at(g + 8, 8 * kb + 2 * t);
     v[kb][3] = at(g + 8, 8 * kb + 2 * t + 1);
   }
-  AFrag<MODE> a;
-  acc_to_a<MODE>(v, a);  // same register order as an accumulator fragment
-  Acc16<MODE> acc;
+  HFrag a;
+  to_frag<MODE>(v, a);  // same register order as an accumulator fragment
+  HAcc<MODE> acc;
   acc.zero();
-  mma16<MODE>(acc, a, bm);
+  mma_bd<MODE>(acc, a, bm);
   __syncwarp();
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int row = g + 8 * (i >> 1), n = 8 * nt + 2 * t + (i & 1);
-      if (along_p) P[n * 17 + row] = acc.val(nt, i); else P[row * 17 + n] = acc.val(nt, i);
+      if (along_p) P[n * PLP + row] = acc.val(nt, i); else P[row * PLP + n] = acc.val(nt, i);
     }
-}
-
-template <int MODE>
-__device__ __forceinline__ void trace_masses_tc(const HTile<MODE>& T, const HTables* tab) {
-  BFrag<MODE> bm;
-  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
-  // 8 planes (faces 2..5, alpha/beta) along q, two per warp
-  for (int task = T.warp; task < 8; task += kThreads / 32) {
-    const int face = 2 + (task >> 1);
-    if (!((T.nbm >> face) & 1)) continue;
-    plane_mass<MODE>(T.tr + (face * 2 + (task & 1)) * (16 * 17), false, bm, T.g, T.t);
-  }
-  __syncthreads();
-  for (int task = T.warp; task < 4; task += kThreads / 32) {
-    const int face = 4 + (task >> 1);
-    if (!((T.nbm >> face) & 1)) continue;
-    plane_mass<MODE>(T.tr + (face * 2 + (task & 1)) * (16 * 17), true, bm, T.g, T.t);
-  }
 }
 
 // L2 prefetch of this tile's rows of b (read in the z stage of the colour / restriction kernels)
@@ -376,25 +349,22 @@ __device__ __forceinline__ void prefetch_b_rows(const Geom& g, const float* __re
   }
 }
 
-// prologue + x/y stages; leaves c in U and dd in B (f16 tensors), trace planes ready
-// KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells); the tile is a
-// 16^3-point box either way, the line operators come from the tables.
+// prologue + x/y stages; leaves c in U and dd in B (f16 tensors), halo words ready.
+// KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells).
 template <int MODE, int KK = K>
 __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<KK, MODE>& op,
                                            const HTables* tab, const float* __restrict__ u) {
-  T.uh = reinterpret_cast<__half*>(smem);
-  T.bh = T.uh + TVOL;
-  T.tr = reinterpret_cast<float*>(smem + sizeof(__half) * (MODE == MODE_FP16_EC ? 4 : 2) * TVOL);
-  if (MODE == MODE_FP16_EC) T.bh = T.uh + TVOL;  // layout: uh | bh | ud | bd
-  T.s_exp = reinterpret_cast<int*>(T.tr + 12 * 16 * 17);
+  T.sm = smem;
+  T.s0 = smem_u32(smem);
+  T.s_exp = reinterpret_cast<int*>(smem + SM_EXP);
+  float* tr = reinterpret_cast<float*>(smem + SM_BH);  // f32 trace planes [face][alpha/beta][16][17]
   constexpr int CPL = 16 / KK;
   TileEngine<KK, MODE, 1, 16> e(smem, g);
-  e.tr = T.tr;
+  e.tr = tr;
   e.s_exp = T.s_exp;
   int cx, cy, cz;
   if (!e.tile_cells(g, 0, cx, cy, cz)) return false;
   if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
-  __syncthreads();
   T.cx = cx; T.cy = cy; T.cz = cz;
   T.skip[0] = e.skip[0]; T.skip[1] = e.skip[1]; T.skip[2] = e.skip[2];
   T.sy = e.sy; T.sz = e.sz;
@@ -411,27 +381,26 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   T.warp = threadIdx.x >> 5;
   T.g = T.lane >> 2;
   T.t = T.lane & 3;
-#pragma unroll
-  for (int hd = 0; hd < 2; ++hd)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {  // zero for lanes whose outputs are not in the line's first / last cell
-      const int n0 = 2 * T.t + i, n1 = 2 * T.t + i - (8 - KK);
-      T.hur[hd][i] = n0 < KK ? __ldg(&tab->urow[hd][n0]) : 0.f;
-      T.huc[hd][i] = n1 >= 0 ? __ldg(&tab->ucol[hd][n1]) : 0.f;
-    }
+  T.q = T.lane >> 3;
+  T.j = T.lane & 7;
+  {
+    const uint4 w = __ldg(&tab->halo[T.lane]);
+    T.hb[0] = w.x; T.hb[1] = w.y; T.hb[2] = w.z; T.hb[3] = w.w;
+  }
+  __syncthreads();
   // tile -> registers -> block exponent -> scaled (h, d) tensors
   const float* ub = u + (long long)(cz * KK) * T.sz + (long long)(cy * KK) * T.sy + cx * KK;
-  // EC: the two x-neighbour cell layers (256 rows of KK floats per face) go to the still-free
-  // B tensors by cp.async -- coalesced 16-byte chunks instead of per-lane KK-float loads that
-  // touch 32 cache lines per warp instruction; the x traces are formed from shared memory below.
+  // EC: the two x-neighbour cell layers (256 rows of KK floats per face) go to the B region by
+  // cp.async -- coalesced 16-byte chunks; the x traces are formed from shared memory below.
   constexpr bool kStageX = (MODE == MODE_FP16_EC) && (KK == 8 || KK == 4);
   constexpr int XC = KK / 4;  // 16-byte chunks per staged row
+  float* xs = reinterpret_cast<float*>(smem + SM_BH);  // [hi][row 256][KK]
   if constexpr (kStageX) {
     const int sy = (int)T.sy, sz = (int)T.sz;
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       if (!((T.nbm >> hi) & 1)) continue;
-      float* dst = reinterpret_cast<float*>(hi ? T.bd() : T.bh);
+      float* dst = xs + hi * 256 * KK;
 #pragma unroll
       for (int k2 = 0; k2 < 256 * XC / kThreads; ++k2) {
         const int c = threadIdx.x + kThreads * k2, ch = c % XC, row = c / XC, y = row & 15, z = row >> 4;
@@ -461,6 +430,8 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   T.eu = block_exp(__int_as_float(T.s_exp[0]));
   e.eu = T.eu;
   const float us = pow2f(T.eu);
+  __half* uh = reinterpret_cast<__half*>(smem + SM_UH);
+  __half* ud = reinterpret_cast<__half*>(smem + SM_UD);
 #pragma unroll
   for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
     const int i = threadIdx.x + k2 * kThreads;
@@ -470,127 +441,149 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     demote_pair<MODE>(q4[k2].x * us, q4[k2].y * us, hv.x, dv.x);
     demote_pair<MODE>(q4[k2].z * us, q4[k2].w * us, hv.y, dv.y);
     const int o = hidx(z, y, x4);
-    *reinterpret_cast<uint2*>(T.uh + o) = hv;
-    if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(T.ud() + o) = dv;
+    *reinterpret_cast<uint2*>(uh + o) = hv;
+    if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(ud + o) = dv;
   }
   if constexpr (kStageX) {
-    // x traces from the staged rows: item (hi, p = z, q = y); EC beta in fp32 (as TileEngine::traces)
+    // x traces from the staged rows: line (p = z, q = y), both faces; EC beta in fp32 (as TileEngine::traces)
 #pragma unroll
-    for (int k2 = 0; k2 < 512 / kThreads; ++k2) {
-      const int it = threadIdx.x + kThreads * k2, hi = it >> 8, row = it & 255, p = row >> 4, q = row & 15;
-      if (!((T.nbm >> hi) & 1)) continue;
-      const float* src = reinterpret_cast<const float*>(hi ? T.bd() : T.bh) + row * KK;
-      float w[KK];
+    for (int k2 = 0; k2 < 256 / kThreads; ++k2) {
+      const int row = threadIdx.x + kThreads * k2, p = row >> 4, qq = row & 15;
+      float a2[2] = {0.f, 0.f}, b2[2] = {0.f, 0.f};
 #pragma unroll
-      for (int ch = 0; ch < XC; ++ch) {
-        const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;
-        const float4 v4 = *reinterpret_cast<const float4*>(src + 4 * sw);
-        w[4 * ch] = v4.x; w[4 * ch + 1] = v4.y; w[4 * ch + 2] = v4.z; w[4 * ch + 3] = v4.w;
+      for (int hi = 0; hi < 2; ++hi) {
+        if (!((T.nbm >> hi) & 1)) continue;
+        const float* src = xs + hi * 256 * KK + row * KK;
+        float w[KK];
+#pragma unroll
+        for (int ch = 0; ch < XC; ++ch) {
+          const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;
+          const float4 v4 = *reinterpret_cast<const float4*>(src + 4 * sw);
+          w[4 * ch] = v4.x; w[4 * ch + 1] = v4.y; w[4 * ch + 2] = v4.z; w[4 * ch + 3] = v4.w;
+        }
+        float bs = 0.f;
+        if (hi) {
+          a2[1] = w[0] * us;
+#pragma unroll
+          for (int jj = 1; jj < KK; ++jj) bs = fmaf(op.urow[jj].h + op.urow[jj].d / kEcScale, w[jj] * us, bs);
+        } else {
+          a2[0] = w[KK - 1] * us;
+#pragma unroll
+          for (int jj = 0; jj < KK - 1; ++jj) bs = fmaf(op.ucol[jj].h + op.ucol[jj].d / kEcScale, w[jj] * us, bs);
+        }
+        b2[hi] = bs;
       }
-      float alpha, bs = 0.f;
-      if (hi) {
-        alpha = w[0] * us;
-#pragma unroll
-        for (int jj = 1; jj < KK; ++jj) bs = fmaf(op.urow[jj].h + op.urow[jj].d / kEcScale, w[jj] * us, bs);
-      } else {
-        alpha = w[KK - 1] * us;
-#pragma unroll
-        for (int jj = 0; jj < KK - 1; ++jj) bs = fmaf(op.ucol[jj].h + op.ucol[jj].d / kEcScale, w[jj] * us, bs);
-      }
-      float* pl = T.tr + (hi * 2) * (16 * 17);
-      pl[p * 17 + q] = alpha;
-      pl[16 * 17 + p * 17 + q] = bs;
+      put_halo<MODE>(smem, 0, p, qq, a2[0], a2[1], b2[0], b2[1]);
     }
+    __syncthreads();  // staged rows consumed before the trace planes overwrite them
     e.template traces<kThreads, 1>(g, op, u);
   } else {
     e.template traces<kThreads>(g, op, u);
   }
-  T.lane = threadIdx.x & 31;
-  T.warp = threadIdx.x >> 5;
-  T.g = T.lane >> 2;
-  T.t = T.lane & 3;
   __syncthreads();
-  trace_masses_tc<MODE>(T, tab);
+  // tangential masses: y faces (2, 3) Mx along q, z faces (4, 5) Mx along q then My along p
+  HOpFrag bm;
+  ld_op(bm, tab->M, T.lane);
+  for (int task = T.warp; task < 8; task += kThreads / 32) {
+    const int face = 2 + (task >> 1);
+    if (!((T.nbm >> face) & 1)) continue;
+    plane_mass<MODE>(tr + (face * 2 + (task & 1)) * PLS, false, bm, T.g, T.t);
+  }
+  __syncthreads();
+  for (int task = T.warp; task < 4; task += kThreads / 32) {
+    const int face = 4 + (task >> 1);
+    if (!((T.nbm >> face) & 1)) continue;
+    plane_mass<MODE>(tr + (face * 2 + (task & 1)) * PLS, true, bm, T.g, T.t);
+  }
+  __syncthreads();
+  // f32 planes -> halo words (domain-boundary faces contribute zero: Nitsche is in L_line[kind])
+  constexpr int A0 = kStageX ? 1 : 0;
+  for (int it = threadIdx.x; it < (3 - A0) * 256; it += kThreads) {
+    const int axis = A0 + (it >> 8), pq = it & 255, p = pq >> 4, qq = pq & 15;
+    const float* lo = tr + (4 * axis) * PLS + p * PLP + qq;   // face 2 axis, alpha
+    const float* hi = tr + (4 * axis + 2) * PLS + p * PLP + qq;
+    const bool hl = (T.nbm >> (2 * axis)) & 1, hh = (T.nbm >> (2 * axis + 1)) & 1;
+    put_halo<MODE>(smem, axis, p, qq, hl ? lo[0] : 0.f, hh ? hi[0] : 0.f, hl ? lo[PLS] : 0.f, hh ? hi[PLS] : 0.f);
+  }
   __syncthreads();
 
-  int q, j;
-  lane_qj(T.lane, q, j);
-  BFrag<MODE> bm, bl;
-  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
   // x and y stages on the warp's 4 z planes (in place)
+  constexpr bool kBD = false;  // L is never block diagonal
+  HOpFrag blx, bly;
+  ld_op(blx, tab->L[T.kind[0]], T.lane);
+  ld_op(bly, tab->L[T.kind[1]], T.lane);
+#pragma unroll
   for (int zz = 0; zz < 4; ++zz) {
     const int z = 4 * T.warp + zz;
-    load_b<MODE>(bl, &tab->L[T.kind[0]][0][0][0][0], T.lane);
     {
-      AFrag<MODE> a;
-      ld_a<MODE>(a, T.uh, T.ud(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), false);
-      Acc16<MODE> am, as;
+      const unsigned off = T.ox(z);
+      HFrag a;
+      ld_a<MODE>(a, T.UH(), T.UD(), off, false);
+      HAcc<MODE> am, as;
       am.zero();
       as.zero();
-      mma16<MODE>(am, a, bm);
-      mma16<MODE>(as, a, bl);
-      halo16<MODE>(T, as, tab, 0, trp(T, 0, 0) + z * 17, trp(T, 0, 1) + z * 17, trp(T, 1, 0) + z * 17,
-                   trp(T, 1, 1) + z * 17);
+      mma_bd<MODE>(am, a, bm);
+      mma_op<MODE, kBD>(as, a, blx);
+      unsigned w0, w1;
+      T.halo(0, z, w0, w1);
+      mma_halo<MODE>(as, w0, w1, T.hb);
       float va[2][4], vb[2][4];
-      finals<MODE>(am, va);
-      finals<MODE>(as, vb);
+      am.vals(va);
+      as.vals(vb);
+      HFrag fa, fb;
+      to_frag<MODE>(va, fa);
+      to_frag<MODE>(vb, fb);
       __syncwarp();
-      st_acc<MODE>(T.uh, T.ud(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), va, false);
-      st_acc<MODE>(T.bh, T.bd(), hidx(z, j + 8 * (q & 1), 8 * (q >> 1)), vb, false);
+      st_a<MODE>(T.UH(), T.UD(), off, fa, false);
+      st_a<MODE>(T.BH(), T.BD(), off, fb, false);
     }
     __syncwarp();
-    load_b<MODE>(bl, &tab->L[T.kind[1]][0][0][0][0], T.lane);
     {
       // y lines: rows = x, k = y (memory rows along y -> trans)
-      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
-      AFrag<MODE> a, b;
-      ld_a<MODE>(a, T.uh, T.ud(), off, true);
-      ld_a<MODE>(b, T.bh, T.bd(), off, true);
-      Acc16<MODE> c, d, e2;
+      const unsigned off = T.oy(z);
+      HFrag a, b;
+      ld_a<MODE>(a, T.UH(), T.UD(), off, true);
+      ld_a<MODE>(b, T.BH(), T.BD(), off, true);
+      HAcc<MODE> c, d;
       c.zero();
       d.zero();
-      e2.zero();
-      mma16<MODE>(c, a, bm);
-      mma16<MODE>(d, a, bl);
-      halo16<MODE>(T, d, tab, 1, trp(T, 2, 0) + z * 17, trp(T, 2, 1) + z * 17, trp(T, 3, 0) + z * 17,
-                   trp(T, 3, 1) + z * 17);
-      mma16<MODE>(e2, b, bm);
+      mma_bd<MODE>(c, a, bm);
+      mma_op<MODE, kBD>(d, a, bly);
+      unsigned w0, w1;
+      T.halo(1, z, w0, w1);
+      mma_halo<MODE>(d, w0, w1, T.hb);
+      mma_bd<MODE>(d, b, bm);
       float vc[2][4], vd[2][4];
-      finals<MODE>(c, vc);
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) vd[nt][i] = d.val(nt, i) + e2.val(nt, i);
+      c.vals(vc);
+      d.vals(vd);
+      HFrag fc, fd;
+      to_frag<MODE>(vc, fc);
+      to_frag<MODE>(vd, fd);
       __syncwarp();
-      st_acc<MODE>(T.uh, T.ud(), off, vc, true);
-      st_acc<MODE>(T.bh, T.bd(), off, vd, true);
+      st_a<MODE>(T.UH(), T.UD(), off, fc, true);
+      st_a<MODE>(T.BH(), T.BD(), off, fd, true);
     }
     __syncwarp();
   }
   return true;
 }
 
-// z stage for row y: v (16 lines x, 16 outputs z) as f32 values
+// z stage for row y: v (16 lines x, 16 outputs z) as f32 values (scaled units)
 template <int MODE>
-__device__ __forceinline__ void z_lines(const HTile<MODE>& T, const HTables* tab, int y, const BFrag<MODE>& bm,
-                                        const BFrag<MODE>& bl, float (&v)[2][4]) {
-  int q, j;
-  lane_qj(T.lane, q, j);
-  const int off = hidx(j + 8 * (q >> 1), y, 8 * (q & 1));
-  AFrag<MODE> c, d;
-  ld_a<MODE>(c, T.uh, T.ud(), off, true);
-  ld_a<MODE>(d, T.bh, T.bd(), off, true);
-  Acc16<MODE> s, m;
+__device__ __forceinline__ void z_lines(const HTile<MODE>& T, int y, const HOpFrag& bm, const HOpFrag& bl,
+                                        float (&v)[2][4]) {
+  const unsigned off = T.oz(y);
+  HFrag c, d;
+  ld_a<MODE>(c, T.UH(), T.UD(), off, true);
+  ld_a<MODE>(d, T.BH(), T.BD(), off, true);
+  HAcc<MODE> s;
   s.zero();
-  m.zero();
-  mma16<MODE>(s, c, bl);
-  halo16<MODE>(T, s, tab, 2, trp(T, 4, 0) + y * 17, trp(T, 4, 1) + y * 17, trp(T, 5, 0) + y * 17,
-               trp(T, 5, 1) + y * 17);
-  mma16<MODE>(m, d, bm);
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[nt][i] = s.val(nt, i) + m.val(nt, i);
+  mma_dense<MODE>(s, c, bl);
+  unsigned w0, w1;
+  T.halo(2, y, w0, w1);
+  mma_halo<MODE>(s, w0, w1, T.hb);
+  mma_bd<MODE>(s, d, bm);
+  s.vals(v);
 }
 
 // accumulator element (nt, i): line = g + 8*(i>>1), output = 8nt + 2t + (i&1)
@@ -603,57 +596,66 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
   v += (long long)blockIdx.y * g.batch_stride;
   if (!tile_front<MODE, KK>(T, smem, g, op, tab, u)) return;
   __syncthreads();
-  BFrag<MODE> bm, bl;
-  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
-  load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
-  float* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
+  HOpFrag bm, bl;
+  ld_op(bm, tab->M, T.lane);
+  ld_op(bl, tab->L[T.kind[2]], T.lane);
+  float* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
   const float os = pow2f(-(op.sc.aA + T.eu));
+#pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     float o[2][4];
-    z_lines<MODE>(T, tab, y, bm, bl, o);
+    z_lines<MODE>(T, y, bm, bl, o);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
         vb[(long long)z * T.sz + (long long)y * T.sy + x] = o[nt][i] * os;
       }
   }
 }
 
-// smoother colour pass (see sf_dmma.cu k_colour_dmma8 for the stage order)
+// smoother colour pass: residual r = b - A x on the tile, fast-diagonalisation patch solve
+// V (x3) Lambda^-1 V^T (x3) r, x_new = x_old + correction (sf_dmma.cu k_colour_dmma8 stage order)
 template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restrict__ xo, const float* __restrict__ b,
                                                           float* __restrict__ xn, Geom g, LevelOp<KK, MODE> op,
-                                                          const HTables* __restrict__ tab) {
+                                                          const HTables* __restrict__ tab,
+                                                          const DenTab* __restrict__ den) {
   extern __shared__ __align__(128) char smem[];
+  constexpr bool kBDV = KK < 8;  // Q3 / Q1: the line transform is blockdiag of the patches' V
   HTile<MODE> T;
   prefetch_b_rows<KK>(g, b);
   if (!tile_front<MODE, KK>(T, smem, g, op, tab, xo)) return;
   __syncthreads();
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
-  int q, j;
-  lane_qj(T.lane, q, j);
-  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
-  BFrag<MODE> bm, bl, bv;
-  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
-  load_b<MODE>(bl, &tab->L[kz][0][0][0][0], T.lane);
-  load_b<MODE>(bv, &tab->Vf[kz][0][0][0][0], T.lane);
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
+  HOpFrag bm, bl, bv;
+  ld_op(bm, tab->M, T.lane);
+  ld_op(bl, tab->L[kz], T.lane);
+  ld_op(bv, tab->Vf[kz], T.lane);
   // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
   float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    z_lines<MODE>(T, tab, y, bm, bl, rr[yy]);
+    float bvv[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        bvv[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x);
+      }
+    z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        rr[yy][nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x) - rr[yy][nt][i] * os;
+        rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
         mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
       }
     smax(&T.s_exp[1], mx);
@@ -668,96 +670,119 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) rr[yy][nt][i] *= rs;
-    AFrag<MODE> a;
-    acc_to_a<MODE>(rr[yy], a);
-    Acc16<MODE> acc;
+    HFrag a;
+    to_frag<MODE>(rr[yy], a);
+    HAcc<MODE> acc;
     acc.zero();
-    mma16<MODE>(acc, a, bv);
+    mma_op<MODE, kBDV>(acc, a, bv);
     float o[2][4];
-    finals<MODE>(acc, o);
-    st_acc<MODE>(T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), o, true);
+    acc.vals(o);
+    HFrag f;
+    to_frag<MODE>(o, f);
+    st_a<MODE>(T.UH(), T.UD(), T.oz(y), f, true);
   }
   __syncthreads();
   // warp-private z' planes: V_y^T | V_x^T, 1/lambda, V_x | V_y
-  const double* lamx = tab->lam[kx];
-  const double* lamy = tab->lam[ky];
-  const double* lamz = tab->lam[kz];
+  HOpFrag bfy, bfx, bbx, bby;
+  ld_op(bfy, tab->Vf[ky], T.lane);
+  ld_op(bfx, tab->Vf[kx], T.lane);
+  ld_op(bbx, tab->Vb[kx], T.lane);
+  ld_op(bby, tab->Vb[ky], T.lane);
+  const DenTab* dt = den + (kx * 16 + ky * 4 + kz);
+#pragma unroll
   for (int zz = 0; zz < 4; ++zz) {
     const int z = 4 * T.warp + zz;
+    // denominators of this lane's V_x^T outputs (issued early)
+    const float4* dp = reinterpret_cast<const float4*>(&dt->d[z][T.lane][0]);
+    const float4* rp = reinterpret_cast<const float4*>(&dt->r[z][T.lane][0]);
+    const float4 d0 = __ldg(dp), d1 = __ldg(dp + 1), r0 = __ldg(rp), r1 = __ldg(rp + 1);
     {
-      load_b<MODE>(bv, &tab->Vf[ky][0][0][0][0], T.lane);
-      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
-      AFrag<MODE> a;
-      ld_a<MODE>(a, T.uh, T.ud(), off, true);
-      Acc16<MODE> acc;
+      const unsigned off = T.oy(z);
+      HFrag a;
+      ld_a<MODE>(a, T.UH(), T.UD(), off, true);
+      HAcc<MODE> acc;
       acc.zero();
-      mma16<MODE>(acc, a, bv);
+      mma_op<MODE, kBDV>(acc, a, bfy);
       float o[2][4];
-      finals<MODE>(acc, o);
+      acc.vals(o);
+      HFrag f;
+      to_frag<MODE>(o, f);
       __syncwarp();
-      st_acc<MODE>(T.uh, T.ud(), off, o, true);
+      st_a<MODE>(T.UH(), T.UD(), off, f, true);
     }
     __syncwarp();
     {
-      load_b<MODE>(bv, &tab->Vf[kx][0][0][0][0], T.lane);
-      const int off = hidx(z, j + 8 * (q & 1), 8 * (q >> 1));
-      AFrag<MODE> a;
-      ld_a<MODE>(a, T.uh, T.ud(), off, false);
-      Acc16<MODE> acc;
+      const unsigned off = T.ox(z);
+      HFrag a;
+      ld_a<MODE>(a, T.UH(), T.UD(), off, false);
+      HAcc<MODE> acc;
       acc.zero();
-      mma16<MODE>(acc, a, bv);
+      mma_op<MODE, kBDV>(acc, a, bfx);
       float o[2][4];
-      const double lz = 0.0 + __ldg(lamz + z);
+      acc.vals(o);
+      const float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      const float rcp[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int y = T.g + 8 * (i >> 1), x = 8 * nt + 2 * T.t + (i & 1);
-          o[nt][i] = acc.val(nt, i) / (float)(((lz + __ldg(lamy + y)) + __ldg(lamx + x)) * pow2d(-op.sc.aD));
+        for (int i = 0; i < 4; ++i) {  // o / d correctly rounded: q = o r, e = o - q d (exact), q + e r
+          const float qt = o[nt][i] * rcp[4 * nt + i];
+          const float ee = fmaf(-qt, dd[4 * nt + i], o[nt][i]);
+          o[nt][i] = fmaf(ee, rcp[4 * nt + i], qt);
         }
-      acc_to_a<MODE>(o, a);
-      load_b<MODE>(bv, &tab->Vb[kx][0][0][0][0], T.lane);
+      to_frag<MODE>(o, a);
       acc.zero();
-      mma16<MODE>(acc, a, bv);
-      finals<MODE>(acc, o);
+      mma_op<MODE, kBDV>(acc, a, bbx);
+      acc.vals(o);
+      HFrag f;
+      to_frag<MODE>(o, f);
       __syncwarp();
-      st_acc<MODE>(T.uh, T.ud(), off, o, false);
+      st_a<MODE>(T.UH(), T.UD(), off, f, false);
     }
     __syncwarp();
     {
-      load_b<MODE>(bv, &tab->Vb[ky][0][0][0][0], T.lane);
-      const int off = hidx(z, j + 8 * (q >> 1), 8 * (q & 1));
-      AFrag<MODE> a;
-      ld_a<MODE>(a, T.uh, T.ud(), off, true);
-      Acc16<MODE> acc;
+      const unsigned off = T.oy(z);
+      HFrag a;
+      ld_a<MODE>(a, T.UH(), T.UD(), off, true);
+      HAcc<MODE> acc;
       acc.zero();
-      mma16<MODE>(acc, a, bv);
+      mma_op<MODE, kBDV>(acc, a, bby);
       float o[2][4];
-      finals<MODE>(acc, o);
+      acc.vals(o);
+      HFrag f;
+      to_frag<MODE>(o, f);
       __syncwarp();
-      st_acc<MODE>(T.uh, T.ud(), off, o, true);
+      st_a<MODE>(T.UH(), T.UD(), off, f, true);
     }
     __syncwarp();
   }
   __syncthreads();
   // z lines: backward V_z, x_new = x_old + correction (back to true units)
-  load_b<MODE>(bv, &tab->Vb[kz][0][0][0][0], T.lane);
+  ld_op(bv, tab->Vb[kz], T.lane);
   const float cs = pow2f(-(op.sc.aD + 6 * op.sc.aV + er));
+#pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    AFrag<MODE> a;
-    ld_a<MODE>(a, T.uh, T.ud(), hidx(j + 8 * (q >> 1), y, 8 * (q & 1)), true);
-    Acc16<MODE> acc;
+    float xv[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        xv[nt][i] = __ldg(xo + off0 + (long long)z * T.sz + (long long)y * T.sy + x);
+      }
+    HFrag a;
+    ld_a<MODE>(a, T.UH(), T.UD(), T.oz(y), true);
+    HAcc<MODE> acc;
     acc.zero();
-    mma16<MODE>(acc, a, bv);
+    mma_op<MODE, kBDV>(acc, a, bv);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
         if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
-        const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
-        xn[o] = __ldg(xo + o) + acc.val(nt, i) * cs;
+        xn[off0 + (long long)z * T.sz + (long long)y * T.sy + 8 * (i >> 1)] = fmaf(acc.val(nt, i), cs, xv[nt][i]);
       }
   }
 }
@@ -782,23 +807,30 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
   prefetch_b_rows<KK>(g, b);
   if (!tile_front<MODE, KK>(T, smem, g, op, tab, x)) return;
   __syncthreads();
-  BFrag<MODE> bm, bl;
-  load_b<MODE>(bm, &tab->M[0][0][0][0], T.lane);
-  load_b<MODE>(bl, &tab->L[T.kind[2]][0][0][0][0], T.lane);
-  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
+  HOpFrag bm, bl;
+  ld_op(bm, tab->M, T.lane);
+  ld_op(bl, tab->L[T.kind[2]], T.lane);
+  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
   float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    z_lines<MODE>(T, tab, y, bm, bl, rr[yy]);
+    float bvv[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int xx = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
+        bvv[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx);
+      }
+    z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int xx = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        rr[yy][nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx) - rr[yy][nt][i] * os;
+        rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
         mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
       }
     smax(&T.s_exp[1], mx);
@@ -812,7 +844,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
     q0 = __ldg(&pt->PT[1][0][T.lane]);
     q1 = __ldg(&pt->PT[1][1][T.lane]);
   }
-  float* S1 = reinterpret_cast<float*>(T.uh);  // [zc][y][x], plane pitch 260
+  float* S1 = reinterpret_cast<float*>(smem + SM_UH);  // [zc][y][x], plane pitch 260
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
@@ -820,13 +852,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) rr[yy][nt][i] *= rs;
-    AFrag<MODE> a;
-    acc_to_a<MODE>(rr[yy], a);
+    HFrag a;
+    to_frag<MODE>(rr[yy], a);
     float m[4] = {0.f, 0.f, 0.f, 0.f}, c[4] = {0.f, 0.f, 0.f, 0.f};
-    hmma(m, a.h, p0, p1);
+    hmma16(m, a.h[0], a.h[1], a.h[2], a.h[3], p0, p1);
     if constexpr (MODE == MODE_FP16_EC) {
-      hmma(c, a.h, q0, q1);
-      hmma(c, a.d, p0, p1);
+      hmma16(c, a.h[0], a.h[1], a.h[2], a.h[3], q0, q1);
+      hmma16(c, a.d[0], a.d[1], a.d[2], a.d[3], p0, p1);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -835,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
     }
   }
   __syncthreads();
-  float* S2 = reinterpret_cast<float*>(T.bh);  // [zc][yc][x]
+  float* S2 = reinterpret_cast<float*>(smem + SM_BH);  // [zc][yc][x]
   {  // y lines (zc, x): 128 lines, one per thread
     const int xx = threadIdx.x & 15, zc = threadIdx.x >> 4;
     Op<MODE> w[16];
@@ -880,6 +912,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
 }
 
 // ------------------------------------------------------------- host side
+static unsigned short half_bits(float x) {
+  const __half h = __float2half_rn(x);
+  return *reinterpret_cast<const unsigned short*>(&h);
+}
 static void split_host(int mode, double x, unsigned short& h, unsigned short& d) {
   const float x32 = (float)x;
   const __half hh = __float2half_rn(x32);
@@ -889,48 +925,93 @@ static void split_host(int mode, double x, unsigned short& h, unsigned short& d)
   d = mode == MODE_FP16_EC ? *reinterpret_cast<const unsigned short*>(&dd) : 0;
 }
 
-static void pack_op_frags(int mode, const double* Op /* [16][16] */, unsigned* dst /* [2][2][2][32] */) {
-  for (int nt = 0; nt < 2; ++nt)
-    for (int jj = 0; jj < 2; ++jj)
-      for (int ln = 0; ln < 32; ++ln) {
+// B words of Op (16 out x 16 in) for every lane: word nt*2 + j = (Op[8nt+g][2t+8j], Op[..][..+1])
+static void pack_op_frags(int mode, const double* Op /* [16][16] */, HOp& dst) {
+  for (int ln = 0; ln < 32; ++ln) {
+    unsigned wh[4], wd[4];
+    for (int nt = 0; nt < 2; ++nt)
+      for (int jj = 0; jj < 2; ++jj) {
         const int n = 8 * nt + (ln >> 2), k0 = 2 * (ln & 3) + 8 * jj;
         unsigned short h0, d0, h1, d1;
         split_host(mode, Op[n * 16 + k0], h0, d0);
         split_host(mode, Op[n * 16 + k0 + 1], h1, d1);
-        dst[(0 * 4 + nt * 2 + jj) * 32 + ln] = (unsigned)h0 | ((unsigned)h1 << 16);
-        dst[(1 * 4 + nt * 2 + jj) * 32 + ln] = (unsigned)d0 | ((unsigned)d1 << 16);
+        wh[nt * 2 + jj] = (unsigned)h0 | ((unsigned)h1 << 16);
+        wd[nt * 2 + jj] = (unsigned)d0 | ((unsigned)d1 << 16);
       }
+    dst.w[ln][0] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+    dst.w[ln][1] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  }
 }
 
-static HTables build_tables(int mode, int KK, const double* opd, const double* eigd) {
-  HTables t;
+// halo B words (see mma_halo / put_halo): k rows 0: alpha_lo coupling urow (outputs < KK),
+// 1: alpha_hi coupling ucol (outputs >= 16 - KK), 2: beta_lo -> output 0, 3: beta_hi -> output 15;
+// EC corr rows 4..7 carry the main halves against the data's residual halves; fp16 rows 6, 7
+// add beta's residual half / 2048.
+static void pack_halo(int mode, int KK, const double* ucol, const double* urow, uint4* dst /* [32] */) {
+  for (int ln = 0; ln < 32; ++ln) {
+    const int gg = ln >> 2, tt = ln & 3;
+    unsigned w[4];
+    for (int nt = 0; nt < 2; ++nt) {
+      const int n = 8 * nt + gg;
+      unsigned short ch[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};  // coupling (h, d) of rows 0..3 at n
+      if (n < KK) split_host(mode, urow[n], ch[0], cd[0]);
+      if (n >= 16 - KK) split_host(mode, ucol[n - (16 - KK)], ch[1], cd[1]);
+      if (n == 0) ch[2] = half_bits(1.0f);
+      if (n == 15) ch[3] = half_bits(1.0f);
+      unsigned short mrow[8] = {ch[0], ch[1], ch[2], ch[3], 0, 0, 0, 0};
+      unsigned short crow[8] = {cd[0], cd[1], 0, 0, ch[0], ch[1], ch[2], ch[3]};
+      if (mode != MODE_FP16_EC) {
+        mrow[6] = n == 0 ? half_bits(1.0f / kEc) : 0;
+        mrow[7] = n == 15 ? half_bits(1.0f / kEc) : 0;
+      }
+      w[nt] = (unsigned)mrow[2 * tt] | ((unsigned)mrow[2 * tt + 1] << 16);
+      w[2 + nt] = (unsigned)crow[2 * tt] | ((unsigned)crow[2 * tt + 1] << 16);
+    }
+    dst[ln] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+static void build_tables(int mode, int KK, const double* opd, const double* eigd, HTables& t) {
   std::memset(&t, 0, sizeof(t));
   double Mp[256], L[4][256], V[4][256], lam[4][16];
   build_line_ops_host(KK, opd, eigd, Mp, &L[0][0], eigd ? &V[0][0] : nullptr, &lam[0][0]);
-  pack_op_frags(mode, Mp, &t.M[0][0][0][0]);
-  for (int q = 0; q < 4; ++q) pack_op_frags(mode, L[q], &t.L[q][0][0][0][0]);
+  pack_op_frags(mode, Mp, t.M);
+  for (int q = 0; q < 4; ++q) pack_op_frags(mode, L[q], t.L[q]);
   if (eigd) {
     for (int q = 0; q < 4; ++q) {
       double VT[256];
       for (int i = 0; i < 16; ++i)
         for (int jj = 0; jj < 16; ++jj) VT[i * 16 + jj] = V[q][jj * 16 + i];
-      pack_op_frags(mode, VT, &t.Vf[q][0][0][0][0]);
-      pack_op_frags(mode, V[q], &t.Vb[q][0][0][0][0]);
+      pack_op_frags(mode, VT, t.Vf[q]);
+      pack_op_frags(mode, V[q], t.Vb[q]);
       for (int i = 0; i < 16; ++i) t.lam[q][i] = lam[q][i];
     }
   }
   const double* ucol = opd + 2 * KK * KK;
   const double* urow = ucol + KK;
-  for (int i = 0; i < KK; ++i) {
-    unsigned short h, d;
-    split_host(mode, ucol[i], h, d);
-    t.ucol[0][i] = __half2float(*reinterpret_cast<__half*>(&h));
-    t.ucol[1][i] = __half2float(*reinterpret_cast<__half*>(&d));
-    split_host(mode, urow[i], h, d);
-    t.urow[0][i] = __half2float(*reinterpret_cast<__half*>(&h));
-    t.urow[1][i] = __half2float(*reinterpret_cast<__half*>(&d));
-  }
-  return t;
+  pack_halo(mode, KK, ucol, urow, t.halo);
+}
+
+// denominators f32((lam_z + lam_y + lam_x) 2^-aD) (the reference sums in fp64 and casts,
+// multigrid.py:60-69,80) and their correctly rounded f32 reciprocals, per kind combination
+static void build_den(const HTables& t, int aD, std::vector<DenTab>& out) {
+  out.resize(64);
+  const double sc = std::ldexp(1.0, -aD);
+  for (int kx = 0; kx < 4; ++kx)
+    for (int ky = 0; ky < 4; ++ky)
+      for (int kz = 0; kz < 4; ++kz) {
+        DenTab& D = out[kx * 16 + ky * 4 + kz];
+        for (int z = 0; z < 16; ++z)
+          for (int ln = 0; ln < 32; ++ln)
+            for (int nt = 0; nt < 2; ++nt)
+              for (int i = 0; i < 4; ++i) {
+                const int y = (ln >> 2) + 8 * (i >> 1), x = 8 * nt + 2 * (ln & 3) + (i & 1);
+                const float d = (float)(((t.lam[kz][z] + t.lam[ky][y]) + t.lam[kx][x]) * sc);
+                volatile float one = 1.0f;
+                D.d[z][ln][nt * 4 + i] = d;
+                D.r[z][ln][nt * 4 + i] = one / d;  // IEEE single division: RN(1/d)
+              }
+      }
 }
 
 static std::mutex g_mu;
@@ -938,10 +1019,12 @@ struct Entry {
   int dev, mode;
   std::vector<double> key;
   void* ptr;
+  void* den;
 };
 static std::vector<Entry> g_cache;
 
-static const HTables* tables(int mode, const double* opd, const double* eigd, int KK = K) {
+static const HTables* tables(int mode, const double* opd, const double* eigd, int KK = K,
+                             const DenTab** den = nullptr) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int nop = 2 * KK * KK + 4 * KK, neig = 4 * 4 * KK * KK + 4 * 2 * KK;
@@ -951,14 +1034,27 @@ static const HTables* tables(int mode, const double* opd, const double* eigd, in
   key.push_back((double)KK);
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& e : g_cache)
-    if (e.dev == dev && e.mode == mode && e.key == key) return reinterpret_cast<const HTables*>(e.ptr);
+    if (e.dev == dev && e.mode == mode && e.key == key) {
+      if (den) *den = reinterpret_cast<const DenTab*>(e.den);
+      return reinterpret_cast<const HTables*>(e.ptr);
+    }
   double op_s[2 * K * K + 4 * K], eig_s[4 * 256 + 4 * 16];
-  level_scales(KK, opd, eigd, op_s, eigd ? eig_s : nullptr);
-  HTables host = build_tables(mode, KK, op_s, eigd ? eig_s : nullptr);
+  const Scales sc = level_scales(KK, opd, eigd, op_s, eigd ? eig_s : nullptr);
+  std::vector<HTables> host(1);
+  build_tables(mode, KK, op_s, eigd ? eig_s : nullptr, host[0]);
   void* d = nullptr;
+  void* dd = nullptr;
   if (cudaMalloc(&d, sizeof(HTables)) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, &host, sizeof(HTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  g_cache.push_back({dev, mode, std::move(key), d});
+  if (cudaMemcpy(d, host.data(), sizeof(HTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  if (eigd) {
+    std::vector<DenTab> dens;
+    build_den(host[0], sc.aD, dens);
+    if (cudaMalloc(&dd, sizeof(DenTab) * dens.size()) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(dd, dens.data(), sizeof(DenTab) * dens.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return nullptr;
+  }
+  g_cache.push_back({dev, mode, std::move(key), d, dd});
+  if (den) *den = reinterpret_cast<const DenTab*>(dd);
   return reinterpret_cast<const HTables*>(d);
 }
 
@@ -983,78 +1079,54 @@ static LevelOp<KK, MODE> pack_op_h(const double* opd_raw, const double* eig_raw)
   return op;
 }
 
-template <int MODE>
-static int vmult(const Geom& g, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
-  const HTables* tab = tables(MODE, opd, nullptr);
-  if (!tab) return -3;
-  auto op = pack_op_h<MODE>(opd, nullptr);
-  if (cudaFuncSetAttribute(k_vmult_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
-      cudaSuccess)
-    return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_vmult_h8<MODE><<<dim3(tiles, batch), kThreads, smem_bytes<MODE>(), st>>>((const float*)u, (float*)v, g, op, tab);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+template <typename F>
+static bool smem_attr(F* fn) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) == cudaSuccess;
 }
 
-template <int MODE>
-static int colour(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
-                  cudaStream_t st) {
-  const HTables* tab = tables(MODE, opd, eigd);
-  if (!tab) return -3;
-  auto op = pack_op_h<MODE>(opd, eigd);
-  if (cudaFuncSetAttribute(k_colour_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<MODE>()) !=
-      cudaSuccess)
-    return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_colour_h8<MODE><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)xo, (const float*)b, (float*)xn, g, op,
-                                                                 tab);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
-}
-
-
-// Q3 / Q1 (KK = 4, 2): the 16-point tile-line kernels; kUseGeneric when the grid does not tile
+// Q7 (KK = 8) and the 16-point line tiles (KK = 4, 2; kUseGeneric when the grid does not tile)
 template <int MODE, int KK>
-static int vmult_line(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
+static int vmult_t(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   constexpr int CPL = 16 / KK;
-  const int zc = 2 * g0.ntz;  // the caller's z range in cells
-  if (g0.nx % CPL || g0.ny % CPL || zc % CPL) return kUseGeneric;
   Geom g = g0;
-  g.ntx = g.nx / CPL;
-  g.nty = g.ny / CPL;
-  g.ntz = zc / CPL;
+  if (KK < 8) {
+    const int zc = 2 * g0.ntz;  // the caller's z range in cells
+    if (g0.nx % CPL || g0.ny % CPL || zc % CPL) return kUseGeneric;
+    g.ntx = g.nx / CPL;
+    g.nty = g.ny / CPL;
+    g.ntz = zc / CPL;
+  }
   const HTables* tab = tables(MODE, opd, nullptr, KK);
   if (!tab) return -3;
   auto op = pack_op_h<MODE, KK>(opd, nullptr);
-  if (cudaFuncSetAttribute(k_vmult_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_bytes<MODE>()) != cudaSuccess)
-    return -3;
+  if (!smem_attr(k_vmult_h8<MODE, KK>)) return -3;
   const int tiles = g.ntx * g.nty * g.ntz;
-  k_vmult_h8<MODE, KK><<<dim3(tiles, batch), kThreads, smem_bytes<MODE>(), st>>>((const float*)u, (float*)v, g, op,
-                                                                                 tab);
+  k_vmult_h8<MODE, KK><<<dim3(tiles, batch), kThreads, kSmem, st>>>((const float*)u, (float*)v, g, op, tab);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
 template <int MODE, int KK>
-static int colour_line(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
-                       cudaStream_t st) {
+static int colour_t(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
+                    cudaStream_t st) {
   constexpr int CPL = 16 / KK;
-  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
-  const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
-  for (int a = 0; a < 3; ++a)
-    if (s3[a] && n3[a] < CPL + 2) return kUseGeneric;
   Geom g = g0;
-  g.ntx = g.nx / CPL;
-  g.nty = g.ny / CPL;
-  g.ntz = g.nz / CPL;
-  const HTables* tab = tables(MODE, opd, eigd, KK);
-  if (!tab) return -3;
+  if (KK < 8) {
+    if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
+    const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
+    for (int a = 0; a < 3; ++a)
+      if (s3[a] && n3[a] < CPL + 2) return kUseGeneric;
+    g.ntx = g.nx / CPL;
+    g.nty = g.ny / CPL;
+    g.ntz = g.nz / CPL;
+  }
+  const DenTab* den = nullptr;
+  const HTables* tab = tables(MODE, opd, eigd, KK, &den);
+  if (!tab || !den) return -3;
   auto op = pack_op_h<MODE, KK>(opd, eigd);
-  if (cudaFuncSetAttribute(k_colour_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_bytes<MODE>()) != cudaSuccess)
-    return -3;
+  if (!smem_attr(k_colour_h8<MODE, KK>)) return -3;
   const int tiles = g.ntx * g.nty * g.ntz;
-  k_colour_h8<MODE, KK><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)xo, (const float*)b, (float*)xn, g,
-                                                                     op, tab);
+  k_colour_h8<MODE, KK><<<tiles, kThreads, kSmem, st>>>((const float*)xo, (const float*)b, (float*)xn, g, op, tab,
+                                                         den);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -1099,41 +1171,25 @@ static const HPTab* ptables(int mode, const double* embd_raw, int KK = K) {
   return reinterpret_cast<const HPTab*>(d);
 }
 
-template <int MODE>
-static int resid_restrict(const Geom& g, const double* opd, const double* embd, const void* x, const void* b,
-                          void* coarse, cudaStream_t st) {
-  const HTables* tab = tables(MODE, opd, nullptr);
-  const HPTab* pt = ptables(MODE, embd);
-  if (!tab || !pt) return -3;
-  auto op = pack_op_h<MODE>(opd, nullptr);
-  if (cudaFuncSetAttribute(k_resid_restrict_h8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_bytes<MODE>()) != cudaSuccess)
-    return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_resid_restrict_h8<MODE><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)x, (const float*)b,
-                                                                         (float*)coarse, g, op, tab, pt);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
-}
-
 template <int MODE, int KK>
-static int resid_restrict_line(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
-                               void* coarse, cudaStream_t st) {
+static int resid_restrict_t(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
+                            void* coarse, cudaStream_t st) {
   constexpr int CPL = 16 / KK;
-  if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
   Geom g = g0;
-  g.ntx = g.nx / CPL;
-  g.nty = g.ny / CPL;
-  g.ntz = g.nz / CPL;
+  if (KK < 8) {
+    if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
+    g.ntx = g.nx / CPL;
+    g.nty = g.ny / CPL;
+    g.ntz = g.nz / CPL;
+  }
   const HTables* tab = tables(MODE, opd, nullptr, KK);
   const HPTab* pt = ptables(MODE, embd, KK);
   if (!tab || !pt) return -3;
   auto op = pack_op_h<MODE, KK>(opd, nullptr);
-  if (cudaFuncSetAttribute(k_resid_restrict_h8<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_bytes<MODE>()) != cudaSuccess)
-    return -3;
+  if (!smem_attr(k_resid_restrict_h8<MODE, KK>)) return -3;
   const int tiles = g.ntx * g.nty * g.ntz;
-  k_resid_restrict_h8<MODE, KK><<<tiles, kThreads, smem_bytes<MODE>(), st>>>((const float*)x, (const float*)b,
-                                                                             (float*)coarse, g, op, tab, pt);
+  k_resid_restrict_h8<MODE, KK><<<tiles, kThreads, kSmem, st>>>((const float*)x, (const float*)b, (float*)coarse, g,
+                                                                op, tab, pt);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -1142,49 +1198,49 @@ static int resid_restrict_line(const Geom& g0, const double* opd, const double* 
 int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
                            cudaStream_t st) {
   const bool ec = mode == MODE_FP16_EC;
-  if (k_nodes == 4) return ec ? hm::vmult_line<MODE_FP16_EC, 4>(g, opd, u, v, batch, st)
-                              : hm::vmult_line<MODE_FP16, 4>(g, opd, u, v, batch, st);
-  if (k_nodes == 2) return ec ? hm::vmult_line<MODE_FP16_EC, 2>(g, opd, u, v, batch, st)
-                              : hm::vmult_line<MODE_FP16, 2>(g, opd, u, v, batch, st);
+  if (k_nodes == 4) return ec ? hm::vmult_t<MODE_FP16_EC, 4>(g, opd, u, v, batch, st)
+                              : hm::vmult_t<MODE_FP16, 4>(g, opd, u, v, batch, st);
+  if (k_nodes == 2) return ec ? hm::vmult_t<MODE_FP16_EC, 2>(g, opd, u, v, batch, st)
+                              : hm::vmult_t<MODE_FP16, 2>(g, opd, u, v, batch, st);
   return kUseGeneric;
 }
 
 int launch_colour_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const double* eigd,
                             const void* xo, const void* b, void* xn, cudaStream_t st) {
   const bool ec = mode == MODE_FP16_EC;
-  if (k_nodes == 4) return ec ? hm::colour_line<MODE_FP16_EC, 4>(g, opd, eigd, xo, b, xn, st)
-                              : hm::colour_line<MODE_FP16, 4>(g, opd, eigd, xo, b, xn, st);
-  if (k_nodes == 2) return ec ? hm::colour_line<MODE_FP16_EC, 2>(g, opd, eigd, xo, b, xn, st)
-                              : hm::colour_line<MODE_FP16, 2>(g, opd, eigd, xo, b, xn, st);
+  if (k_nodes == 4) return ec ? hm::colour_t<MODE_FP16_EC, 4>(g, opd, eigd, xo, b, xn, st)
+                              : hm::colour_t<MODE_FP16, 4>(g, opd, eigd, xo, b, xn, st);
+  if (k_nodes == 2) return ec ? hm::colour_t<MODE_FP16_EC, 2>(g, opd, eigd, xo, b, xn, st)
+                              : hm::colour_t<MODE_FP16, 2>(g, opd, eigd, xo, b, xn, st);
   return kUseGeneric;
 }
 
 int launch_vmult_hmma8(int mode, const Geom& g, const double* opd, const void* u, void* v, int batch,
                        cudaStream_t st) {
-  return mode == MODE_FP16 ? hm::vmult<MODE_FP16>(g, opd, u, v, batch, st)
-                           : hm::vmult<MODE_FP16_EC>(g, opd, u, v, batch, st);
+  return mode == MODE_FP16 ? hm::vmult_t<MODE_FP16, 8>(g, opd, u, v, batch, st)
+                           : hm::vmult_t<MODE_FP16_EC, 8>(g, opd, u, v, batch, st);
 }
 
 int launch_colour_hmma8(int mode, const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b,
                         void* xn, cudaStream_t st) {
-  return mode == MODE_FP16 ? hm::colour<MODE_FP16>(g, opd, eigd, xo, b, xn, st)
-                           : hm::colour<MODE_FP16_EC>(g, opd, eigd, xo, b, xn, st);
+  return mode == MODE_FP16 ? hm::colour_t<MODE_FP16, 8>(g, opd, eigd, xo, b, xn, st)
+                           : hm::colour_t<MODE_FP16_EC, 8>(g, opd, eigd, xo, b, xn, st);
 }
 
 int launch_resid_restrict_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const double* embd,
                                     const void* x, const void* b, void* coarse, cudaStream_t st) {
   const bool ec = mode == MODE_FP16_EC;
-  if (k_nodes == 4) return ec ? hm::resid_restrict_line<MODE_FP16_EC, 4>(g, opd, embd, x, b, coarse, st)
-                              : hm::resid_restrict_line<MODE_FP16, 4>(g, opd, embd, x, b, coarse, st);
-  if (k_nodes == 2) return ec ? hm::resid_restrict_line<MODE_FP16_EC, 2>(g, opd, embd, x, b, coarse, st)
-                              : hm::resid_restrict_line<MODE_FP16, 2>(g, opd, embd, x, b, coarse, st);
+  if (k_nodes == 4) return ec ? hm::resid_restrict_t<MODE_FP16_EC, 4>(g, opd, embd, x, b, coarse, st)
+                              : hm::resid_restrict_t<MODE_FP16, 4>(g, opd, embd, x, b, coarse, st);
+  if (k_nodes == 2) return ec ? hm::resid_restrict_t<MODE_FP16_EC, 2>(g, opd, embd, x, b, coarse, st)
+                              : hm::resid_restrict_t<MODE_FP16, 2>(g, opd, embd, x, b, coarse, st);
   return kUseGeneric;
 }
 
 int launch_resid_restrict_hmma8(int mode, const Geom& g, const double* opd, const double* embd, const void* x,
                                 const void* b, void* coarse, cudaStream_t st) {
-  return mode == MODE_FP16 ? hm::resid_restrict<MODE_FP16>(g, opd, embd, x, b, coarse, st)
-                           : hm::resid_restrict<MODE_FP16_EC>(g, opd, embd, x, b, coarse, st);
+  return mode == MODE_FP16 ? hm::resid_restrict_t<MODE_FP16, 8>(g, opd, embd, x, b, coarse, st)
+                           : hm::resid_restrict_t<MODE_FP16_EC, 8>(g, opd, embd, x, b, coarse, st);
 }
 
 }  // namespace sf
