@@ -38,8 +38,8 @@
 #include <vector>
 
 #include "sf_common.cuh"
+#include "sf_dmma.cuh"
 #include "sf_internal.h"
-#include "sf_tile.cuh"
 
 namespace sf {
 namespace hm {
@@ -52,14 +52,17 @@ constexpr float kEc = 2048.0f;
 constexpr float kInvEc = 1.0f / 2048.0f;
 
 // shared memory map (bytes): U_h | U_d | B_h | B_d | halo words | exponent words.
-// During the prologue the B region holds the f32 face-trace planes (and, for EC, the
-// staged x-neighbour cell layers).
+// During the prologue the B region + halo words hold the f32 face-trace planes and the staged
+// x-neighbour cell layers (consumed before the halo words are written).
 constexpr int SM_UH = 0, SM_UD = 2 * TVOL, SM_BH = 4 * TVOL, SM_BD = 6 * TVOL;
 constexpr int SM_HALO = 8 * TVOL;                 // [axis][p 16][q 16] x 16 B
-constexpr int SM_EXP = SM_HALO + 3 * 256 * 16;
-constexpr int kSmem = SM_EXP + 16;
 constexpr int PLP = 17;                           // f32 trace plane pitch
 constexpr int PLS = 16 * PLP;                     // floats per trace plane
+constexpr int SM_TR = SM_BH;                      // 12 planes: (face * 2 + alpha/beta) * PLS
+constexpr int SM_XST = SM_TR + 12 * PLS * 4;      // [hi][256 rows][KK <= 8] f32
+constexpr int SM_EXP_A = SM_HALO + 3 * 256 * 16, SM_EXP_B = SM_XST + 2 * 256 * 8 * 4;
+constexpr int SM_EXP = SM_EXP_A > SM_EXP_B ? SM_EXP_A : SM_EXP_B;
+constexpr int kSmem = SM_EXP + 16;
 
 __device__ __forceinline__ int hidx(int z, int y, int x) {
   return z * PZ + y * 16 + ((((x >> 3) ^ (y >> 2)) & 1) << 3) + (x & 7);
@@ -189,7 +192,8 @@ __device__ __forceinline__ void mma_op(HAcc<MODE>& acc, const HFrag& a, const HO
 }
 
 // rank-2 face coupling of a stiffness accumulator: k8 A = the lines' halo words
-// (t = 0: alpha_h lo|hi, 1: beta_h, 2: alpha_d, 3: beta_d), B = hb (main nt0, nt1, corr nt0, nt1)
+// (t = 0: alpha_h|beta_h of the lo face, 1: of the hi face, 2, 3: the residual halves), B = hb (main nt0, nt1,
+// corr nt0, nt1)
 template <int MODE>
 __device__ __forceinline__ void mma_halo(HAcc<MODE>& acc, unsigned w0, unsigned w1, const unsigned (&hb)[4]) {
   hmma8(acc.m[0], w0, w1, hb[0]);
@@ -244,7 +248,7 @@ struct HTile {
   int* s_exp;   // block-exponent words ([0] input, [1] residual)
   int eu;       // input block exponent: u^ = 2^eu u
   int cx, cy, cz;
-  long long sy, sz;
+  int sy, sz;   // element strides of y and z (tile-local offsets stay below 16 sz < 2^31)
   unsigned nbm;
   int kind[3];
   int lane, warp, g, t, q, j;
@@ -267,6 +271,8 @@ struct HTile {
     w0 = hw[g * 4];
     w1 = hw[(g + 8) * 4];
   }
+  // tile-local element offset of this lane's z-stage output (nt, i) at row y: x = g + 8(i>>1), z = 8nt + 2t + (i&1)
+  __device__ __forceinline__ int zoff(int nt, int i1, int y) const { return (8 * nt + 2 * t + i1) * sz + y * sy + g; }
 };
 
 template <int MODE>
@@ -290,90 +296,120 @@ __device__ __forceinline__ void st_a(unsigned h, unsigned d, unsigned off, const
   }
 }
 
-// split f32 alpha / beta trace values into one 16-byte halo word (see mma_halo)
+// Halo words: 16 bytes per line (axis, p, q) = packed halves
+//   [alpha_h lo, beta_h lo | alpha_h hi, beta_h hi | alpha_d lo, beta_d lo | alpha_d hi, beta_d hi]
+// (k rows of the halo MMA; see pack_halo).  A face writes its two 32-bit words (lo: 0, 2; hi: 1, 3).
+// fp16: alpha is a demoted operand (no residual half); beta keeps its residual half.
 template <int MODE>
-__device__ __forceinline__ void put_halo(char* sm, int axis, int p, int q, float al, float ah, float bl, float bh) {
-  unsigned ah2, ad2, bh2, bd2;
-  demote_pair<MODE_FP16_EC>(al, ah, ah2, ad2);
-  demote_pair<MODE_FP16_EC>(bl, bh, bh2, bd2);
-  if constexpr (MODE != MODE_FP16_EC) ad2 = 0;  // fp16: alpha is a demoted operand; beta keeps its residual
-  *reinterpret_cast<uint4*>(sm + SM_HALO + ((axis * 16 + p) * 16 + q) * 16) = make_uint4(ah2, bh2, ad2, bd2);
+__device__ __forceinline__ void put_face(char* sm, int axis, int p, int q, int hi, float alpha, float beta) {
+  unsigned h, d;
+  demote_pair<MODE_FP16_EC>(alpha, beta, h, d);
+  if constexpr (MODE != MODE_FP16_EC) d &= 0xffff0000u;
+  unsigned* w = reinterpret_cast<unsigned*>(sm + SM_HALO + ((axis * 16 + p) * 16 + q) * 16);
+  w[hi] = h;
+  w[2 + hi] = d;
 }
 
-// Tangential mass of a y-face (Mx along q) or z-face (My along p) trace plane on the tensor cores:
-// plane = 16 x 16 f32 (pitch 17), A fragment gathered from f32 shared memory with demotion, in place.
+// Tangential mass of one face's (alpha, beta) trace planes on the tensor cores (16 x 16 f32 planes,
+// pitch 17, A fragments gathered from shared memory with demotion).  along_p = false: mass along q
+// (row = p, k = q); true: along p (row = q, k = p).  to_halo: write the face's halo words, else the
+// f32 planes in place.
 template <int MODE>
-__device__ __forceinline__ void plane_mass(float* P, bool along_p, const HOpFrag& bm, int g, int t) {
-  float v[2][4];
-  // A[row][k]: along q: row = p, k = q;  along p: row = q, k = p
-  auto at = [&](int row, int k) -> float { return along_p ? P[k * PLP + row] : P[row * PLP + k]; };
+__device__ __forceinline__ void face_mass(const HTile<MODE>& T, float* pa, bool along_p, bool to_halo, int axis,
+                                          int hi, const HOpFrag& bm) {
+  float o[2][2][4];  // [alpha / beta][nt][i]
 #pragma unroll
-  for (int kb = 0; kb < 2; ++kb) {
-    v[kb][0] = at(g, 8 * kb + 2 * t);
-    v[kb][1] = at(g, 8 * kb + 2 * t + 1);
-    v[kb][2] = at(g + 8, 8 * kb + 2 * t);
-    v[kb][3] = at(g + 8, 8 * kb + 2 * t + 1);
+  for (int ab = 0; ab < 2; ++ab) {
+    const float* P = pa + ab * PLS;
+    auto at = [&](int row, int k) -> float { return along_p ? P[k * PLP + row] : P[row * PLP + k]; };
+    float v[2][4];
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+      v[kb][0] = at(T.g, 8 * kb + 2 * T.t);
+      v[kb][1] = at(T.g, 8 * kb + 2 * T.t + 1);
+      v[kb][2] = at(T.g + 8, 8 * kb + 2 * T.t);
+      v[kb][3] = at(T.g + 8, 8 * kb + 2 * T.t + 1);
+    }
+    HFrag a;
+    to_frag<MODE>(v, a);  // same register order as an accumulator fragment
+    HAcc<MODE> acc;
+    acc.zero();
+    mma_bd<MODE>(acc, a, bm);
+    acc.vals(o[ab]);
   }
-  HFrag a;
-  to_frag<MODE>(v, a);  // same register order as an accumulator fragment
-  HAcc<MODE> acc;
-  acc.zero();
-  mma_bd<MODE>(acc, a, bm);
   __syncwarp();
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int row = g + 8 * (i >> 1), n = 8 * nt + 2 * t + (i & 1);
-      if (along_p) P[n * PLP + row] = acc.val(nt, i); else P[row * PLP + n] = acc.val(nt, i);
+      const int row = T.g + 8 * (i >> 1), n = 8 * nt + 2 * T.t + (i & 1);
+      const int p = along_p ? n : row, qq = along_p ? row : n;
+      if (to_halo) {
+        put_face<MODE>(T.sm, axis, p, qq, hi, o[0][nt][i], o[1][nt][i]);
+      } else {
+        pa[p * PLP + qq] = o[0][nt][i];
+        pa[PLS + p * PLP + qq] = o[1][nt][i];
+      }
     }
 }
 
-// L2 prefetch of this tile's rows of b (read in the z stage of the colour / restriction kernels)
-template <int KK = K>
-__device__ __forceinline__ void prefetch_b_rows(const Geom& g, const float* __restrict__ b) {
-  if ((int)blockIdx.x >= g.ntx * g.nty * g.ntz) return;
-  constexpr int CPL = 16 / KK;
-  int tx, ty, tz;
-  tile_coords<8>(g, blockIdx.x, tx, ty, tz);
-  const long long sy = (long long)g.nx * KK, sz = sy * (long long)g.ny * KK;
-  int cx = g.tx0 + CPL * tx, cy = g.ty0 + CPL * ty, cz = g.tz0 + CPL * tz;
-  if (CPL > 2) {
-    if (g.tx0 & 1) cx = min(cx, g.nx - CPL - g.tx0);
-    if (g.ty0 & 1) cy = min(cy, g.ny - CPL - g.ty0);
-    if (g.tz0 & 1) cz = min(cz, g.nz - CPL - g.tz0);
+// face traces of a neighbour line of KK values w (nearest node last for lo, first for hi):
+// alpha = nearest value, beta = U-row dot product (krylov-free part of the rank-2 coupling).
+// EC: beta in fp32 from the exact coefficients (main + residual / 2048 reconstruct the fp32
+// values to 2^-22, so this is the EC product or better); fp16: demoted products, fp32 sum.
+template <int MODE, int KK>
+__device__ __forceinline__ void line_trace(const float (&w)[KK], const float (&cf)[KK], int hi, float us,
+                                           float& alpha, float& beta) {
+  float s = 0.f;
+  if constexpr (MODE == MODE_FP16_EC) {
+#pragma unroll
+    for (int c = 0; c < KK; ++c)
+      if (hi ? c > 0 : c < KK - 1) s = fmaf(cf[c], w[c], s);
+    beta = s * us;
+  } else {
+#pragma unroll
+    for (int c = 0; c < KK; ++c)
+      if (hi ? c > 0 : c < KK - 1) s = fmaf(cf[c], demote16(w[c] * us), s);
+    beta = s;
   }
-  for (int r = threadIdx.x; r < 256; r += kThreads) {
-    const float* p = b + (long long)(cz * KK + (r >> 4)) * sz + (long long)(cy * KK + (r & 15)) * sy + cx * KK;
-    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-  }
+  alpha = (hi ? w[0] : w[KK - 1]) * us;
 }
 
 // prologue + x/y stages; leaves c in U and dd in B (f16 tensors), halo words ready.
 // KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells).
+// Tile order: the banded 3-D grid of the FP64 kernels (dm::band_tile, no integer divisions).
 template <int MODE, int KK = K>
-__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const LevelOp<KK, MODE>& op,
-                                           const HTables* tab, const float* __restrict__ u) {
+__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const dm::Band& bd,
+                                           const LevelOp<KK, MODE>& op, const HTables* tab, const float*& u,
+                                           int& batch, const float* __restrict__ pf = nullptr) {
+  constexpr int CPL = 16 / KK;
+  int tx, ty, tz;
+  if (!dm::band_tile(g, bd, tx, ty, tz, batch)) return false;
+  u += (long long)batch * g.batch_stride;
   T.sm = smem;
   T.s0 = smem_u32(smem);
   T.s_exp = reinterpret_cast<int*>(smem + SM_EXP);
-  float* tr = reinterpret_cast<float*>(smem + SM_BH);  // f32 trace planes [face][alpha/beta][16][17]
-  constexpr int CPL = 16 / KK;
-  TileEngine<KK, MODE, 1, 16> e(smem, g);
-  e.tr = tr;
-  e.s_exp = T.s_exp;
-  int cx, cy, cz;
-  if (!e.tile_cells(g, 0, cx, cy, cz)) return false;
-  if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
-  T.cx = cx; T.cy = cy; T.cz = cz;
-  T.skip[0] = e.skip[0]; T.skip[1] = e.skip[1]; T.skip[2] = e.skip[2];
-  T.sy = e.sy; T.sz = e.sz;
+  T.cx = g.tx0 + CPL * tx;
+  T.cy = g.ty0 + CPL * ty;
+  T.cz = g.tz0 + CPL * tz;
+  T.skip[0] = T.skip[1] = T.skip[2] = 0;
+  if constexpr (KK < 8) {  // shifted colour (odd offset): the last line ends at cell n-2 (overlaps its neighbour)
+    const int ux = T.cx, uy = T.cy, uz = T.cz;
+    if (g.tx0 & 1) T.cx = min(T.cx, g.nx - CPL - g.tx0);
+    if (g.ty0 & 1) T.cy = min(T.cy, g.ny - CPL - g.ty0);
+    if (g.tz0 & 1) T.cz = min(T.cz, g.nz - CPL - g.tz0);
+    T.skip[0] = (ux - T.cx) * KK;
+    T.skip[1] = (uy - T.cy) * KK;
+    T.skip[2] = (uz - T.cz) * KK;
+  }
+  T.sy = g.nx * KK;
+  T.sz = T.sy * g.ny * KK;
+  const int c0[3] = {T.cx, T.cy, T.cz};
   T.nbm = 0;
-  const int c0[3] = {cx, cy, cz};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (e.face_src(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
-    if (e.face_src(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
+    if (dm::face_src<KK>(g, a, 0, c0[a]) != 2) T.nbm |= 1u << (2 * a);
+    if (dm::face_src<KK>(g, a, 1, c0[a]) != 2) T.nbm |= 1u << (2 * a + 1);
     const int n = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);  // kind of the 16-point line
     T.kind[a] = 2 * ((c0[a] == 0 && g.bnd_lo[a]) ? 1 : 0) + ((c0[a] + CPL == n && g.bnd_hi[a]) ? 1 : 0);
   }
@@ -387,35 +423,44 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     const uint4 w = __ldg(&tab->halo[T.lane]);
     T.hb[0] = w.x; T.hb[1] = w.y; T.hb[2] = w.z; T.hb[3] = w.w;
   }
-  __syncthreads();
-  // tile -> registers -> block exponent -> scaled (h, d) tensors
-  const float* ub = u + (long long)(cz * KK) * T.sz + (long long)(cy * KK) * T.sy + cx * KK;
-  // EC: the two x-neighbour cell layers (256 rows of KK floats per face) go to the B region by
-  // cp.async -- coalesced 16-byte chunks; the x traces are formed from shared memory below.
-  constexpr bool kStageX = (MODE == MODE_FP16_EC) && (KK == 8 || KK == 4);
+  if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
+  const int tid = threadIdx.x;
+  const int sy = T.sy, sz = T.sz;
+  const long long tile_base = (long long)(T.cz * KK) * sz + (long long)(T.cy * KK) * sy + T.cx * KK;
+  const float* ub = u + tile_base;
+  if (pf) {  // L2 prefetch of this tile's rows of b (read in the z stage): DRAM latency paid here
+    const float* p = pf + (long long)batch * g.batch_stride + tile_base + (tid >> 4) * (long long)sz + (tid & 15) * sy;
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p + 8 * (long long)sz));
+  }
+  float* tr = reinterpret_cast<float*>(smem + SM_TR);   // f32 trace planes [face][alpha/beta][16][17]
+  float* xs = reinterpret_cast<float*>(smem + SM_XST);  // staged x-neighbour rows [hi][row 256][KK]
+  // (1) x-neighbour cell layers -> shared memory by cp.async (coalesced 16-byte chunks; a per-lane load
+  //     of a row's KK contiguous values would touch a different cache line per lane)
+  constexpr bool kStageX = KK >= 4;
   constexpr int XC = KK / 4;  // 16-byte chunks per staged row
-  float* xs = reinterpret_cast<float*>(smem + SM_BH);  // [hi][row 256][KK]
   if constexpr (kStageX) {
-    const int sy = (int)T.sy, sz = (int)T.sz;
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       if (!((T.nbm >> hi) & 1)) continue;
       float* dst = xs + hi * 256 * KK;
 #pragma unroll
       for (int k2 = 0; k2 < 256 * XC / kThreads; ++k2) {
-        const int c = threadIdx.x + kThreads * k2, ch = c % XC, row = c / XC, y = row & 15, z = row >> 4;
+        const int c = tid + kThreads * k2, ch = c % XC, row = c / XC, y = row & 15, z = row >> 4;
         const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;  // conflict-free LDS.128 quarter-warps
         cp_async16(dst + row * KK + 4 * sw, ub + z * sz + y * sy + (hi ? 16 : -KK) + 4 * ch);
       }
     }
   }
+  // (2) the tile -> registers (block maximum), and the y-neighbour lines (item p = z, q = x;
+  //     lanes along x: coalesced) so that all loads are in flight together
   float4 q4[1024 / kThreads];
   float mx = 0.f;
 #pragma unroll
   for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
-    const int i = threadIdx.x + k2 * kThreads;
+    const int i = tid + k2 * kThreads;
     const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
-    const float* src = ub + z * T.sz + y * T.sy + x4;
+    const float* src = ub + z * sz + y * sy + x4;
     if constexpr (KK == 2) {  // shifted colours start at an odd cell: only 8-byte alignment
       const float2 lo = __ldg(reinterpret_cast<const float2*>(src)), hi = __ldg(reinterpret_cast<const float2*>(src + 2));
       q4[k2] = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -424,17 +469,38 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     }
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q4[k2].x), fabsf(q4[k2].y)), fmaxf(fabsf(q4[k2].z), fabsf(q4[k2].w))));
   }
+  const int pq = tid & 15, pp = tid >> 4;  // this thread's trace items: (p, q) = (pp + 8 r, pq), r = 0, 1
+  float wy[2][2][KK];                      // [hi][r][node]
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+    if (!((T.nbm >> (2 + hi)) & 1)) continue;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float* b1 = ub + (pp + 8 * r) * sz + pq + (hi ? 16 : -KK) * sy;
+#pragma unroll
+      for (int c = 0; c < KK; ++c) wy[hi][r][c] = __ldg(b1 + c * sy);
+    }
+  }
   smax(&T.s_exp[0], mx);
-  if constexpr (kStageX) cp_async_wait_all();
+  float cl[KK], chi[KK];  // beta coefficients: lo neighbour ucol, hi neighbour urow
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    if constexpr (MODE == MODE_FP16_EC) {
+      cl[c] = op.ucol[c].h + op.ucol[c].d / kEcScale;
+      chi[c] = op.urow[c].h + op.urow[c].d / kEcScale;
+    } else {
+      cl[c] = op.ucol[c].h;
+      chi[c] = op.urow[c].h;
+    }
+  }
   __syncthreads();
   T.eu = block_exp(__int_as_float(T.s_exp[0]));
-  e.eu = T.eu;
   const float us = pow2f(T.eu);
   __half* uh = reinterpret_cast<__half*>(smem + SM_UH);
   __half* ud = reinterpret_cast<__half*>(smem + SM_UD);
 #pragma unroll
   for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {
-    const int i = threadIdx.x + k2 * kThreads;
+    const int i = tid + k2 * kThreads;
     const int x4 = (i & 3) * 4, y = (i >> 2) & 15, z = i >> 6;
     // x4..x4+3 are 4 consecutive halves of one 8-block in hidx: one 64-bit store per tensor
     uint2 hv, dv;
@@ -444,71 +510,108 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     *reinterpret_cast<uint2*>(uh + o) = hv;
     if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(ud + o) = dv;
   }
-  if constexpr (kStageX) {
-    // x traces from the staged rows: line (p = z, q = y), both faces; EC beta in fp32 (as TileEngine::traces)
+  // (3) y traces -> planes (faces 2, 3)
 #pragma unroll
-    for (int k2 = 0; k2 < 256 / kThreads; ++k2) {
-      const int row = threadIdx.x + kThreads * k2, p = row >> 4, qq = row & 15;
-      float a2[2] = {0.f, 0.f}, b2[2] = {0.f, 0.f};
+  for (int hi = 0; hi < 2; ++hi) {
+    if (!((T.nbm >> (2 + hi)) & 1)) continue;
 #pragma unroll
-      for (int hi = 0; hi < 2; ++hi) {
-        if (!((T.nbm >> hi) & 1)) continue;
+    for (int r = 0; r < 2; ++r) {
+      float al, be;
+      line_trace<MODE, KK>(wy[hi][r], hi ? chi : cl, hi, us, al, be);
+      float* pl = tr + ((2 + hi) * 2) * PLS + (pp + 8 * r) * PLP + pq;
+      pl[0] = al;
+      pl[PLS] = be;
+    }
+  }
+  // (4) z-neighbour lines (item p = y, q = x; ghost planes past the slab) -> planes (faces 4, 5)
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+    if (!((T.nbm >> (4 + hi)) & 1)) continue;
+    const bool inside = hi ? (T.cz + CPL < g.nz) : (T.cz > 0);
+    const float* zb;
+    if (inside) zb = ub + (hi ? 16 : -KK) * (long long)sz;
+    else zb = reinterpret_cast<const float*>(hi ? g.ghost_hi : g.ghost_lo) + ((long long)(T.cy * KK) * sy + T.cx * KK);
+    float w[2][KK];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float* b2 = zb + (pp + 8 * r) * sy + pq;
+#pragma unroll
+      for (int c = 0; c < KK; ++c) w[r][c] = __ldg(b2 + c * (long long)sz);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float al, be;
+      line_trace<MODE, KK>(w[r], hi ? chi : cl, hi, us, al, be);
+      float* pl = tr + ((4 + hi) * 2) * PLS + (pp + 8 * r) * PLP + pq;
+      pl[0] = al;
+      pl[PLS] = be;
+    }
+  }
+  // (5) x traces (item p = z, q = y) from the staged rows, or per-lane loads for Q1 (8-byte rows)
+  if constexpr (kStageX) cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int hi = 0; hi < 2; ++hi) {
+    if (!((T.nbm >> hi) & 1)) continue;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = pp + 8 * r, row = p * 16 + pq;
+      float w[KK];
+      if constexpr (kStageX) {
         const float* src = xs + hi * 256 * KK + row * KK;
-        float w[KK];
 #pragma unroll
         for (int ch = 0; ch < XC; ++ch) {
           const int sw = XC == 2 ? (ch ^ ((row >> 2) & 1)) : ch;
           const float4 v4 = *reinterpret_cast<const float4*>(src + 4 * sw);
           w[4 * ch] = v4.x; w[4 * ch + 1] = v4.y; w[4 * ch + 2] = v4.z; w[4 * ch + 3] = v4.w;
         }
-        float bs = 0.f;
-        if (hi) {
-          a2[1] = w[0] * us;
-#pragma unroll
-          for (int jj = 1; jj < KK; ++jj) bs = fmaf(op.urow[jj].h + op.urow[jj].d / kEcScale, w[jj] * us, bs);
-        } else {
-          a2[0] = w[KK - 1] * us;
-#pragma unroll
-          for (int jj = 0; jj < KK - 1; ++jj) bs = fmaf(op.ucol[jj].h + op.ucol[jj].d / kEcScale, w[jj] * us, bs);
-        }
-        b2[hi] = bs;
+      } else {
+        const float2 v2 = __ldg(reinterpret_cast<const float2*>(ub + p * sz + pq * sy + (hi ? 16 : -KK)));
+        w[0] = v2.x;
+        w[1] = v2.y;
       }
-      put_halo<MODE>(smem, 0, p, qq, a2[0], a2[1], b2[0], b2[1]);
+      float al, be;
+      line_trace<MODE, KK>(w, hi ? chi : cl, hi, us, al, be);
+      float* pl = tr + (hi * 2) * PLS + p * PLP + pq;
+      pl[0] = al;
+      pl[PLS] = be;
     }
-    __syncthreads();  // staged rows consumed before the trace planes overwrite them
-    e.template traces<kThreads, 1>(g, op, u);
-  } else {
-    e.template traces<kThreads>(g, op, u);
   }
   __syncthreads();
-  // tangential masses: y faces (2, 3) Mx along q, z faces (4, 5) Mx along q then My along p
+  // (6) tangential masses straight into the halo words: y faces Mx along q; z faces Mx along q (f32, in
+  //     place), then My along p; x faces need none.  Domain-boundary faces contribute zero (Nitsche is in
+  //     L_line[kind]).
   HOpFrag bm;
   ld_op(bm, tab->M, T.lane);
-  for (int task = T.warp; task < 8; task += kThreads / 32) {
-    const int face = 2 + (task >> 1);
-    if (!((T.nbm >> face) & 1)) continue;
-    plane_mass<MODE>(tr + (face * 2 + (task & 1)) * PLS, false, bm, T.g, T.t);
+  {
+    const int axis = 1 + (T.warp >> 1), hi = T.warp & 1, f = 2 * axis + hi;
+    float* pa = tr + (2 * f) * PLS;
+    if ((T.nbm >> f) & 1) {
+      face_mass<MODE>(T, pa, false, axis == 1, axis, hi, bm);
+    } else if (axis == 1) {
+      for (int i = T.lane; i < 256; i += 32) put_face<MODE>(smem, 1, i >> 4, i & 15, hi, 0.f, 0.f);
+    }
   }
   __syncthreads();
-  for (int task = T.warp; task < 4; task += kThreads / 32) {
-    const int face = 4 + (task >> 1);
-    if (!((T.nbm >> face) & 1)) continue;
-    plane_mass<MODE>(tr + (face * 2 + (task & 1)) * PLS, true, bm, T.g, T.t);
-  }
-  __syncthreads();
-  // f32 planes -> halo words (domain-boundary faces contribute zero: Nitsche is in L_line[kind])
-  constexpr int A0 = kStageX ? 1 : 0;
-  for (int it = threadIdx.x; it < (3 - A0) * 256; it += kThreads) {
-    const int axis = A0 + (it >> 8), pq = it & 255, p = pq >> 4, qq = pq & 15;
-    const float* lo = tr + (4 * axis) * PLS + p * PLP + qq;   // face 2 axis, alpha
-    const float* hi = tr + (4 * axis + 2) * PLS + p * PLP + qq;
-    const bool hl = (T.nbm >> (2 * axis)) & 1, hh = (T.nbm >> (2 * axis + 1)) & 1;
-    put_halo<MODE>(smem, axis, p, qq, hl ? lo[0] : 0.f, hh ? hi[0] : 0.f, hl ? lo[PLS] : 0.f, hh ? hi[PLS] : 0.f);
+  if (T.warp >= 2) {
+    const int hi = T.warp & 1, f = 4 + hi;
+    if ((T.nbm >> f) & 1) {
+      face_mass<MODE>(T, tr + (2 * f) * PLS, true, true, 2, hi, bm);
+    } else {
+      for (int i = T.lane; i < 256; i += 32) put_face<MODE>(smem, 2, i >> 4, i & 15, hi, 0.f, 0.f);
+    }
+  } else {
+    const int hi = T.warp & 1;
+    const bool on = (T.nbm >> hi) & 1;
+    const float* pa = tr + (2 * hi) * PLS;
+    for (int i = T.lane; i < 256; i += 32) {
+      const int p = i >> 4, qq = i & 15;
+      put_face<MODE>(smem, 0, p, qq, hi, on ? pa[p * PLP + qq] : 0.f, on ? pa[PLS + p * PLP + qq] : 0.f);
+    }
   }
   __syncthreads();
 
   // x and y stages on the warp's 4 z planes (in place)
-  constexpr bool kBD = false;  // L is never block diagonal
   HOpFrag blx, bly;
   ld_op(blx, tab->L[T.kind[0]], T.lane);
   ld_op(bly, tab->L[T.kind[1]], T.lane);
@@ -523,7 +626,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
       am.zero();
       as.zero();
       mma_bd<MODE>(am, a, bm);
-      mma_op<MODE, kBD>(as, a, blx);
+      mma_dense<MODE>(as, a, blx);
       unsigned w0, w1;
       T.halo(0, z, w0, w1);
       mma_halo<MODE>(as, w0, w1, T.hb);
@@ -548,7 +651,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
       c.zero();
       d.zero();
       mma_bd<MODE>(c, a, bm);
-      mma_op<MODE, kBD>(d, a, bly);
+      mma_dense<MODE>(d, a, bly);
       unsigned w0, w1;
       T.halo(1, z, w0, w1);
       mma_halo<MODE>(d, w0, w1, T.hb);
@@ -586,20 +689,35 @@ __device__ __forceinline__ void z_lines(const HTile<MODE>& T, int y, const HOpFr
   s.vals(v);
 }
 
+// this lane's 8 z-stage values of row y from a global vector (tile base p0): x = g + 8(i>>1)
+template <int MODE>
+__device__ __forceinline__ void ld_row(const HTile<MODE>& T, const float* __restrict__ p0, int y, float (&v)[2][4]) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i1 = 0; i1 < 2; ++i1) {
+      const float* p = p0 + T.zoff(nt, i1, y);
+      v[nt][i1] = __ldg(p);
+      v[nt][2 + i1] = __ldg(p + 8);
+    }
+}
+
 // accumulator element (nt, i): line = g + 8*(i>>1), output = 8nt + 2t + (i&1)
 template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restrict__ u, float* __restrict__ v, Geom g,
-                                                         LevelOp<KK, MODE> op, const HTables* __restrict__ tab) {
+                                                         dm::Band bd, LevelOp<KK, MODE> op,
+                                                         const HTables* __restrict__ tab) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
-  u += (long long)blockIdx.y * g.batch_stride;
-  v += (long long)blockIdx.y * g.batch_stride;
-  if (!tile_front<MODE, KK>(T, smem, g, op, tab, u)) return;
+  int batch;
+  const float* uin = u;
+  if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, uin, batch)) return;
+  v += (long long)batch * g.batch_stride;
   __syncthreads();
   HOpFrag bm, bl;
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[T.kind[2]], T.lane);
-  float* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
+  float* vb = v + ((long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK);
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
@@ -609,9 +727,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        vb[(long long)z * T.sz + (long long)y * T.sy + x] = o[nt][i] * os;
+      for (int i1 = 0; i1 < 2; ++i1) {
+        float* p = vb + T.zoff(nt, i1, y);
+        p[0] = o[nt][i1] * os;
+        p[8] = o[nt][2 + i1] * os;
       }
   }
 }
@@ -620,17 +739,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
 // V (x3) Lambda^-1 V^T (x3) r, x_new = x_old + correction (sf_dmma.cu k_colour_dmma8 stage order)
 template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restrict__ xo, const float* __restrict__ b,
-                                                          float* __restrict__ xn, Geom g, LevelOp<KK, MODE> op,
-                                                          const HTables* __restrict__ tab,
+                                                          float* __restrict__ xn, Geom g, dm::Band bd,
+                                                          LevelOp<KK, MODE> op, const HTables* __restrict__ tab,
                                                           const DenTab* __restrict__ den) {
   extern __shared__ __align__(128) char smem[];
   constexpr bool kBDV = KK < 8;  // Q3 / Q1: the line transform is blockdiag of the patches' V
   HTile<MODE> T;
-  prefetch_b_rows<KK>(g, b);
-  if (!tile_front<MODE, KK>(T, smem, g, op, tab, xo)) return;
+  int batch;
+  const float* xin = xo;
+  if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
   __syncthreads();
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
-  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
+  const long long base = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
+  const float* bb = b + base;
   HOpFrag bm, bl, bv;
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[kz], T.lane);
@@ -642,13 +763,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     float bvv[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        bvv[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + x);
-      }
+    ld_row<MODE>(T, bb, y, bvv);
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
@@ -760,17 +875,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   // z lines: backward V_z, x_new = x_old + correction (back to true units)
   ld_op(bv, tab->Vb[kz], T.lane);
   const float cs = pow2f(-(op.sc.aD + 6 * op.sc.aV + er));
+  const float* xb = xo + base;
+  float* nb = xn + base;
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     float xv[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        xv[nt][i] = __ldg(xo + off0 + (long long)z * T.sz + (long long)y * T.sy + x);
-      }
+    ld_row<MODE>(T, xb, y, xv);
     HFrag a;
     ld_a<MODE>(a, T.UH(), T.UD(), T.oz(y), true);
     HAcc<MODE> acc;
@@ -779,10 +890,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = T.g + 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
-        xn[off0 + (long long)z * T.sz + (long long)y * T.sy + 8 * (i >> 1)] = fmaf(acc.val(nt, i), cs, xv[nt][i]);
+      for (int i1 = 0; i1 < 2; ++i1) {
+        float* p = nb + T.zoff(nt, i1, y);
+        const int z = 8 * nt + 2 * T.t + i1;
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8) {
+          const int i = 2 * h8 + i1;
+          if (KK < 8 && (T.g + 8 * h8 < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
+          p[8 * h8] = fmaf(acc.val(nt, i), cs, xv[nt][i]);
+        }
       }
   }
 }
@@ -798,32 +914,27 @@ struct HPTab {
 template <int MODE, int KK = K>
 __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* __restrict__ x,
                                                                   const float* __restrict__ b,
-                                                                  float* __restrict__ coarse, Geom g,
+                                                                  float* __restrict__ coarse, Geom g, dm::Band bd,
                                                                   LevelOp<KK, MODE> op,
                                                                   const HTables* __restrict__ tab,
                                                                   const HPTab* __restrict__ pt) {
   extern __shared__ __align__(128) char smem[];
   HTile<MODE> T;
-  prefetch_b_rows<KK>(g, b);
-  if (!tile_front<MODE, KK>(T, smem, g, op, tab, x)) return;
+  int batch;
+  const float* xin = x;
+  if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
   __syncthreads();
   HOpFrag bm, bl;
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[T.kind[2]], T.lane);
-  const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK + T.g;
+  const float* bb = b + ((long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK);
   float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     float bvv[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int xx = 8 * (i >> 1), z = 8 * nt + 2 * T.t + (i & 1);
-        bvv[nt][i] = __ldg(b + off0 + (long long)z * T.sz + (long long)y * T.sy + xx);
-      }
+    ld_row<MODE>(T, bb, y, bvv);
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
@@ -943,10 +1054,9 @@ static void pack_op_frags(int mode, const double* Op /* [16][16] */, HOp& dst) {
   }
 }
 
-// halo B words (see mma_halo / put_halo): k rows 0: alpha_lo coupling urow (outputs < KK),
-// 1: alpha_hi coupling ucol (outputs >= 16 - KK), 2: beta_lo -> output 0, 3: beta_hi -> output 15;
-// EC corr rows 4..7 carry the main halves against the data's residual halves; fp16 rows 6, 7
-// add beta's residual half / 2048.
+// halo B words (see mma_halo / put_face): k rows 0: alpha_lo coupling urow (outputs < KK), 1: beta_lo ->
+// output 0, 2: alpha_hi coupling ucol (outputs >= 16 - KK), 3: beta_hi -> output 15; EC corr rows 4..7
+// carry the main halves against the data's residual halves; fp16 rows 5, 7 add beta's residual / 2048.
 static void pack_halo(int mode, int KK, const double* ucol, const double* urow, uint4* dst /* [32] */) {
   for (int ln = 0; ln < 32; ++ln) {
     const int gg = ln >> 2, tt = ln & 3;
@@ -955,13 +1065,13 @@ static void pack_halo(int mode, int KK, const double* ucol, const double* urow, 
       const int n = 8 * nt + gg;
       unsigned short ch[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};  // coupling (h, d) of rows 0..3 at n
       if (n < KK) split_host(mode, urow[n], ch[0], cd[0]);
-      if (n >= 16 - KK) split_host(mode, ucol[n - (16 - KK)], ch[1], cd[1]);
-      if (n == 0) ch[2] = half_bits(1.0f);
+      if (n == 0) ch[1] = half_bits(1.0f);
+      if (n >= 16 - KK) split_host(mode, ucol[n - (16 - KK)], ch[2], cd[2]);
       if (n == 15) ch[3] = half_bits(1.0f);
       unsigned short mrow[8] = {ch[0], ch[1], ch[2], ch[3], 0, 0, 0, 0};
-      unsigned short crow[8] = {cd[0], cd[1], 0, 0, ch[0], ch[1], ch[2], ch[3]};
+      unsigned short crow[8] = {cd[0], 0, cd[2], 0, ch[0], ch[1], ch[2], ch[3]};
       if (mode != MODE_FP16_EC) {
-        mrow[6] = n == 0 ? half_bits(1.0f / kEc) : 0;
+        mrow[5] = n == 0 ? half_bits(1.0f / kEc) : 0;
         mrow[7] = n == 15 ? half_bits(1.0f / kEc) : 0;
       }
       w[nt] = (unsigned)mrow[2 * tt] | ((unsigned)mrow[2 * tt + 1] << 16);
@@ -1085,48 +1195,62 @@ static bool smem_attr(F* fn) {
 }
 
 // Q7 (KK = 8) and the 16-point line tiles (KK = 4, 2; kUseGeneric when the grid does not tile)
+// banded 3-D grid of the tiles (dm::band_tile); very large batches are split across launches
+static dim3 band_grid(const Geom& g, const dm::Band& bd, int batch) {
+  return dim3(g.ntx, bd.by, bd.zb * batch);
+}
+
+// the 16-point line tiles of Q3 / Q1 (KK = 4, 2): tile counts in lines (kUseGeneric when the grid does not tile)
+template <int KK>
+static bool line_geom(const Geom& g0, Geom& g, bool colour, int zcells) {
+  constexpr int CPL = 16 / KK;
+  g = g0;
+  if (KK == 8) return true;
+  if (g0.nx % CPL || g0.ny % CPL || zcells % CPL) return false;
+  if (colour) {
+    const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
+    for (int a = 0; a < 3; ++a)
+      if (s3[a] && n3[a] < CPL + 2) return false;
+  }
+  g.ntx = g.nx / CPL;
+  g.nty = g.ny / CPL;
+  g.ntz = zcells / CPL;
+  return true;
+}
+
+// Q7 (KK = 8) and the 16-point line tiles (KK = 4, 2)
 template <int MODE, int KK>
 static int vmult_t(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
-  constexpr int CPL = 16 / KK;
-  Geom g = g0;
-  if (KK < 8) {
-    const int zc = 2 * g0.ntz;  // the caller's z range in cells
-    if (g0.nx % CPL || g0.ny % CPL || zc % CPL) return kUseGeneric;
-    g.ntx = g.nx / CPL;
-    g.nty = g.ny / CPL;
-    g.ntz = zc / CPL;
-  }
+  Geom g;
+  if (!line_geom<KK>(g0, g, false, 2 * g0.ntz)) return kUseGeneric;  // 2 ntz: the caller's z range in cells
   const HTables* tab = tables(MODE, opd, nullptr, KK);
   if (!tab) return -3;
   auto op = pack_op_h<MODE, KK>(opd, nullptr);
   if (!smem_attr(k_vmult_h8<MODE, KK>)) return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_vmult_h8<MODE, KK><<<dim3(tiles, batch), kThreads, kSmem, st>>>((const float*)u, (float*)v, g, op, tab);
+  const dm::Band bd = dm::make_band(g);
+  const int per = 65535 / bd.zb;  // batches per launch (gridDim.z limit)
+  for (int b0 = 0; b0 < batch; b0 += per) {
+    const int nb = batch - b0 < per ? batch - b0 : per;
+    const long long off = (long long)b0 * g.batch_stride;
+    k_vmult_h8<MODE, KK><<<band_grid(g, bd, nb), kThreads, kSmem, st>>>((const float*)u + off, (float*)v + off, g,
+                                                                        bd, op, tab);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
 template <int MODE, int KK>
 static int colour_t(const Geom& g0, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
                     cudaStream_t st) {
-  constexpr int CPL = 16 / KK;
-  Geom g = g0;
-  if (KK < 8) {
-    if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
-    const int n3[3] = {g0.nx, g0.ny, g0.nz}, s3[3] = {g0.tx0, g0.ty0, g0.tz0};
-    for (int a = 0; a < 3; ++a)
-      if (s3[a] && n3[a] < CPL + 2) return kUseGeneric;
-    g.ntx = g.nx / CPL;
-    g.nty = g.ny / CPL;
-    g.ntz = g.nz / CPL;
-  }
+  Geom g;
+  if (!line_geom<KK>(g0, g, true, g0.nz)) return kUseGeneric;
   const DenTab* den = nullptr;
   const HTables* tab = tables(MODE, opd, eigd, KK, &den);
   if (!tab || !den) return -3;
   auto op = pack_op_h<MODE, KK>(opd, eigd);
   if (!smem_attr(k_colour_h8<MODE, KK>)) return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_colour_h8<MODE, KK><<<tiles, kThreads, kSmem, st>>>((const float*)xo, (const float*)b, (float*)xn, g, op, tab,
-                                                         den);
+  const dm::Band bd = dm::make_band(g);
+  k_colour_h8<MODE, KK><<<band_grid(g, bd, 1), kThreads, kSmem, st>>>((const float*)xo, (const float*)b, (float*)xn,
+                                                                      g, bd, op, tab, den);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -1174,22 +1298,16 @@ static const HPTab* ptables(int mode, const double* embd_raw, int KK = K) {
 template <int MODE, int KK>
 static int resid_restrict_t(const Geom& g0, const double* opd, const double* embd, const void* x, const void* b,
                             void* coarse, cudaStream_t st) {
-  constexpr int CPL = 16 / KK;
-  Geom g = g0;
-  if (KK < 8) {
-    if (g0.nx % CPL || g0.ny % CPL || g0.nz % CPL) return kUseGeneric;
-    g.ntx = g.nx / CPL;
-    g.nty = g.ny / CPL;
-    g.ntz = g.nz / CPL;
-  }
+  Geom g;
+  if (!line_geom<KK>(g0, g, false, g0.nz)) return kUseGeneric;
   const HTables* tab = tables(MODE, opd, nullptr, KK);
   const HPTab* pt = ptables(MODE, embd, KK);
   if (!tab || !pt) return -3;
   auto op = pack_op_h<MODE, KK>(opd, nullptr);
   if (!smem_attr(k_resid_restrict_h8<MODE, KK>)) return -3;
-  const int tiles = g.ntx * g.nty * g.ntz;
-  k_resid_restrict_h8<MODE, KK><<<tiles, kThreads, kSmem, st>>>((const float*)x, (const float*)b, (float*)coarse, g,
-                                                                op, tab, pt);
+  const dm::Band bd = dm::make_band(g);
+  k_resid_restrict_h8<MODE, KK><<<band_grid(g, bd, 1), kThreads, kSmem, st>>>((const float*)x, (const float*)b,
+                                                                               (float*)coarse, g, bd, op, tab, pt);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
