@@ -469,16 +469,24 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     }
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q4[k2].x), fabsf(q4[k2].y)), fmaxf(fabsf(q4[k2].z), fabsf(q4[k2].w))));
   }
-  const int pq = tid & 15, pp = tid >> 4;  // this thread's trace items: (p, q) = (pp + 8 r, pq), r = 0, 1
-  float wy[2][2][KK];                      // [hi][r][node]
+  // trace items of one axis: (hi, p, q0..q0+VW-1), VW consecutive lines along x per vector load
+  constexpr int VW = KK == 2 ? 2 : 4;         // Q1 shifted colours start at odd cells: 8-byte alignment
+  constexpr int NQ = 16 / VW, IPT = 2 * 16 * NQ / kThreads;  // items per thread and axis
+  float wy[IPT][KK][VW];
 #pragma unroll
-  for (int hi = 0; hi < 2; ++hi) {
+  for (int it = 0; it < IPT; ++it) {
+    const int item = tid + kThreads * it, hi = item / (16 * NQ), p = (item / NQ) & 15, q0 = (item % NQ) * VW;
     if (!((T.nbm >> (2 + hi)) & 1)) continue;
+    const float* b1 = ub + p * sz + q0 + (hi ? 16 : -KK) * sy;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float* b1 = ub + (pp + 8 * r) * sz + pq + (hi ? 16 : -KK) * sy;
-#pragma unroll
-      for (int c = 0; c < KK; ++c) wy[hi][r][c] = __ldg(b1 + c * sy);
+    for (int c = 0; c < KK; ++c) {
+      if constexpr (VW == 4) {
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(b1 + c * sy));
+        wy[it][c][0] = v4.x; wy[it][c][1] = v4.y; wy[it][c][2] = v4.z; wy[it][c][3] = v4.w;
+      } else {
+        const float2 v2 = __ldg(reinterpret_cast<const float2*>(b1 + c * sy));
+        wy[it][c][0] = v2.x; wy[it][c][1] = v2.y;
+      }
     }
   }
   smax(&T.s_exp[0], mx);
@@ -511,45 +519,60 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(ud + o) = dv;
   }
   // (3) y traces -> planes (faces 2, 3)
+  auto traces_out = [&](const float (&w)[KK][VW], int face, int p, int q0, int hi) {
 #pragma unroll
-  for (int hi = 0; hi < 2; ++hi) {
-    if (!((T.nbm >> (2 + hi)) & 1)) continue;
+    for (int v = 0; v < VW; ++v) {
+      float wl[KK];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+      for (int c = 0; c < KK; ++c) wl[c] = w[c][v];
       float al, be;
-      line_trace<MODE, KK>(wy[hi][r], hi ? chi : cl, hi, us, al, be);
-      float* pl = tr + ((2 + hi) * 2) * PLS + (pp + 8 * r) * PLP + pq;
+      line_trace<MODE, KK>(wl, hi ? chi : cl, hi, us, al, be);
+      float* pl = tr + (face * 2) * PLS + p * PLP + q0 + v;
       pl[0] = al;
       pl[PLS] = be;
     }
+  };
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const int item = tid + kThreads * it, hi = item / (16 * NQ), p = (item / NQ) & 15, q0 = (item % NQ) * VW;
+    if (!((T.nbm >> (2 + hi)) & 1)) continue;
+    traces_out(wy[it], 2 + hi, p, q0, hi);
   }
   // (4) z-neighbour lines (item p = y, q = x; ghost planes past the slab) -> planes (faces 4, 5)
+  {
+    float wz[IPT][KK][VW];
 #pragma unroll
-  for (int hi = 0; hi < 2; ++hi) {
-    if (!((T.nbm >> (4 + hi)) & 1)) continue;
-    const bool inside = hi ? (T.cz + CPL < g.nz) : (T.cz > 0);
-    const float* zb;
-    if (inside) zb = ub + (hi ? 16 : -KK) * (long long)sz;
-    else zb = reinterpret_cast<const float*>(hi ? g.ghost_hi : g.ghost_lo) + ((long long)(T.cy * KK) * sy + T.cx * KK);
-    float w[2][KK];
+    for (int it = 0; it < IPT; ++it) {
+      const int item = tid + kThreads * it, hi = item / (16 * NQ), p = (item / NQ) & 15, q0 = (item % NQ) * VW;
+      if (!((T.nbm >> (4 + hi)) & 1)) continue;
+      const bool inside = hi ? (T.cz + CPL < g.nz) : (T.cz > 0);
+      const float* zb;
+      if (inside) zb = ub + (hi ? 16 : -KK) * (long long)sz;
+      else zb = reinterpret_cast<const float*>(hi ? g.ghost_hi : g.ghost_lo) +
+                ((long long)(T.cy * KK) * sy + T.cx * KK);
+      const float* b2 = zb + p * sy + q0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float* b2 = zb + (pp + 8 * r) * sy + pq;
-#pragma unroll
-      for (int c = 0; c < KK; ++c) w[r][c] = __ldg(b2 + c * (long long)sz);
+      for (int c = 0; c < KK; ++c) {
+        if constexpr (VW == 4) {
+          const float4 v4 = __ldg(reinterpret_cast<const float4*>(b2 + c * (long long)sz));
+          wz[it][c][0] = v4.x; wz[it][c][1] = v4.y; wz[it][c][2] = v4.z; wz[it][c][3] = v4.w;
+        } else {
+          const float2 v2 = __ldg(reinterpret_cast<const float2*>(b2 + c * (long long)sz));
+          wz[it][c][0] = v2.x; wz[it][c][1] = v2.y;
+        }
+      }
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      float al, be;
-      line_trace<MODE, KK>(w[r], hi ? chi : cl, hi, us, al, be);
-      float* pl = tr + ((4 + hi) * 2) * PLS + (pp + 8 * r) * PLP + pq;
-      pl[0] = al;
-      pl[PLS] = be;
+    for (int it = 0; it < IPT; ++it) {
+      const int item = tid + kThreads * it, hi = item / (16 * NQ), p = (item / NQ) & 15, q0 = (item % NQ) * VW;
+      if (!((T.nbm >> (4 + hi)) & 1)) continue;
+      traces_out(wz[it], 4 + hi, p, q0, hi);
     }
   }
   // (5) x traces (item p = z, q = y) from the staged rows, or per-lane loads for Q1 (8-byte rows)
   if constexpr (kStageX) cp_async_wait_all();
   __syncthreads();
+  const int pq = tid & 15, pp = tid >> 4;  // x trace items (p = pp + 8 r, q = pq)
 #pragma unroll
   for (int hi = 0; hi < 2; ++hi) {
     if (!((T.nbm >> hi) & 1)) continue;
@@ -615,7 +638,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   HOpFrag blx, bly;
   ld_op(blx, tab->L[T.kind[0]], T.lane);
   ld_op(bly, tab->L[T.kind[1]], T.lane);
-#pragma unroll
+#pragma unroll 1
   for (int zz = 0; zz < 4; ++zz) {
     const int z = 4 * T.warp + zz;
     {
@@ -804,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   ld_op(bbx, tab->Vb[kx], T.lane);
   ld_op(bby, tab->Vb[ky], T.lane);
   const DenTab* dt = den + (kx * 16 + ky * 4 + kz);
-#pragma unroll
+#pragma unroll 1
   for (int zz = 0; zz < 4; ++zz) {
     const int z = 4 * T.warp + zz;
     // denominators of this lane's V_x^T outputs (issued early)
