@@ -771,22 +771,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   int batch;
   const float* xin = xo;
   if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
-  __syncthreads();
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
   const long long base = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   const float* bb = b + base;
+  float rr[4][2][4];  // b of this warp's rows (in flight across the barrier), then the residual
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, bb, 4 * T.warp + yy, rr[yy]);
+  __syncthreads();
   HOpFrag bm, bl, bv;
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[kz], T.lane);
   ld_op(bv, tab->Vf[kz], T.lane);
   // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
-  float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    float bvv[2][4];
-    ld_row<MODE>(T, bb, y, bvv);
+    const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
+                             {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
@@ -894,17 +896,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
     }
     __syncwarp();
   }
+  // x_old values of this warp's final rows in flight across the barrier (L2 latency hidden behind it)
+  const float* xb = xo + base;
+  float* nb = xn + base;
+  float xv4[4][2][4];
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, xb, 4 * T.warp + yy, xv4[yy]);
   __syncthreads();
   // z lines: backward V_z, x_new = x_old + correction (back to true units)
   ld_op(bv, tab->Vb[kz], T.lane);
   const float cs = pow2f(-(op.sc.aD + 6 * op.sc.aV + er));
-  const float* xb = xo + base;
-  float* nb = xn + base;
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    float xv[2][4];
-    ld_row<MODE>(T, xb, y, xv);
+    const float (&xv)[2][4] = xv4[yy];
     HFrag a;
     ld_a<MODE>(a, T.UH(), T.UD(), T.oz(y), true);
     HAcc<MODE> acc;
@@ -946,18 +951,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
   int batch;
   const float* xin = x;
   if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
+  const float* bb = b + ((long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK);
+  float rr[4][2][4];  // b of this warp's rows (in flight across the barrier), then the residual
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, bb, 4 * T.warp + yy, rr[yy]);
   __syncthreads();
   HOpFrag bm, bl;
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[T.kind[2]], T.lane);
-  const float* bb = b + ((long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK);
-  float rr[4][2][4];
   const float os = pow2f(-(op.sc.aA + T.eu));
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    float bvv[2][4];
-    ld_row<MODE>(T, bb, y, bvv);
+    const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
+                             {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
     float mx = 0.f;
 #pragma unroll
