@@ -109,43 +109,55 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(threads=None, level=5, k=7, reps=2):
-    """Reference algorithm on the host: numpy port of apply_operator, all host threads."""
-    from oracle import port
+def cpu_baseline(reps=3):
+    """The reference path on the host as BASELINE.md §3 defines it (oracle/cpu_timing.py): C1 = Q7 L4
+    fp64 vmult on ONE pinned core, the reference's compiled kernel (oracle/_ref) vs its numpy einsum
+    fallback, best of 3, the faster reported; plus the all-cores figure (threaded BLAS form, Q7 L5)."""
+    from oracle import cpu_timing
 
-    threads = threads or port.default_threads()
-    H = port.Hierarchy(level, k)
-    u = np.random.default_rng(0).standard_normal(H.n_dofs(level))
-    port.apply_operator(H, level, u, "fp64", threads)  # warm-up
-    best = math.inf
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        port.apply_operator(H, level, u, "fp64", threads)
-        best = min(best, time.perf_counter() - t0)
-    return {"value": H.n_dofs(level) / best / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"Q{k} level {level} ({H.n_dofs(level)} DoF) fp64 vmult, oracle/port.py (numpy einsum, "
-                      f"outer batch split over {threads} threads), best of {reps}",
-            "seconds_per_vmult": best}
+    c1 = cpu_timing.run([("vmult", 7, 4)], reps=reps)
+    case = c1["cases"]["vmult Q7 L4"]
+    allc = cpu_timing.all_cores_vmult()
+    best = case["best_backend"]
+    return {"value": case["mdofs_per_s"] / 1e3, "unit": UNIT, "cores": 1,
+            "kind": "reference" if best == "compiled" else "port",
+            "sample": f"C1: Q7 level 4 (16^3 cells, {case['dofs']} DoF) fp64 vmult on one pinned core, best of "
+                      f"{reps}; backend {best} (compiled oracle/_ref {case['seconds']['compiled']} s, numpy einsum "
+                      f"{case['seconds']['einsum']} s per vmult)",
+            "cpu_model": c1["cpu_model"], "nproc": c1["nproc"],
+            "all_cores": {"value": allc["dofs"] / allc["seconds"] / 1e9, "unit": UNIT, "cores": allc["threads"],
+                          "sample": f"{allc['case']} fp64 vmult, contractions as threaded BLAS GEMMs, best of 2"},
+            "seconds_per_vmult": min(v for v in case["seconds"].values() if v)}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path with all host threads (bounded sample per step),
+    plus the single-core as-shipped C1 figure."""
     if rank != 0:
         return
+    from oracle import cpu_timing
+
     steps = []
     res = None
     for _ in range(args.warmup):
-        cpu_baseline(reps=1)
+        cpu_timing.all_cores_vmult(reps=1)
     for _ in range(args.steps):
-        res = cpu_baseline(reps=1)
-        steps.append(res["value"])
+        res = cpu_timing.all_cores_vmult(reps=1)
+        steps.append(res["dofs"] / res["seconds"] / 1e9)
     value = float(np.median(steps))
+    single = cpu_baseline()
+    sample = (f"Q7 level 5 ({res['dofs']} DoF) fp64 vmult per step, the reference algorithm (oracle/port.py) "
+              f"with its contractions as threaded BLAS GEMMs on {res['threads']} host threads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["seconds_per_vmult"] * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": res["dofs"] / value / 1e6, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "Q7 SIPG Laplace vmult, fp64 (bounded CPU sample: Q7 level 5, 16.8M DoF)",
-                       "degree": 7, "level": 5, "dofs": 16777216},
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                       "degree": 7, "level": 5, "dofs": res["dofs"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["threads"], "kind": "port",
+                             "sample": sample, "cpu_model": single["cpu_model"], "nproc": single["nproc"],
+                             "single_core_as_shipped": {k: single[k] for k in ("value", "unit", "cores", "kind",
+                                                                               "sample")}},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -277,9 +289,15 @@ def main():
                 "hbm": {"achieved": 16 * D / (kms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                         "frac": 16 * D / (kms * 1e-3) / 1e9 / hbm, "peak_source": hbm_src}}
     traffic = os.path.join(ROOT, "profiles", "vmult_traffic.json")
-    if os.path.exists(traffic):
+    if os.path.exists(traffic):  # ncu-measured bytes, used only while the kernel sources are unchanged
         try:
-            roofline["traffic"] = json.load(open(traffic)).get(f"k{k}_l{lvl}_fp64")
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from record_traffic import source_hash
+
+            rec = json.load(open(traffic))
+            if rec.get("source_hash") == source_hash():
+                roofline["traffic"] = rec.get(f"k{k}_l{lvl}_fp64")
+                roofline["traffic_source"] = "profiles/vmult_traffic.json (ncu dram bytes, same kernel sources)"
         except Exception:
             pass
 

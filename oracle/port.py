@@ -175,11 +175,35 @@ class Hierarchy:
 # ----------------------------------------------------------- contraction
 
 
+# Single-threaded contraction backend (_core/__init__.py:12-24 picks one at import time):
+# "einsum" = the reference's numpy fallback (_core/fallback.py:10-15), "compiled" = the
+# reference's own Cython kernel contract_f8/_f4 built from its sources into oracle/_ref
+# (oracle/build_ref.py) -- both exactly as the reference ships them.
+BACKEND = "einsum"
+_REF_KERNEL = None
+
+
+def set_backend(name: str) -> str:
+    """Select "einsum" or "compiled" (needs oracle/_ref); returns the previous backend."""
+    global BACKEND, _REF_KERNEL
+    if name not in ("einsum", "compiled"):
+        raise ValueError(name)
+    if name == "compiled" and _REF_KERNEL is None:
+        from oracle import build_ref
+
+        _REF_KERNEL = build_ref.load()
+        if _REF_KERNEL is None:
+            raise RuntimeError("oracle/_ref is not built (python oracle/build_ref.py)")
+    prev, BACKEND = BACKEND, name
+    return prev
+
+
 def contract(m: np.ndarray, w: np.ndarray, axis: int, threads: int = 1) -> np.ndarray:
     """_core/__init__.py:27-59 + _core/fallback.py:10-15: out[o,i,r] = sum_k m[i,k] w[o,k,r].
 
     threads == 1: numpy einsum without ``optimize`` -- the reference's own
-    fallback backend, single-threaded, ascending k (the checker path).
+    fallback backend, single-threaded, ascending k (the checker path); or, with
+    set_backend("compiled"), the reference's compiled kernel from oracle/_ref.
     threads > 1: the same contraction as BLAS GEMMs (np.matmul) on ``threads``
     BLAS threads -- used only for the multi-core CPU *baseline* timing; it
     differs from einsum by summation order only (~1e-16 relative).
@@ -192,7 +216,10 @@ def contract(m: np.ndarray, w: np.ndarray, axis: int, threads: int = 1) -> np.nd
     shape = w.shape[:axis] + (m.shape[0],) + w.shape[axis + 1:]
     if threads <= 1:
         out = np.empty((outer, m.shape[0], inner), dtype=w.dtype)
-        np.einsum("ik,okr->oir", m, w3, out=out)
+        if BACKEND == "compiled":  # _core/__init__.py:53-58 -> _contract.pyx:14-45
+            (_REF_KERNEL.contract_f8 if w.dtype == np.float64 else _REF_KERNEL.contract_f4)(w3, m, out)
+        else:
+            np.einsum("ik,okr->oir", m, w3, out=out)
         return out.reshape(shape)
     from threadpoolctl import threadpool_limits
 
