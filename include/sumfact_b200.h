@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 2  /* 2: sf_div, SF_LINCOMB_MAX_TERMS */
+#define SF_ABI_VERSION 3  /* 2: sf_div, SF_LINCOMB_MAX_TERMS; 3: sf_quad_error / sf_quad_load / sf_face_load */
 #define SF_MAX_DEGREE 7
 
 #define SF_OK 0
@@ -145,6 +145,28 @@ int sf_axpby(long long n, double alpha, const double* x, double beta, double* y,
 
 /* float variant used inside low-precision V-cycles: y = alpha * x + beta * y (fp32). */
 int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream);
+
+/* ---- device pre/post-processing with general data (discretization.py:317-459) ----
+ * Level with n cells per axis, degree k (K = k + 1 nodes), q Gauss points per cell axis (k + 2 or k + 3);
+ * a z-chunk of nzc cells starting at global cell z0.  Gauss-point data are tabulated by the caller on the
+ * chunk's (nzc q) x (n q) x (n q) point grid (z, y, x); w = the n q per-axis weights (times h).
+ *
+ * sf_quad_error: *out_dev = sum over the chunk of w_z w_y w_x (I u - fq)^2, I = Sz (x) Sy (x) Sx applied to
+ * u (the chunk's cells, flat (z, y, x)); mats = [Sx | Sy | Sz], each q x K (values, or one derivative axis).
+ * part_dev: n * n * nzc doubles of scratch (fixed-order two-level reduction).
+ * Replaces l2_error / h1_seminorm_error's _quadrature_values + weighted sum   discretization.py:405-459. */
+int sf_quad_error(int k, int q, int n, int z0, int nzc, const double* u, const double* mats, const double* fq,
+                  const double* w, double* part_dev, double* out_dev, void* stream);
+/* sf_quad_load: b (the chunk's cells) = (S^T (x) S^T (x) S^T)(w f) cell by cell; st = S^T (K x q).
+ * Replaces assemble_rhs's cell integrals                                        discretization.py:317-348. */
+int sf_quad_load(int k, int q, int n, int z0, int nzc, const double* fq, const double* st, const double* w,
+                 double* b, void* stream);
+/* sf_face_load: b (local slab [z0, z0 + nzc) cells) += Nitsche data term of one domain face: normal tensor
+ * axis 0..2, side 0 / 1; g = the face's (n q)^2 point grid (slow, fast tangential axis, global); coef = the
+ * K normal coefficients (gamma e0 + d0, or gamma e1 - d1).  Replaces _rhs_boundary   discretization.py:351-394. */
+int sf_face_load(int k, int q, int n, int z0, int nzc, int axis, int side, const double* g, const double* st,
+                 const double* w, const double* coef, double* b, void* stream);
+const char* sf_quad_last_error(void);
 
 /* ---- binary16 primitives of the precision semantics (precision.py:60-197), same cvt as the FP16 kernels ---- */
 

@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["sf_ops.cu", "sf_vec.cu", "sf_dmma.cu", "sf_hmma.cu", "sf_contract.cu", "sf_half.cu"]
+SOURCES = ["sf_ops.cu", "sf_vec.cu", "sf_dmma.cu", "sf_hmma.cu", "sf_contract.cu", "sf_half.cu", "sf_quad.cu"]
 
 
 def _deps():

@@ -292,21 +292,6 @@ def materialize_operator(hier: MeshHierarchy, level: int, mode: PrecisionMode = 
 # same sum-factorised quadrature as the reference.
 
 
-def _cells_view(arr, n, q):
-    return np.ascontiguousarray(arr.reshape(n, q, n, q, n, q).transpose(0, 2, 4, 1, 3, 5))
-
-
-def _cells_back(w, n, q):
-    return w.transpose(0, 3, 1, 4, 2, 5).reshape(n * q, n * q, n * q)
-
-
-def _contract_last3(w, mats):
-    """mats[a] along tensor axis a (numpy axis 5-a), x first."""
-    w = np.einsum("ik,...k->...i", mats[0], w)
-    w = np.einsum("ik,...kx->...ix", mats[1], w)
-    return np.einsum("ik,...kyx->...iyx", mats[2], w)
-
-
 def _axis_points(hier, level, pts):
     n, h = hier.n_cells(level), hier.h(level)
     return ((np.arange(n)[:, None] + np.asarray(pts)[None, :]) * h).ravel()
@@ -317,51 +302,174 @@ def _coords(axis_pts):
     return X, Y, Z
 
 
-def _weights(hier, level, rule):
-    wa = np.tile(rule.weights, hier.n_cells(level)) * hier.h(level)
-    return wa[:, None, None] * wa[None, :, None] * wa[None, None, :]
+# ------------------------------------------- device pre/post-processing, general data
+# The reference evaluates f, g and the exact solution on the full Gauss-point grid and contracts with
+# numpy (discretization.py:317-459).  Here the contractions are the library's own sum-factorised
+# kernels (csrc/sf_quad.cu) and the data are tabulated one z-chunk of cells at a time: on the device
+# when the callable accepts CUDA tensors (torch operations), else on the host for that chunk only.
 
 
-def assemble_rhs(hier: MeshHierarchy, level: int, f, g=None, quad_points: int | None = None) -> np.ndarray:
-    """Load vector: cell integrals of f v (+ Nitsche data terms for g), discretization.py:317-394."""
-    from .basis import gauss_rule, lagrange_derivatives, lagrange_values, penalty
+def _eval_chunk(fn, X, Y, Z, shape):
+    """fn at the broadcast coordinates X (1,1,nx), Y (1,ny,1), Z (nz,1,1) -> contiguous fp64 CUDA tensor."""
+    try:
+        v = fn(X, Y, Z)
+        if isinstance(v, torch.Tensor) and v.is_cuda:
+            return v.to(torch.float64).expand(shape).contiguous()
+    except Exception:  # numpy-only callable (the reference's convention): evaluate this chunk on the host
+        pass
+    Xh, Yh, Zh = (t.cpu().numpy() for t in (X, Y, Z))
+    v = np.broadcast_to(np.asarray(fn(Xh, Yh, Zh), dtype=np.float64), shape)
+    return torch.from_numpy(np.ascontiguousarray(v)).cuda()
 
-    k, n, h = hier.degree, hier.n_cells(level), hier.h(level)
-    K = k + 1
-    rule = gauss_rule(quad_points or (k + 2))
-    q = len(rule.points)
-    S = lagrange_values(hier.basis.nodes, rule.points)
-    ax = _axis_points(hier, level, rule.points)
-    vals = np.broadcast_to(np.asarray(f(*_coords(ax)), dtype=np.float64), (n * q,) * 3) * _weights(hier, level, rule)
-    b = _cells_back(_contract_last3(_cells_view(vals, n, q), [S.T] * 3), n, K)
+
+def _eval_chunk_vec(fn, X, Y, Z, shape):
+    """a vector-valued callable (the gradient): 3 components as CUDA tensors."""
+    try:
+        v = fn(X, Y, Z)
+        if all(isinstance(c, torch.Tensor) and c.is_cuda for c in v):
+            return [c.to(torch.float64).expand(shape).contiguous() for c in v]
+    except Exception:
+        pass
+    Xh, Yh, Zh = (t.cpu().numpy() for t in (X, Y, Z))
+    return [torch.from_numpy(np.ascontiguousarray(np.broadcast_to(np.asarray(c, dtype=np.float64), shape))).cuda()
+            for c in fn(Xh, Yh, Zh)]
+
+
+class _QuadLevel:
+    """Gauss rule, evaluation matrices and device copies for one (level, q)."""
+
+    def __init__(self, hier, level, q):
+        from .basis import gauss_rule, lagrange_derivatives, lagrange_values
+
+        self.n, self.h, self.K, self.k = hier.n_cells(level), hier.h(level), hier.degree + 1, hier.degree
+        self.rule = gauss_rule(q)
+        self.q = q
+        self.S = lagrange_values(hier.basis.nodes, self.rule.points)             # (q, K)
+        self.D = lagrange_derivatives(hier.basis.nodes, self.rule.points) / self.h
+        self.ax = _axis_points(hier, level, self.rule.points)                    # (n q,)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+        self.ax_d = cu(self.ax)
+        self.w_d = cu(np.tile(self.rule.weights, self.n) * self.h)
+        self.ST_d = cu(self.S.T)
+        self.mats_d = {None: cu(np.concatenate([self.S.ravel()] * 3))}
+        for a in range(3):
+            self.mats_d[a] = cu(np.concatenate([(self.D if b == a else self.S).ravel() for b in range(3)]))
+
+    def chunk_cells(self, limit_points=1 << 27):
+        return max(1, limit_points // ((self.n * self.q) ** 2 * self.q))
+
+    def coords(self, z0, nz):
+        nq = self.n * self.q
+        X = self.ax_d.view(1, 1, nq)
+        Y = self.ax_d.view(1, nq, 1)
+        Z = self.ax_d[z0 * self.q:(z0 + nz) * self.q].view(nz * self.q, 1, 1)
+        return X, Y, Z, (nz * self.q, nq, nq)
+
+
+def _zrange(hier, level, z_cells):
+    n = hier.n_cells(level)
+    z0, nz = (0, n) if z_cells is None else (int(z_cells[0]), int(z_cells[1]))
+    if z0 < 0 or nz < 1 or z0 + nz > n:
+        raise ValueError(f"z-cell range {z_cells} outside [0, {n})")
+    return z0, nz
+
+
+def assemble_rhs_device(hier: MeshHierarchy, level: int, f, g=None, quad_points: int | None = None,
+                        z_cells=None) -> torch.Tensor:
+    """Load vector (discretization.py:317-394) on the device: cell integrals of f v by sf_quad_load, the
+    Nitsche data terms of g by sf_face_load.  z_cells = (z0, nz): only that z-slab of cells (slab-local
+    vector, what a multi-GPU rank owns); default the whole level."""
+    from .basis import lagrange_derivatives, lagrange_values, penalty
+
+    device.require_cuda()
+    k = hier.degree
+    Q = _QuadLevel(hier, level, quad_points or (k + 2))
+    n, K, q = Q.n, Q.K, Q.q
+    z0, nz = _zrange(hier, level, z_cells)
+    b = torch.empty(nz * K * (n * K) ** 2, dtype=torch.float64, device="cuda")
+    L = _native.lib()
+    step = Q.chunk_cells()
+    layer = K * (n * K) ** 2
+    for c0 in range(z0, z0 + nz, step):
+        c1 = min(c0 + step, z0 + nz)
+        X, Y, Z, shape = Q.coords(c0, c1 - c0)
+        fq = _eval_chunk(f, X, Y, Z, shape)
+        rc = L.sf_quad_load(k, q, n, c0, c1 - c0, device.ptr(fq), device.ptr(Q.ST_d), device.ptr(Q.w_d),
+                            device.ptr(b) + (c0 - z0) * layer * 8, device.stream_ptr())
+        _native.check(rc, "sf_quad_load")
     if g is not None:
-        nodes = hier.basis.nodes
+        nodes, h = hier.basis.nodes, Q.h
         gamma = penalty(k, h, h)
         coef = {0: gamma * lagrange_values(nodes, [0.0])[0] + lagrange_derivatives(nodes, [0.0])[0] / h,
                 1: gamma * lagrange_values(nodes, [1.0])[0] - lagrange_derivatives(nodes, [1.0])[0] / h}
-        wa = np.tile(rule.weights, n) * h
-        for a in range(3):
-            d_np = 2 - a
+        nq = n * q
+        A = Q.ax_d
+        for a in range(3):  # tensor axis of the face normal
             for side in (0, 1):
-                t1, t2 = [np.meshgrid(ax, ax, indexing="ij")[i] for i in (0, 1)]
-                coords = [None, None, None]
-                tang = sorted([bb for bb in range(3) if bb != a], reverse=True)
-                coords[tang[0]], coords[tang[1]] = t1, t2
-                coords[a] = np.full_like(t1, float(side))
-                gv = np.broadcast_to(np.asarray(g(*coords), dtype=np.float64), (n * q, n * q))
-                gv = gv * wa[:, None] * wa[None, :]
-                w2 = np.ascontiguousarray(gv.reshape(n, q, n, q).transpose(0, 2, 1, 3))
-                w2 = np.einsum("ik,...k->...i", S.T, w2)
-                w2 = np.einsum("ik,...kx->...ix", S.T, w2)
-                tan = w2.transpose(0, 2, 1, 3).reshape(n * K, n * K)
-                sl = [slice(None)] * 3
-                sl[d_np] = slice(0, K) if side == 0 else slice(n * K - K, None)
-                cshape = [1, 1, 1]
-                cshape[d_np] = K
-                tshape = list(tan.shape)
-                tshape.insert(d_np, 1)
-                b[tuple(sl)] += coef[side].reshape(cshape) * tan.reshape(tshape)
-    return b.reshape(-1)
+                if a == 2 and not (z0 <= (0 if side == 0 else n - 1) < z0 + nz):
+                    continue  # z face outside this slab
+                pin = torch.full((1, 1), float(side), dtype=torch.float64, device="cuda")
+                slow, fast = A.view(nq, 1), A.view(1, nq)  # face grid (slow, fast) = tangential axes (z|y, y|x)
+                if a == 0:
+                    gv = _eval_chunk(g, pin, fast, slow, (nq, nq))
+                elif a == 1:
+                    gv = _eval_chunk(g, fast, pin, slow, (nq, nq))
+                else:
+                    gv = _eval_chunk(g, fast, slow, pin, (nq, nq))
+                cf = torch.from_numpy(np.ascontiguousarray(coef[side], dtype=np.float64)).cuda()
+                rc = L.sf_face_load(k, q, n, z0, nz, a, side, device.ptr(gv), device.ptr(Q.ST_d),
+                                    device.ptr(Q.w_d), device.ptr(cf), device.ptr(b), device.stream_ptr())
+                _native.check(rc, "sf_face_load")
+    return b
+
+
+def _quad_error_sq(hier, level, u_h: torch.Tensor, fn, deriv_axis, quad_points, z_cells, vector=False):
+    """device scalar: sum over the z-slab of w (I u_h - fn)^2 (per gradient component when vector)."""
+    k = hier.degree
+    Q = _QuadLevel(hier, level, quad_points or (k + 3))
+    n, K, q = Q.n, Q.K, Q.q
+    z0, nz = _zrange(hier, level, z_cells)
+    u = u_h.reshape(-1)
+    if u.numel() != nz * K * (n * K) ** 2:
+        raise ValueError(f"expected {nz * K * (n * K) ** 2} entries, got {u.numel()}")
+    u = u.to(torch.float64).contiguous()
+    L = _native.lib()
+    step = Q.chunk_cells()
+    layer = K * (n * K) ** 2
+    part = torch.empty(n * n * step, dtype=torch.float64, device="cuda")
+    total = torch.zeros(1, dtype=torch.float64, device="cuda")
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    axes = (0, 1, 2) if vector else (deriv_axis,)
+    for c0 in range(z0, z0 + nz, step):
+        c1 = min(c0 + step, z0 + nz)
+        X, Y, Z, shape = Q.coords(c0, c1 - c0)
+        vals = _eval_chunk_vec(fn, X, Y, Z, shape) if vector else [_eval_chunk(fn, X, Y, Z, shape)]
+        for a, fq in zip(axes, vals):
+            rc = L.sf_quad_error(k, q, n, c0, c1 - c0, device.ptr(u) + (c0 - z0) * layer * 8,
+                                 device.ptr(Q.mats_d[a]), device.ptr(fq), device.ptr(Q.w_d), device.ptr(part),
+                                 device.ptr(out), device.stream_ptr())
+            _native.check(rc, "sf_quad_error")
+            total += out
+    return total
+
+
+def l2_error_device(hier: MeshHierarchy, level: int, u_h, exact, quad_points: int | None = None,
+                    z_cells=None) -> torch.Tensor:
+    """Sum of squares of the L2 error over a z-slab (device scalar; sqrt of the all-slab sum = l2_error)."""
+    return _quad_error_sq(hier, level, device.as_device(u_h, torch.float64)[0], exact, None, quad_points, z_cells)
+
+
+def h1_error_device(hier: MeshHierarchy, level: int, u_h, grad_exact, quad_points: int | None = None,
+                    z_cells=None) -> torch.Tensor:
+    """Sum of squares of the broken H1-seminorm error over a z-slab (device scalar)."""
+    return _quad_error_sq(hier, level, device.as_device(u_h, torch.float64)[0], grad_exact, None, quad_points,
+                          z_cells, vector=True)
+
+
+def assemble_rhs(hier: MeshHierarchy, level: int, f, g=None, quad_points: int | None = None) -> np.ndarray:
+    """Load vector: cell integrals of f v (+ Nitsche data terms for g), discretization.py:317-394.
+    Computed on the device (assemble_rhs_device); returned as numpy like the reference."""
+    return assemble_rhs_device(hier, level, f, g, quad_points).cpu().numpy()
 
 
 def interpolate(hier: MeshHierarchy, level: int, func) -> np.ndarray:
@@ -370,40 +478,14 @@ def interpolate(hier: MeshHierarchy, level: int, func) -> np.ndarray:
     return np.broadcast_to(np.asarray(func(*_coords(ax)), dtype=np.float64), hier.shape(level)).reshape(-1).copy()
 
 
-def _qvalues(hier, level, u, pts, deriv_axis=None):
-    from .basis import lagrange_derivatives, lagrange_values
-
-    n, h, K = hier.n_cells(level), hier.h(level), hier.degree + 1
-    S = lagrange_values(hier.basis.nodes, pts)
-    D = lagrange_derivatives(hier.basis.nodes, pts) / h
-    uh = u.detach().double().cpu().numpy() if isinstance(u, torch.Tensor) else np.asarray(u, dtype=np.float64)
-    w = _cells_view(uh.reshape(hier.shape(level)), n, K)
-    return _cells_back(_contract_last3(w, [D if deriv_axis == a else S for a in range(3)]), n, len(pts))
-
-
 def l2_error(hier: MeshHierarchy, level: int, u_h, exact, quad_points: int | None = None) -> float:
-    """discretization.py:431-441."""
-    from .basis import gauss_rule
-
-    rule = gauss_rule(quad_points or (hier.degree + 3))
-    ax = _axis_points(hier, level, rule.points)
-    diff = _qvalues(hier, level, u_h, rule.points) - exact(*_coords(ax))
-    return float(math.sqrt(np.sum(_weights(hier, level, rule) * diff**2)))
+    """L2 distance between a DoF vector and a callable (discretization.py:431-441), on the device."""
+    return float(torch.sqrt(l2_error_device(hier, level, u_h, exact, quad_points)))
 
 
 def h1_seminorm_error(hier: MeshHierarchy, level: int, u_h, grad_exact, quad_points: int | None = None) -> float:
-    """discretization.py:444-459."""
-    from .basis import gauss_rule
-
-    rule = gauss_rule(quad_points or (hier.degree + 3))
-    ax = _axis_points(hier, level, rule.points)
-    W = _weights(hier, level, rule)
-    grads = grad_exact(*_coords(ax))
-    total = 0.0
-    for a in range(3):
-        c = _qvalues(hier, level, u_h, rule.points, deriv_axis=a) - np.asarray(grads[a], float)
-        total += float(np.sum(W * c**2))
-    return math.sqrt(total)
+    """Broken H1-seminorm distance (discretization.py:444-459), on the device."""
+    return float(torch.sqrt(h1_error_device(hier, level, u_h, grad_exact, quad_points)))
 
 
 
@@ -481,11 +563,15 @@ def _rhs_1d(hier, level, f1, q):
     return (vals @ S).reshape(n * K)  # (n*K,)
 
 
-def assemble_rhs_separable(hier: MeshHierarchy, level: int, f1, scale: float = 1.0) -> torch.Tensor:
-    """Load vector of f = scale * f1(x) f1(y) f1(z) on the device (fp64, flat (z,y,x))."""
+def assemble_rhs_separable(hier: MeshHierarchy, level: int, f1, scale: float = 1.0, z_cells=None) -> torch.Tensor:
+    """Load vector of f = scale * f1(x) f1(y) f1(z) on the device (fp64, flat (z,y,x)); z_cells = (z0, nz):
+    only that z-slab of cells (O(local DoF) memory on a multi-GPU rank)."""
     device.require_cuda()
     b1 = torch.from_numpy(_rhs_1d(hier, level, f1, hier.degree + 2)).cuda()
-    return (scale * b1[:, None, None] * b1[None, :, None] * b1[None, None, :]).reshape(-1).contiguous()
+    z0, nz = _zrange(hier, level, z_cells)
+    K = hier.degree + 1
+    bz = b1[z0 * K:(z0 + nz) * K]
+    return (scale * bz[:, None, None] * b1[None, :, None] * b1[None, None, :]).reshape(-1).contiguous()
 
 
 def _separable_error_sq(hier, level, u_h, mats, factors, slab_cells=8, nz=None):

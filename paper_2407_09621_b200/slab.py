@@ -427,7 +427,7 @@ def run_solve_distributed(degree: int, level: int, comm: SlabComm, mode: Precisi
     op = DistributedOperator(hier, level, comm)
     sl = mg.slabs[level]
     sine = lambda x: np.sin(np.pi * x)
-    b = assemble_rhs_separable(hier, level, sine, 3.0 * math.pi**2)[sl.global_slice].contiguous()
+    b = assemble_rhs_separable(hier, level, sine, 3.0 * math.pi**2, z_cells=(sl.z0, sl.nz))  # slab-local
     x, rep = fgmres_distributed(op, mg, b, comm, tol=tol, maxit=maxit)
     # L2 error: the separable quadrature over this rank's z cells, all-reduced
     rule = gauss_rule(hier.degree + 3)

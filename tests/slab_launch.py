@@ -16,12 +16,12 @@ def free_port():
     return p
 
 
-def run(world, *args, timeout=600):
+def run(world, *args, timeout=600, one_gpu_per_rank=False):
     port = free_port()
     procs = []
     for r in range(world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                   LOCAL_RANK="0")
+                   LOCAL_RANK=str(r) if one_gpu_per_rank else "0")
         procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "slab_worker.py"), *map(str, args)],
                                       env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     results = {}

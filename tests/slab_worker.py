@@ -64,7 +64,7 @@ def gpu_case(args):
     from paper_2407_09621_b200 import slab
     from paper_2407_09621_b200.discretization import vmult_device
 
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(args.device)
     comm = slab.SlabComm()
     r = comm.rank
     k, L = args.degree, args.level
@@ -128,6 +128,26 @@ def gpu_case(args):
     return out
 
 
+def memory_case(args):
+    """Peak device memory of one rank's distributed solve (O(local DoF): slab-local load vector, slab
+    V-cycle buffers, slab Krylov bases; only the agglomerated coarse levels are replicated)."""
+    import paper_2407_09621_b200 as sf
+    from paper_2407_09621_b200 import slab
+
+    torch.cuda.set_device(args.device)
+    comm = slab.SlabComm()
+    k, L = args.degree, args.level
+    hier = sf.build_hierarchy(L, k, max_dofs=2**30)
+    mode = sf.PrecisionMode.parse(args.mode)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    _, rep, l2 = slab.run_solve_distributed(k, L, comm, mode=mode, hier=hier)
+    torch.cuda.synchronize()
+    return {"rank": comm.rank, "peak_bytes": torch.cuda.max_memory_allocated() - base, "its": rep.iterations,
+            "l2": l2, "global_dofs": hier.n_dofs(L)}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", default="host")
@@ -135,9 +155,16 @@ if __name__ == "__main__":
     ap.add_argument("--level", type=int, default=3)
     ap.add_argument("--mode", default="fp64")
     ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--backend", default="gloo")
     a = ap.parse_args()
-    dist.init_process_group("gloo")
-    res = host_case(a) if a.case == "host" else gpu_case(a)
+    a.device = 0
+    if a.backend == "nccl":  # one GPU per rank (the driver's multi-GPU boxes)
+        a.device = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(a.device)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", a.device))
+    else:
+        dist.init_process_group("gloo")
+    res = {"host": host_case, "gpu": gpu_case, "memory": memory_case}[a.case](a)
     print("RESULT " + json.dumps(res), flush=True)
     dist.barrier()
     dist.destroy_process_group()

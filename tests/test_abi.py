@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     lib.sf_abi_version.restype = ctypes.c_int
     from paper_2407_09621_b200 import _native
 
-    assert lib.sf_abi_version() == _native.ABI_VERSION == 2
+    assert lib.sf_abi_version() == _native.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_only():

@@ -38,3 +38,26 @@ def test_distributed_fgmres_solve_matches_single_gpu(world, k, lvl, mode):
         # rounding-level differences of the slab V-cycle)
         tol = 1e-6 if mode == "fp64" else 1e-2
         assert abs(r["run_solve_dist_l2"] - r["run_solve_l2"]) <= tol * r["run_solve_l2"], r
+
+
+def test_distributed_solve_memory_is_slab_local():
+    """Per-rank device memory of the distributed solve is O(local DoF): at 2 ranks each rank's peak is
+    well below the 1-rank peak (the global load vector used to be built on every rank)."""
+    one = run(1, "--case", "memory", "--degree", 3, "--level", 6, "--mode", "fp64")[0]
+    two = run(2, "--case", "memory", "--degree", 3, "--level", 6, "--mode", "fp64")
+    for r in two:
+        assert r["its"] == one["its"], (r, one)
+        assert r["peak_bytes"] <= 0.62 * one["peak_bytes"], (r["peak_bytes"], one["peak_bytes"])
+
+
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2, reason="needs >= 2 GPUs (NCCL over NVLink)")
+@pytest.mark.parametrize("world,k,lvl,mode", [(2, 7, 4, "fp64"), (2, 7, 4, "fp16_ec")])
+def test_nccl_one_gpu_per_rank(world, k, lvl, mode):
+    """The NCCL branch of SlabComm (batch_isend_irecv halos on NCCL's stream, all-reduced dots) with one
+    GPU per rank, as the driver's multi-GPU run uses it."""
+    world = min(world, __import__("torch").cuda.device_count())
+    res = run(world, "--case", "gpu", "--degree", k, "--level", lvl, "--mode", mode, "--solve", "--backend", "nccl",
+              one_gpu_per_rank=True)
+    for r in res:
+        assert r["vmult_rel_err"] <= 1e-14, r
+        assert r["its_dist"] == r["its_single"], r

@@ -182,6 +182,26 @@ def error_profiles():
     print(f"wrote {path}", flush=True)
 
 
+def quadrature():
+    """Pre/post-processing with general (non-separable) data: assemble_rhs with a boundary term g,
+    l2_error and h1_seminorm_error of a seeded DoF vector (discretization.py:317-459)."""
+    from sumfact.discretization import assemble_rhs, h1_seminorm_error, l2_error
+
+    f = lambda x, y, z: np.exp(x) * np.cos(2.0 * y + z) + x * y * z
+    g = lambda x, y, z: np.sin(3.0 * x + y) - z * z + 0.5
+    ex = lambda x, y, z: np.cos(x * y) + np.exp(z) * x
+    gr = lambda x, y, z: (-y * np.sin(x * y) + np.exp(z), -x * np.sin(x * y), np.exp(z) * x)
+    out = {}
+    for k, lvl in [(1, 2), (2, 2), (3, 2), (7, 1), (7, 2)]:
+        hier = build_hierarchy(lvl, k)
+        out[f"k{k}_l{lvl}_rhs_f"] = assemble_rhs(hier, lvl, f)
+        out[f"k{k}_l{lvl}_rhs_fg"] = assemble_rhs(hier, lvl, f, g)
+        u = np.random.default_rng(5).standard_normal(hier.n_dofs(lvl))
+        out[f"k{k}_l{lvl}_l2"] = np.array(l2_error(hier, lvl, u, ex))
+        out[f"k{k}_l{lvl}_h1"] = np.array(h1_seminorm_error(hier, lvl, u, gr))
+    save("quadrature", **out)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     globals()[sys.argv[1]]()
     sys.exit(0)
