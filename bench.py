@@ -362,6 +362,9 @@ def main():
         dist.destroy_process_group()
 
 
+SOLVE_KEYS = ("iterations", "solve_s", "solve_s_min", "solve_s_max", "solves_timed", "setup_s", "l2_error")
+
+
 def extras(sf, hier, lvl, k, u, v):
     """Secondary measurements of the other configs (FP16 paths, Q3, smoother, solve)."""
     import torch
@@ -413,13 +416,17 @@ def extras(sf, hier, lvl, k, u, v):
         from bench_solve import solve_once
 
         for mode in (P.FP64, P.FP16_EC):
-            r = solve_once(h6, 6, mode, reps=2)
-            res[f"solve_q{k}_l6_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
+            r = solve_once(h6, 6, mode, reps=5)
+            res[f"solve_q{k}_l6_{mode.value}"] = {kk: r[kk] for kk in SOLVE_KEYS}
         del h6
         h37 = sf.build_hierarchy(7, 3, max_dofs=2**34)  # Q3 level 7: the other 1.34e8-DoF solve config
         for mode in (P.FP64, P.FP16_EC):
-            r = solve_once(h37, 7, mode, reps=2)
-            res[f"solve_q3_l7_{mode.value}"] = {kk: r[kk] for kk in ("iterations", "solve_s", "setup_s", "l2_error")}
+            r = solve_once(h37, 7, mode, reps=5)
+            res[f"solve_q3_l7_{mode.value}"] = {kk: r[kk] for kk in SOLVE_KEYS}
+        for cfg in ("q7_l6", "q3_l7"):  # mixed-precision speed-up at the same tolerance (BASELINE configs[3])
+            a, b = res.get(f"solve_{cfg}_fp64"), res.get(f"solve_{cfg}_fp16_ec")
+            if a and b:
+                res[f"solve_{cfg}_fp16_ec_speedup_vs_fp64"] = a["solve_s"] / b["solve_s"]
     except Exception as exc:  # secondary measurement only
         res["solve_error"] = repr(exc)[:200]
     return res

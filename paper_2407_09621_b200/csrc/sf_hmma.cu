@@ -63,6 +63,22 @@ constexpr int SM_XST = SM_TR + 12 * PLS * 4;      // [hi][256 rows][KK <= 8] f32
 constexpr int SM_EXP_A = SM_HALO + 3 * 256 * 16, SM_EXP_B = SM_XST + 2 * 256 * 8 * 4;
 constexpr int SM_EXP = SM_EXP_A > SM_EXP_B ? SM_EXP_A : SM_EXP_B;
 constexpr int kSmem = SM_EXP + 16;
+// tcgen05 (UMMA) kernels: two operand buffers P0 / P1, each a binary16 main-half tensor and (at + UM_D)
+// the EC residual-half tensor in canonical no-swizzle layouts; halo words, operator B tables, the
+// mbarrier, the TMEM base and the exponent words after them.  During the prologue P1 and the halo
+// region hold the f32 trace planes and the staged x-neighbour layers.
+constexpr int UM_MN_SBO = 144, UM_MN_LBO = 32 * UM_MN_SBO;  // MN-major: 9 x 16 B per 8-row group (bank spread)
+constexpr int UM_D = 2 * UM_MN_LBO;                          // 9216 B per tensor
+constexpr int UM_P0 = 0, UM_P1 = 2 * UM_D;
+constexpr int UM_HALO = 2 * UM_P1;                           // 36864: [axis][line 256] x 16 B
+constexpr int UM_TAB = UM_HALO + 3 * 256 * 16;               // B operands: [slot][h | d] x 512 B
+constexpr int UM_NOPS = 6;                                   // M, Lx, Ly, Lz, halo main, halo corr
+constexpr int UM_BAR = UM_TAB + UM_NOPS * 1024;              // mbarrier (8 B), TMEM base (4 B)
+constexpr int UM_EXP = UM_BAR + 16;
+constexpr int UM_TR = UM_P1;                                 // prologue: f32 trace planes (13 KB)
+constexpr int UM_XST = UM_TR + 12 * PLS * 4;                 // prologue: staged x layers (16 KB), over halo
+constexpr int kSmemU = UM_EXP + 16;
+static_assert(UM_XST + 2 * 256 * 8 * 4 <= UM_TAB, "prologue scratch must not reach the operator tables");
 
 __device__ __forceinline__ int hidx(int z, int y, int x) {
   return z * PZ + y * 16 + ((((x >> 3) ^ (y >> 2)) & 1) << 3) + (x & 7);
@@ -300,12 +316,15 @@ __device__ __forceinline__ void st_a(unsigned h, unsigned d, unsigned off, const
 //   [alpha_h lo, beta_h lo | alpha_h hi, beta_h hi | alpha_d lo, beta_d lo | alpha_d hi, beta_d hi]
 // (k rows of the halo MMA; see pack_halo).  A face writes its two 32-bit words (lo: 0, 2; hi: 1, 3).
 // fp16: alpha is a demoted operand (no residual half); beta keeps its residual half.
-template <int MODE>
+// ZT (tcgen05 kernels): the z-axis lines are ordered (x, y) -- line index q * 16 + p -- as the z stage's
+// MMA rows are.
+template <int MODE, bool ZT = false>
 __device__ __forceinline__ void put_face(char* sm, int axis, int p, int q, int hi, float alpha, float beta) {
   unsigned h, d;
   demote_pair<MODE_FP16_EC>(alpha, beta, h, d);
   if constexpr (MODE != MODE_FP16_EC) d &= 0xffff0000u;
-  unsigned* w = reinterpret_cast<unsigned*>(sm + SM_HALO + ((axis * 16 + p) * 16 + q) * 16);
+  const int line = (ZT && axis == 2) ? q * 16 + p : p * 16 + q;
+  unsigned* w = reinterpret_cast<unsigned*>(sm + (ZT ? UM_HALO : SM_HALO) + (axis * 256 + line) * 16);
   w[hi] = h;
   w[2 + hi] = d;
 }
@@ -314,7 +333,7 @@ __device__ __forceinline__ void put_face(char* sm, int axis, int p, int q, int h
 // pitch 17, A fragments gathered from shared memory with demotion).  along_p = false: mass along q
 // (row = p, k = q); true: along p (row = q, k = p).  to_halo: write the face's halo words, else the
 // f32 planes in place.
-template <int MODE>
+template <int MODE, bool ZT = false>
 __device__ __forceinline__ void face_mass(const HTile<MODE>& T, float* pa, bool along_p, bool to_halo, int axis,
                                           int hi, const HOpFrag& bm) {
   float o[2][2][4];  // [alpha / beta][nt][i]
@@ -345,7 +364,7 @@ __device__ __forceinline__ void face_mass(const HTile<MODE>& T, float* pa, bool 
       const int row = T.g + 8 * (i >> 1), n = 8 * nt + 2 * T.t + (i & 1);
       const int p = along_p ? n : row, qq = along_p ? row : n;
       if (to_halo) {
-        put_face<MODE>(T.sm, axis, p, qq, hi, o[0][nt][i], o[1][nt][i]);
+        put_face<MODE, ZT>(T.sm, axis, p, qq, hi, o[0][nt][i], o[1][nt][i]);
       } else {
         pa[p * PLP + qq] = o[0][nt][i];
         pa[PLS + p * PLP + qq] = o[1][nt][i];
@@ -375,20 +394,39 @@ __device__ __forceinline__ void line_trace(const float (&w)[KK], const float (&c
   alpha = (hi ? w[0] : w[KK - 1]) * us;
 }
 
+// linear tile id of the banded grid (ntx, by, zb [* batch]) -> tile coordinates (persistent CTAs)
+__device__ __forceinline__ bool band_tile_id(const Geom& g, const dm::Band& bd, int id, int& tx, int& ty, int& tz,
+                                             int& batch) {
+  tx = id % g.ntx;
+  const int r = id / g.ntx;
+  const int yy = r % bd.by;
+  int zz = r / bd.by;
+  batch = zz / bd.zb;
+  zz -= batch * bd.zb;
+  const int band = zz / g.ntz;
+  tz = zz - band * g.ntz;
+  ty = band * bd.by + yy;
+  return ty < g.nty;
+}
+
 // prologue + x/y stages; leaves c in U and dd in B (f16 tensors), halo words ready.
 // KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells).
 // Tile order: the banded 3-D grid of the FP64 kernels (dm::band_tile, no integer divisions).
-template <int MODE, int KK = K>
+template <int MODE, int KK = K, bool UM = false>
 __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const dm::Band& bd,
                                            const LevelOp<KK, MODE>& op, const HTables* tab, const float*& u,
-                                           int& batch, const float* __restrict__ pf = nullptr) {
+                                           int& batch, const float* __restrict__ pf = nullptr, int tile_id = -1) {
   constexpr int CPL = 16 / KK;
   int tx, ty, tz;
-  if (!dm::band_tile(g, bd, tx, ty, tz, batch)) return false;
+  if (tile_id < 0) {
+    if (!dm::band_tile(g, bd, tx, ty, tz, batch)) return false;
+  } else if (!band_tile_id(g, bd, tile_id, tx, ty, tz, batch)) {
+    return false;
+  }
   u += (long long)batch * g.batch_stride;
   T.sm = smem;
   T.s0 = smem_u32(smem);
-  T.s_exp = reinterpret_cast<int*>(smem + SM_EXP);
+  T.s_exp = reinterpret_cast<int*>(smem + (UM ? UM_EXP : SM_EXP));
   T.cx = g.tx0 + CPL * tx;
   T.cy = g.ty0 + CPL * ty;
   T.cz = g.tz0 + CPL * tz;
@@ -433,8 +471,8 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
     asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p + 8 * (long long)sz));
   }
-  float* tr = reinterpret_cast<float*>(smem + SM_TR);   // f32 trace planes [face][alpha/beta][16][17]
-  float* xs = reinterpret_cast<float*>(smem + SM_XST);  // staged x-neighbour rows [hi][row 256][KK]
+  float* tr = reinterpret_cast<float*>(smem + (UM ? UM_TR : SM_TR));   // f32 trace planes [face][a/b][16][17]
+  float* xs = reinterpret_cast<float*>(smem + (UM ? UM_XST : SM_XST));  // staged x-neighbour rows [hi][256][KK]
   // (1) x-neighbour cell layers -> shared memory by cp.async (coalesced 16-byte chunks; a per-lane load
   //     of a row's KK contiguous values would touch a different cache line per lane)
   constexpr bool kStageX = KK >= 4;
@@ -514,9 +552,15 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     uint2 hv, dv;
     demote_pair<MODE>(q4[k2].x * us, q4[k2].y * us, hv.x, dv.x);
     demote_pair<MODE>(q4[k2].z * us, q4[k2].w * us, hv.y, dv.y);
-    const int o = hidx(z, y, x4);
-    *reinterpret_cast<uint2*>(uh + o) = hv;
-    if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(ud + o) = dv;
+    if constexpr (UM) {  // tcgen05: the x stage's K-major canonical A layout (sf_hmma.cu, UMMA section)
+      const int o = ((z * 2 + (y >> 3)) * 256 + (x4 >> 3) * 128 + (y & 7) * 16 + (x4 & 7) * 2);
+      *reinterpret_cast<uint2*>(smem + UM_P0 + o) = hv;
+      if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(smem + UM_P0 + UM_D + o) = dv;
+    } else {
+      const int o = hidx(z, y, x4);
+      *reinterpret_cast<uint2*>(uh + o) = hv;
+      if constexpr (MODE == MODE_FP16_EC) *reinterpret_cast<uint2*>(ud + o) = dv;
+    }
   }
   // (3) y traces -> planes (faces 2, 3)
   auto traces_out = [&](const float (&w)[KK][VW], int face, int p, int q0, int hi) {
@@ -610,18 +654,18 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     const int axis = 1 + (T.warp >> 1), hi = T.warp & 1, f = 2 * axis + hi;
     float* pa = tr + (2 * f) * PLS;
     if ((T.nbm >> f) & 1) {
-      face_mass<MODE>(T, pa, false, axis == 1, axis, hi, bm);
+      face_mass<MODE, UM>(T, pa, false, axis == 1, axis, hi, bm);
     } else if (axis == 1) {
-      for (int i = T.lane; i < 256; i += 32) put_face<MODE>(smem, 1, i >> 4, i & 15, hi, 0.f, 0.f);
+      for (int i = T.lane; i < 256; i += 32) put_face<MODE, UM>(smem, 1, i >> 4, i & 15, hi, 0.f, 0.f);
     }
   }
   __syncthreads();
   if (T.warp >= 2) {
     const int hi = T.warp & 1, f = 4 + hi;
     if ((T.nbm >> f) & 1) {
-      face_mass<MODE>(T, tr + (2 * f) * PLS, true, true, 2, hi, bm);
+      face_mass<MODE, UM>(T, tr + (2 * f) * PLS, true, true, 2, hi, bm);
     } else {
-      for (int i = T.lane; i < 256; i += 32) put_face<MODE>(smem, 2, i >> 4, i & 15, hi, 0.f, 0.f);
+      for (int i = T.lane; i < 256; i += 32) put_face<MODE, UM>(smem, 2, i >> 4, i & 15, hi, 0.f, 0.f);
     }
   } else {
     const int hi = T.warp & 1;
@@ -629,8 +673,13 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     const float* pa = tr + (2 * hi) * PLS;
     for (int i = T.lane; i < 256; i += 32) {
       const int p = i >> 4, qq = i & 15;
-      put_face<MODE>(smem, 0, p, qq, hi, on ? pa[p * PLP + qq] : 0.f, on ? pa[PLS + p * PLP + qq] : 0.f);
+      put_face<MODE, UM>(smem, 0, p, qq, hi, on ? pa[p * PLP + qq] : 0.f, on ? pa[PLS + p * PLP + qq] : 0.f);
     }
+  }
+  if constexpr (UM) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // u split + halo words -> tensor core
+    __syncthreads();
+    return true;
   }
   __syncthreads();
 
@@ -932,6 +981,287 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
 }
 
 
+// ================================================================ tcgen05 (UMMA) kernels
+// The same cell-wise schedule on the 5th-generation tensor cores: one elected thread issues
+// tcgen05.mma.kind::f16 (M = 128 lines, N = 16 outputs, K = 16 line points, f32 accumulators in
+// TMEM); every thread then owns TMEM lane = one line of the M block, reads its 16 outputs with
+// tcgen05.ld, combines EC main + corr / 2048, splits to binary16 and writes the line straight into the
+// NEXT stage's operand layout.  No A/B fragments or accumulators live in registers, so the per-DoF
+// instruction stream is the binary16 arithmetic itself.  Operand layouts (canonical, no swizzle;
+// byte offsets, m = MMA row, k = line point):
+//   x stage  A[m = z*16 + y][k = x]   K-major : (m/8)*256 + (k/8)*128 + (m%8)*16 + (k%8)*2  (LBO 128, SBO 256)
+//   y stage  A[m = z*16 + x][k = y]   MN-major: (m/8)*128 + (k/8)*4096 + (k%8)*16 + (m%8)*2  (SBO 128, LBO 4096)
+//   z stage  A[m = x*16 + y][k = z]   MN-major: same formula
+//   halo     A[m = line][k = 0..7 | repeated]  K-major, 16 B per line (SBO 128, LBO 0 -> B rows 8..15 are 0)
+//   B = Op^T  K-major over n: (n/8)*256 + (k/8)*128 + (n%8)*16 + (k%8)*2
+// A line's 16 outputs are always 8-element contiguous runs of the next stage's M dimension, so each
+// thread writes 16-byte rows.  One tile (16^3 points) per CTA, 128 threads = 128 TMEM lanes, 2 M blocks.
+namespace um {
+
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
+}
+// kind::f16, f16 x f16 -> f32, M = 128, N = 16, A K-major (0) or MN-major (1), B K-major
+__host__ __device__ constexpr uint32_t idesc(int a_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t dt, uint64_t a, uint64_t b, uint32_t id, int acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void wait(uint32_t bar, uint32_t phase) {
+  // suspend-time hint: the waiting warps sleep in the instruction instead of spinning on issue slots
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n @!p bra W;\n}\n"
+      ::"r"(bar), "r"(phase)
+      : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// 16 consecutive f32 columns of this thread's lane
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// accumulator pair (main, corr) of one line -> f32 values (main + corr / 2048 for EC)
+template <int MODE>
+__device__ __forceinline__ void line_vals(uint32_t tcol, float (&v)[16]) {
+  ld16(tcol, v);
+  if constexpr (MODE == MODE_FP16_EC) {
+    float c[16];
+    ld16(tcol + 16, c);
+    ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaf(c[i], kInvEc, v[i]);
+  } else {
+    ld_wait();
+  }
+}
+
+// one line's 16 values -> binary16 (h, d) halves -> two 16-byte rows of an operand buffer
+// (elements 0..7 at byte offset o0, 8..15 at o1 within the buffer)
+// swap: this lane stores its second run first (lanes whose runs are 2 groups apart then fall on different
+// bank quads within one STS.128 wavefront, with the 144-byte group stride)
+template <int MODE>
+__device__ __forceinline__ void put_line(char* buf, int o0, int o1, const float (&v)[16], bool swap = false) {
+  uint4 h0, h1, d0, d1;
+  demote_pair<MODE>(v[0], v[1], h0.x, d0.x);
+  demote_pair<MODE>(v[2], v[3], h0.y, d0.y);
+  demote_pair<MODE>(v[4], v[5], h0.z, d0.z);
+  demote_pair<MODE>(v[6], v[7], h0.w, d0.w);
+  demote_pair<MODE>(v[8], v[9], h1.x, d1.x);
+  demote_pair<MODE>(v[10], v[11], h1.y, d1.y);
+  demote_pair<MODE>(v[12], v[13], h1.z, d1.z);
+  demote_pair<MODE>(v[14], v[15], h1.w, d1.w);
+  const int oa = swap ? o1 : o0, ob = swap ? o0 : o1;
+  *reinterpret_cast<uint4*>(buf + oa) = swap ? h1 : h0;
+  *reinterpret_cast<uint4*>(buf + ob) = swap ? h0 : h1;
+  if constexpr (MODE == MODE_FP16_EC) {
+    *reinterpret_cast<uint4*>(buf + UM_D + oa) = swap ? d1 : d0;
+    *reinterpret_cast<uint4*>(buf + UM_D + ob) = swap ? d0 : d1;
+  }
+}
+// MN-major operand offsets of row k (the line point of the next stage) for the M runs mg0, mg0 + 1
+__device__ __forceinline__ int mn_off(int mg, int k) { return mg * UM_MN_SBO + (k >> 3) * UM_MN_LBO + (k & 7) * 16; }
+
+// D += A B for one operator (EC: main <- Ah Bh, corr <- Ah Bd + Ad Bh); a_mn: A MN-major
+template <int MODE>
+__device__ __forceinline__ void op_mma(uint32_t dt, uint64_t ah, uint64_t ad, uint64_t bh, uint64_t bd, int a_mn,
+                                       int acc) {
+  const uint32_t id = idesc(a_mn);
+  mma(dt, ah, bh, id, acc);
+  if constexpr (MODE == MODE_FP16_EC) {
+    mma(dt + 16, ah, bd, id, acc);
+    mma(dt + 16, ad, bh, id, 1);
+  }
+}
+
+struct UTabOp {
+  unsigned short h[256];
+  unsigned short d[256];
+};
+// device table of one level: B operands in the canonical layout
+struct UTab {
+  UTabOp M, L[4], Vf[4], Vb[4], halo[2];  // halo[0] main rows, halo[1] corr rows
+};
+
+}  // namespace um
+
+// tcgen05 vmult, Q7 2-cell tiles; persistent CTAs (TMEM, mbarrier and operator tables set up once)
+// looping over the banded tile order.  TMEM: 128 columns = 2 M blocks x (2 accumulator pairs x 32).
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_vmult_u8(const float* __restrict__ u, float* __restrict__ v, Geom g,
+                                                         dm::Band bd, LevelOp<8, MODE> op,
+                                                         const HTables* __restrict__ tab,
+                                                         const um::UTab* __restrict__ ut, int ntiles) {
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(smem + UM_BAR + 8);
+  const uint32_t bar = smem_u32(smem + UM_BAR);
+  if (tid < 32) {  // warp 0: TMEM allocation
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tm = *tbase;
+  const uint32_t s0 = smem_u32(smem);
+  const uint32_t tb = s0 + UM_TAB;
+  auto bdesc = [&](int slot, int dpart) { return um::desc(tb + slot * 1024 + dpart * 512, 128, 256); };
+  const uint32_t lane_t = tm + ((uint32_t)(tid & ~31) << 16);  // this warp's TMEM lanes
+  uint32_t phase = 0;
+  int kinds_loaded = -1;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    HTile<MODE> T;
+    int batch;
+    const float* uin = u;
+    if (!tile_front<MODE, 8, true>(T, smem, g, bd, op, tab, uin, batch, nullptr, tile)) continue;
+    // operator B tables of this tile's kinds -> shared memory (slots: M, Lx, Ly, Lz, halo main, halo corr)
+    const int kk = T.kind[0] * 16 + T.kind[1] * 4 + T.kind[2];
+    if (kk != kinds_loaded) {  // uniform across the CTA
+      const um::UTabOp* src[6] = {&ut->M, &ut->L[T.kind[0]], &ut->L[T.kind[1]], &ut->L[T.kind[2]], &ut->halo[0],
+                                  &ut->halo[1]};
+#pragma unroll
+      for (int sl = 0; sl < 6; ++sl)
+        if (tid < 64)
+          reinterpret_cast<uint4*>(smem + UM_TAB + sl * 1024)[tid] = __ldg(reinterpret_cast<const uint4*>(src[sl]) + tid);
+      kinds_loaded = kk;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+    }
+    // ---------------- x stage: a = Mx u (cols 0 | 64), b = Lx u + halo (cols 32 | 96)
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        const uint64_t ah = um::desc(s0 + UM_P0 + blk * 4096, 128, 256);
+        const uint64_t ad = um::desc(s0 + UM_P0 + UM_D + blk * 4096, 128, 256);
+        const uint64_t hh = um::desc(s0 + UM_HALO + blk * 2048, 0, 128);
+        um::op_mma<MODE>(tm + blk * 64, ah, ad, bdesc(0, 0), bdesc(0, 1), 0, 0);
+        um::op_mma<MODE>(tm + blk * 64 + 32, ah, ad, bdesc(1, 0), bdesc(1, 1), 0, 0);
+        um::mma(tm + blk * 64 + 32, hh, bdesc(4, 0), um::idesc(0), 1);
+        if (MODE == MODE_FP16_EC) um::mma(tm + blk * 64 + 48, hh, bdesc(5, 0), um::idesc(0), 1);
+      }
+      um::commit(bar);
+    }
+    um::wait(bar, phase);
+    phase ^= 1;
+    // line m = blk * 128 + tid = (z, y): outputs x -> y-stage A rows (m' = z*16 + x, k = y)
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const int m = blk * 128 + tid, z = m >> 4, y = m & 15;
+      float va[16], vb[16];
+      um::line_vals<MODE>(lane_t + blk * 64, va);
+      um::line_vals<MODE>(lane_t + blk * 64 + 32, vb);
+      const int o0 = um::mn_off(z * 2, y), o1 = um::mn_off(z * 2 + 1, y);
+      um::put_line<MODE>(smem + UM_P0, o0, o1, va);
+      um::put_line<MODE>(smem + UM_P1, o0, o1, vb);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    // ---------------- y stage: c = My a (cols 0 | 64), dd = Ly a + halo + My b (cols 32 | 96)
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        const uint64_t ah = um::desc(s0 + UM_P0 + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t ad = um::desc(s0 + UM_P0 + UM_D + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t bh_ = um::desc(s0 + UM_P1 + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t bd_ = um::desc(s0 + UM_P1 + UM_D + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t hh = um::desc(s0 + UM_HALO + 4096 + blk * 2048, 0, 128);
+        um::op_mma<MODE>(tm + blk * 64, ah, ad, bdesc(0, 0), bdesc(0, 1), 1, 0);
+        um::op_mma<MODE>(tm + blk * 64 + 32, ah, ad, bdesc(2, 0), bdesc(2, 1), 1, 0);
+        um::mma(tm + blk * 64 + 32, hh, bdesc(4, 0), um::idesc(0), 1);
+        if (MODE == MODE_FP16_EC) um::mma(tm + blk * 64 + 48, hh, bdesc(5, 0), um::idesc(0), 1);
+        um::op_mma<MODE>(tm + blk * 64 + 32, bh_, bd_, bdesc(0, 0), bdesc(0, 1), 1, 1);
+      }
+      um::commit(bar);
+    }
+    um::wait(bar, phase);
+    phase ^= 1;
+    // line m = (z, x): outputs y -> z-stage A rows (m'' = x*16 + y, k = z)
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const int m = blk * 128 + tid, z = m >> 4, x = m & 15;
+      float vc[16], vd[16];
+      um::line_vals<MODE>(lane_t + blk * 64, vc);
+      um::line_vals<MODE>(lane_t + blk * 64 + 32, vd);
+      const int o0 = um::mn_off(x * 2, z), o1 = um::mn_off(x * 2 + 1, z);
+      const bool sw = (x >> 2) & 1;
+      um::put_line<MODE>(smem + UM_P0, o0, o1, vc, sw);
+      um::put_line<MODE>(smem + UM_P1, o0, o1, vd, sw);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    // ---------------- z stage: v = Lz c + halo + Mz dd (cols 0 | 64)
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        const uint64_t ch = um::desc(s0 + UM_P0 + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t cd = um::desc(s0 + UM_P0 + UM_D + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t dh = um::desc(s0 + UM_P1 + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t ddd = um::desc(s0 + UM_P1 + UM_D + blk * 16 * UM_MN_SBO, UM_MN_LBO, UM_MN_SBO);
+        const uint64_t hh = um::desc(s0 + UM_HALO + 8192 + blk * 2048, 0, 128);
+        um::op_mma<MODE>(tm + blk * 64, ch, cd, bdesc(3, 0), bdesc(3, 1), 1, 0);
+        um::mma(tm + blk * 64, hh, bdesc(4, 0), um::idesc(0), 1);
+        if (MODE == MODE_FP16_EC) um::mma(tm + blk * 64 + 16, hh, bdesc(5, 0), um::idesc(0), 1);
+        um::op_mma<MODE>(tm + blk * 64, dh, ddd, bdesc(0, 0), bdesc(0, 1), 1, 1);
+      }
+      um::commit(bar);
+    }
+    um::wait(bar, phase);
+    phase ^= 1;
+    // line m = (x, y): outputs z -> f32 staging [z][y][x] (pitch 17) over P0 / P1, then coalesced rows to v
+    float* st = reinterpret_cast<float*>(smem + UM_P0);
+    __syncthreads();  // every thread's z-stage MMAs are complete: P0 / P1 reusable
+    const float os = pow2f(-(op.sc.aA + T.eu));
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const int m = blk * 128 + tid, x = m >> 4, y = m & 15;
+      float vv[16];
+      um::line_vals<MODE>(lane_t + blk * 64, vv);
+#pragma unroll
+      for (int z = 0; z < 16; ++z) st[(z * 16 + y) * 17 + x] = vv[z] * os;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    float* vb = v + (long long)batch * g.batch_stride +
+                ((long long)(T.cz * 8) * T.sz + (long long)(T.cy * 8) * T.sy + T.cx * 8);
+    {
+      const int x = tid & 15, y0 = tid >> 4;
+      float* p0 = vb + (y0 * T.sy + x);  // tile-local offsets stay below 16 sz < 2^31
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {  // row (z, y) = (r >> 1, y0 + 8 (r & 1))
+        const int z = r >> 1, y = y0 + 8 * (r & 1);
+        p0[z * T.sz + (r & 1) * 8 * T.sy] = st[(z * 16 + y) * 17 + x];
+      }
+    }
+    __syncthreads();  // staging consumed before the next tile's prologue overwrites it
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tm));
+}
+
 // residual + restriction (multigrid.py:249-250 + restrict :112-125): r = b - A x,
 // block exponent, P^T along z on the tensor cores (chained), y and x on CUDA cores.
 struct HPTab {
@@ -1111,6 +1441,37 @@ static void pack_halo(int mode, int KK, const double* ucol, const double* urow, 
   }
 }
 
+// tcgen05 B operands: Op^T in the K-major canonical layout (half index (n/8)*128 + (k/8)*64 + (n%8)*8 + (k%8))
+static void pack_op_umma(int mode, const double* Op /* [16][16] */, um::UTabOp& dst) {
+  for (int n = 0; n < 16; ++n)
+    for (int k = 0; k < 16; ++k) {
+      const int i = (n >> 3) * 128 + (k >> 3) * 64 + (n & 7) * 8 + (k & 7);
+      split_host(mode, Op[n * 16 + k], dst.h[i], dst.d[i]);
+    }
+}
+// halo B rows (k 0..7 as pack_halo; rows 8..15 zero: the halo A operand repeats its 8 halves there)
+static void pack_halo_umma(int mode, int KK, const double* ucol, const double* urow, um::UTabOp* dst /* [2] */) {
+  std::memset(dst, 0, 2 * sizeof(um::UTabOp));
+  for (int n = 0; n < 16; ++n) {
+    unsigned short ch[4] = {0, 0, 0, 0}, cd[4] = {0, 0, 0, 0};
+    if (n < KK) split_host(mode, urow[n], ch[0], cd[0]);
+    if (n == 0) ch[1] = half_bits(1.0f);
+    if (n >= 16 - KK) split_host(mode, ucol[n - (16 - KK)], ch[2], cd[2]);
+    if (n == 15) ch[3] = half_bits(1.0f);
+    unsigned short mrow[8] = {ch[0], ch[1], ch[2], ch[3], 0, 0, 0, 0};
+    const unsigned short crow[8] = {cd[0], 0, cd[2], 0, ch[0], ch[1], ch[2], ch[3]};
+    if (mode != MODE_FP16_EC) {
+      mrow[5] = n == 0 ? half_bits(1.0f / kEc) : 0;
+      mrow[7] = n == 15 ? half_bits(1.0f / kEc) : 0;
+    }
+    for (int k = 0; k < 8; ++k) {
+      const int i = (n >> 3) * 128 + (n & 7) * 8 + k;  // k < 8: k-group 0
+      dst[0].h[i] = mrow[k];
+      dst[1].h[i] = crow[k];
+    }
+  }
+}
+
 static void build_tables(int mode, int KK, const double* opd, const double* eigd, HTables& t) {
   std::memset(&t, 0, sizeof(t));
   double Mp[256], L[4][256], V[4][256], lam[4][16];
@@ -1130,6 +1491,24 @@ static void build_tables(int mode, int KK, const double* opd, const double* eigd
   const double* ucol = opd + 2 * KK * KK;
   const double* urow = ucol + KK;
   pack_halo(mode, KK, ucol, urow, t.halo);
+}
+
+static void build_utab(int mode, int KK, const double* opd, const double* eigd, um::UTab& t) {
+  std::memset(&t, 0, sizeof(t));
+  double Mp[256], L[4][256], V[4][256], lam[4][16];
+  build_line_ops_host(KK, opd, eigd, Mp, &L[0][0], eigd ? &V[0][0] : nullptr, &lam[0][0]);
+  pack_op_umma(mode, Mp, t.M);
+  for (int q = 0; q < 4; ++q) pack_op_umma(mode, L[q], t.L[q]);
+  if (eigd)
+    for (int q = 0; q < 4; ++q) {
+      double VT[256];
+      for (int i = 0; i < 16; ++i)
+        for (int jj = 0; jj < 16; ++jj) VT[i * 16 + jj] = V[q][jj * 16 + i];
+      pack_op_umma(mode, VT, t.Vf[q]);
+      pack_op_umma(mode, V[q], t.Vb[q]);
+    }
+  const double* ucol = opd + 2 * KK * KK;
+  pack_halo_umma(mode, KK, ucol, ucol + KK, t.halo);
 }
 
 // denominators f32((lam_z + lam_y + lam_x) 2^-aD) (the reference sums in fp64 and casts,
@@ -1160,11 +1539,12 @@ struct Entry {
   std::vector<double> key;
   void* ptr;
   void* den;
+  void* utab;
 };
 static std::vector<Entry> g_cache;
 
 static const HTables* tables(int mode, const double* opd, const double* eigd, int KK = K,
-                             const DenTab** den = nullptr) {
+                             const DenTab** den = nullptr, const um::UTab** utab = nullptr) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int nop = 2 * KK * KK + 4 * KK, neig = 4 * 4 * KK * KK + 4 * 2 * KK;
@@ -1176,6 +1556,7 @@ static const HTables* tables(int mode, const double* opd, const double* eigd, in
   for (auto& e : g_cache)
     if (e.dev == dev && e.mode == mode && e.key == key) {
       if (den) *den = reinterpret_cast<const DenTab*>(e.den);
+      if (utab) *utab = reinterpret_cast<const um::UTab*>(e.utab);
       return reinterpret_cast<const HTables*>(e.ptr);
     }
   double op_s[2 * K * K + 4 * K], eig_s[4 * 256 + 4 * 16];
@@ -1193,8 +1574,14 @@ static const HTables* tables(int mode, const double* opd, const double* eigd, in
     if (cudaMemcpy(dd, dens.data(), sizeof(DenTab) * dens.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return nullptr;
   }
-  g_cache.push_back({dev, mode, std::move(key), d, dd});
+  std::vector<um::UTab> uhost(1);
+  build_utab(mode, KK, op_s, eigd ? eig_s : nullptr, uhost[0]);
+  void* du = nullptr;
+  if (cudaMalloc(&du, sizeof(um::UTab)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(du, uhost.data(), sizeof(um::UTab), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_cache.push_back({dev, mode, std::move(key), d, dd, du});
   if (den) *den = reinterpret_cast<const DenTab*>(dd);
+  if (utab) *utab = reinterpret_cast<const um::UTab*>(du);
   return reinterpret_cast<const HTables*>(d);
 }
 
@@ -1225,6 +1612,15 @@ static bool smem_attr(F* fn) {
 }
 
 // Q7 (KK = 8) and the 16-point line tiles (KK = 4, 2; kUseGeneric when the grid does not tile)
+// tcgen05 path for the Q7 binary16 kernels (SUMFACT_UMMA=0 selects the mma.sync kernels)
+static bool use_umma() {
+  static const bool on = [] {
+    const char* e = std::getenv("SUMFACT_UMMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // banded 3-D grid of the tiles (dm::band_tile); very large batches are split across launches
 static dim3 band_grid(const Geom& g, const dm::Band& bd, int batch) {
   return dim3(g.ntx, bd.by, bd.zb * batch);
@@ -1253,11 +1649,28 @@ template <int MODE, int KK>
 static int vmult_t(const Geom& g0, const double* opd, const void* u, void* v, int batch, cudaStream_t st) {
   Geom g;
   if (!line_geom<KK>(g0, g, false, 2 * g0.ntz)) return kUseGeneric;  // 2 ntz: the caller's z range in cells
-  const HTables* tab = tables(MODE, opd, nullptr, KK);
-  if (!tab) return -3;
+  const um::UTab* ut = nullptr;
+  const HTables* tab = tables(MODE, opd, nullptr, KK, nullptr, &ut);
+  if (!tab || !ut) return -3;
   auto op = pack_op_h<MODE, KK>(opd, nullptr);
-  if (!smem_attr(k_vmult_h8<MODE, KK>)) return -3;
   const dm::Band bd = dm::make_band(g);
+  if constexpr (KK == 8) {
+    if (use_umma()) {
+      if (cudaFuncSetAttribute(k_vmult_u8<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemU) != cudaSuccess)
+        return -3;
+      const int per = 65535 / bd.zb;
+      for (int b0 = 0; b0 < batch; b0 += per) {
+        const int nb = batch - b0 < per ? batch - b0 : per;
+        const long long off = (long long)b0 * g.batch_stride;
+        const int ntiles = g.ntx * bd.by * bd.zb * nb;
+        const int grid = ntiles < 4 * 148 ? ntiles : 4 * 148;  // persistent: 4 CTAs per SM
+        k_vmult_u8<MODE><<<grid, kThreads, kSmemU, st>>>((const float*)u + off, (float*)v + off, g, bd, op, tab, ut,
+                                                         ntiles);
+      }
+      return cudaGetLastError() == cudaSuccess ? 0 : -3;
+    }
+  }
+  if (!smem_attr(k_vmult_h8<MODE, KK>)) return -3;
   const int per = 65535 / bd.zb;  // batches per launch (gridDim.z limit)
   for (int b0 = 0; b0 < batch; b0 += per) {
     const int nb = batch - b0 < per ? batch - b0 : per;
