@@ -401,12 +401,30 @@ def extras(sf, hier, lvl, k, u, v):
     # smoothing step (8 colour passes), Q7 level 6
     h6 = sf.build_hierarchy(6, k, max_dofs=2**34)
     D6 = h6.n_dofs(6)
-    for mode in (P.FP64, P.FP32, P.FP16):
+    from paper_2407_09621_b200 import _native, device as dev
+
+    hbm, _ = peaks()
+    for mode in (P.FP64, P.FP32, P.FP16, P.FP16_EC):
         mg = sf.MultigridPreconditioner(h6, sf.VCycleConfig(mode=mode))
         x = torch.zeros(D6, dtype=mode.torch_dtype, device="cuda")
         b = torch.randn(D6, dtype=mode.torch_dtype, device="cuda")
         ms = timeit(lambda: mg._smooth_device(6, x, b, mode), reps=2)
         res[f"smooth_step_q{k}_l6_{mode.value}_ms"] = ms
+        # one colour pass (shift 000: every DoF in a patch) -- the smoother's kernel, HBM roofline at
+        # 3 vectors (read x, b; write x) of the storage dtype per DoF
+        xn = torch.empty_like(x)
+        lm = h6.matrices(6)
+
+        def colour():
+            rc = _native.lib().sf_smooth_colour(mode.code, k, h6.grid(6), mg._shift_arrays[(0, 0, 0)],
+                                                _native.host_ptr(lm.cell_op), _native.host_ptr(mg.solvers[6].table),
+                                                dev.ptr(x), dev.ptr(b), dev.ptr(xn), dev.stream_ptr())
+            _native.check(rc, "sf_smooth_colour")
+        ms1 = timeit(colour, reps=5)
+        gbs = 3 * x.element_size() * D6 / (ms1 * 1e-3) / 1e9
+        res[f"colour_pass_q{k}_l6_{mode.value}"] = {"ms": ms1, "gdofs": D6 / ms1 / 1e6, "hbm_gbs": gbs,
+                                                   "hbm_frac": gbs / hbm}
+        del xn
     del x, b, mg
     torch.cuda.empty_cache()  # the vmult benches above leave large cached blocks; solves allocate afresh
     # time-to-solution (BASELINE configs[3]): FGMRES(fp64) + V-cycle(fp64 | fp16_ec), Q7 level 6,
