@@ -254,10 +254,24 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    halo_ms = None
     if world > 1:
         for _ in range(3):
             kernel_only()
         torch.cuda.synchronize()
+        # the K-plane halo exchange alone (NCCL send/recv of 2 x K planes), CUDA events on the compute stream
+        from paper_2407_09621_b200.slab import exchange_face_planes
+
+        glo2, ghi2 = op.ghosts(torch.float64)
+        hv = []
+        for _ in range(4):
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            exchange_face_planes(comm, op.slab, u, glo2, ghi2)
+            ev[1].record()
+            hv.append(ev)
+        torch.cuda.synchronize()
+        halo_ms = sum(a.elapsed_time(b) for a, b in hv[1:]) / 3
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         if shared:
@@ -313,6 +327,13 @@ def main():
            "roofline": roofline, "clocks": clk,
            # our kernels per timed step: one vmult; at N > 1 the interior + two boundary tile layers
            "gpu_launches": args.steps * (3 if world > 1 and n >= 3 * (16 // K if K in (2, 4) else 2) else 1)}
+    if halo_ms is not None:  # max over ranks; overlapped with the interior tiles inside the timed step
+        t = torch.tensor([halo_ms], dtype=torch.float64)
+        if not shared:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["halo"] = {"exchange_ms_alone": float(t.item()), "bytes_per_rank": 2 * 8 * K * A * A,
+                       "overlapped_with": "interior tile layers (sf_vmult_zrange) during the timed step"}
 
     # e2e: the public API with pinned HOST buffers, H2D + D2H inside the timed region, every step
     try:

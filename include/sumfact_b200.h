@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 3  /* 2: sf_div, SF_LINCOMB_MAX_TERMS; 3: sf_quad_error / sf_quad_load / sf_face_load */
+#define SF_ABI_VERSION 4  /* 2: sf_div, SF_LINCOMB_MAX_TERMS; 3: sf_quad_*; 4: sf_smooth_colour_zrange, sf_copy_uncovered */
 #define SF_MAX_DEGREE 7
 
 #define SF_OK 0
@@ -78,6 +78,17 @@ int sf_vmult_zrange(int mode, int k, const sf_grid* grid, int z0, int z1, const 
  *                                                          multigrid.py:186-203 (PatchSolver.apply_batch :71-83). */
 int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, const double* level_op,
                      const double* patch_eig, const void* x_old, const void* b, void* x_new, void* stream);
+
+/* One colour restricted to the tiles whose first z cell lies in [z0, z1) (z0 = shift[2] + 2 t, whole 2-cell tiles),
+ * WITHOUT the copy of the cells the shifted colour leaves uncovered (sf_copy_uncovered does that once): a z-slab
+ * rank runs its interior tiles while the ghost cells are in flight and the boundary tiles after.  Q7 (k = 7) only;
+ * SF_EUNSUPPORTED otherwise.  Same operator as sf_smooth_colour                 multigrid.py:186-203. */
+int sf_smooth_colour_zrange(int mode, int k, const sf_grid* grid, const int* shift, int z0, int z1,
+                            const double* level_op, const double* patch_eig, const void* x_old, const void* b,
+                            void* x_new, void* stream);
+/* x_new = x_old on the cells a shifted colour does not cover (the last step of sf_smooth_colour). */
+int sf_copy_uncovered(int mode, int k, const sf_grid* grid, const int* shift, const void* x_old, void* x_new,
+                      void* stream);
 
 /* coarse = R (b - A x) (x != NULL) or R b (x == NULL), R = P^T on each axis.
  * Replaces `r = b - apply_operator(x); restrict(r)`        multigrid.py:249-250, 112-125. */

@@ -99,7 +99,7 @@ def all_cores_vmult(k=7, lvl=5, reps=2):
     return {"seconds": best, "dofs": H.n_dofs(lvl), "threads": threads, "case": f"vmult Q{k} L{lvl}"}
 
 
-def run(cases, reps=3):
+def run(cases, reps=3, verbose=False):
     out = {"cpu_model": cpu_model(), "nproc": os.cpu_count(), "cores_used": 1,
            "method": "child process pinned to one core (sched_setaffinity), BLAS threads 1, best of "
                      f"{reps} after a warm-up; backends: reference compiled kernel (oracle/_ref) and numpy "
@@ -112,7 +112,8 @@ def run(cases, reps=3):
         out["cases"][name] = {"seconds": {b: v.get("seconds") for b, v in r.items()}, "best_backend": best,
                               "dofs": ok[best]["dofs"],
                               "mdofs_per_s": ok[best]["dofs"] / ok[best]["seconds"] / 1e6}
-        print(name, out["cases"][name], flush=True)
+        if verbose:  # (bench.py prints exactly one JSON line: silent there)
+            print(name, out["cases"][name], flush=True)
     return out
 
 
@@ -123,7 +124,7 @@ if __name__ == "__main__":
     a = ap.parse_args()
     cases = [("vmult", 7, 4)] if a.quick else [("vmult", 7, 4), ("vmult", 3, 5), ("smooth", 3, 4), ("smooth", 7, 3),
                                                ("solve", 3, 4)]
-    res = run(cases)
+    res = run(cases, verbose=True)
     res["all_cores"] = all_cores_vmult()
     print(json.dumps(res, indent=1))
     if a.out:

@@ -19,7 +19,7 @@ SF_EUNSUPPORTED = -2
 SF_ECUDA = -3
 SF_DOT_SCRATCH = 1024
 SF_LINCOMB_MAX_TERMS = 128  # include/sumfact_b200.h
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_DEGREE = 7
 
 
@@ -52,6 +52,8 @@ def lib():
             "sf_vmult": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_i, c_p], c_i),
             "sf_vmult_zrange": ([c_i, c_i, P_grid, c_i, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_smooth_colour": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
+            "sf_smooth_colour_zrange": ([c_i, c_i, P_grid, c_p, c_i, c_i, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
+            "sf_copy_uncovered": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p], c_i),
             "sf_residual_restrict": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p, c_p, c_p], c_i),
             "sf_prolongate_add": ([c_i, c_i, P_grid, c_p, c_p, c_p, c_p], c_i),
             "sf_patch_apply": ([c_i, c_i, c_ll, c_p, c_p, c_p, c_p, c_p], c_i),
@@ -94,7 +96,8 @@ def lib():
 EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "sf_smooth_colour", "sf_residual_restrict",
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
             "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_div", "sf_quad_error",
-            "sf_quad_load", "sf_face_load")
+            "sf_quad_load", "sf_face_load",
+            "sf_smooth_colour_zrange", "sf_copy_uncovered")
 
 # which thread-local error buffer each entry point writes (each module clears its own on entry)
 _VEC = {"sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_axpby", "sf_axpby_f32",
@@ -109,7 +112,8 @@ def _error_message(what: str) -> str:
         getter = L.sf_vec_last_error
     elif name in _HALF:
         getter = L.sf_half_last_error
-    elif name in ("sf_quad_error", "sf_quad_load", "sf_face_load"):
+    elif name in ("sf_quad_error", "sf_quad_load", "sf_face_load",
+            "sf_smooth_colour_zrange", "sf_copy_uncovered"):
         getter = L.sf_quad_last_error
     elif name == "sf_contract":
         getter = L.sf_contract_last_error

@@ -691,7 +691,7 @@ static int launch_vmult(const sf_grid* gr, const double* opd, const void* u, voi
 
 template <int K, int MODE>
 static int launch_colour(const sf_grid* gr, const int* shift, const double* opd, const double* eigd, const void* xo,
-                         const void* b, void* xn, cudaStream_t st) {
+                         const void* b, void* xn, cudaStream_t st, int z0 = -1, int z1 = -1, bool copy = true) {
   Geom g;
   // shift[i] is tensor axis i (x = 0), multigrid.py:189-192
   int rc = make_geom(gr, K, shift[0], shift[1], shift[2], g);
@@ -699,7 +699,14 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
   constexpr int TPC = Tpc<K>::value;
   using E = TileEngine<K, MODE, TPC>;
   using S = typename MT<MODE>::S;
+  if (z0 >= 0) {  // tiles whose first cell lies in [z0, z1) only (z-slab interior / boundary split)
+    if (K != 8) return fail(SF_EUNSUPPORTED, "z-range colour passes are Q7 (2-cell tiles) only");
+    if (z1 == z0) return SF_OK;
+    g.tz0 = z0;
+    g.ntz = (z1 - z0) / 2;
+  }
   if (g.ntx < 1 || g.nty < 1 || g.ntz < 1) {
+    if (!copy) return SF_OK;
     // colour without patches: x_new = x_old
     size_t bytes = (size_t)gr->nx * gr->ny * gr->nz * K * K * K * sizeof(S);
     if (cudaMemcpyAsync(xn, xo, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -752,12 +759,21 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
                                                                         eig);
     if ((rc = check_launch("sf_smooth_colour"))) return rc;
   }
-  if (shift[0] || shift[1] || shift[2]) {
+  if (copy && (shift[0] || shift[1] || shift[2])) {
     k_copy_slabs<S><<<148 * 4, 256, 0, st>>>((const S*)xo, (S*)xn, K, gr->nx, gr->ny, gr->nz, shift[0], shift[1],
                                              shift[2]);
     return check_launch("sf_smooth_colour slabs");
   }
   return SF_OK;
+}
+
+template <int K, int MODE>
+static int launch_copy_uncovered(const sf_grid* gr, const int* shift, const void* xo, void* xn, cudaStream_t st) {
+  using S = typename MT<MODE>::S;
+  if (!(shift[0] || shift[1] || shift[2])) return SF_OK;
+  k_copy_slabs<S><<<148 * 4, 256, 0, st>>>((const S*)xo, (S*)xn, K, gr->nx, gr->ny, gr->nz, shift[0], shift[1],
+                                           shift[2]);
+  return check_launch("sf_copy_uncovered");
 }
 
 template <int K, int MODE>
@@ -944,6 +960,39 @@ int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, con
   if (x_old == x_new) return fail(SF_EINVAL, "x_old and x_new must be distinct buffers");
   cudaStream_t st = (cudaStream_t)stream;
 #define CALL(K, M) launch_colour<K, M>(grid, shift, level_op, patch_eig, x_old, b, x_new, st)
+  SF_DISPATCH(k, mode, CALL);
+#undef CALL
+}
+
+int sf_smooth_colour_zrange(int mode, int k, const sf_grid* grid, const int* shift, int z0, int z1,
+                            const double* level_op, const double* patch_eig, const void* x_old, const void* b,
+                            void* x_new, void* stream) {
+  int rc = check_common(mode, k);
+  if (rc) return rc;
+  if (!grid || !shift || !x_old || !b || !x_new || !level_op || !patch_eig) return fail(SF_EINVAL, "null pointer");
+  SF_ALIGNED(x_old, b, x_new);
+  if (misaligned_grid(grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
+  for (int i = 0; i < 3; ++i)
+    if (shift[i] != 0 && shift[i] != 1) return fail(SF_EINVAL, "shift entries must be 0 or 1");
+  if (x_old == x_new) return fail(SF_EINVAL, "x_old and x_new must be distinct buffers");
+  if (z0 < shift[2] || z1 < z0 || z1 > grid->nz || ((z0 - shift[2]) & 1) || ((z1 - z0) & 1) ||
+      z1 > grid->nz - (shift[2] ? 1 : 0))
+    return fail(SF_EINVAL, "z range must start on a tile of the colour and hold whole 2-cell tiles");
+  cudaStream_t st = (cudaStream_t)stream;
+#define CALL(K, M) launch_colour<K, M>(grid, shift, level_op, patch_eig, x_old, b, x_new, st, z0, z1, false)
+  SF_DISPATCH(k, mode, CALL);
+#undef CALL
+}
+
+int sf_copy_uncovered(int mode, int k, const sf_grid* grid, const int* shift, const void* x_old, void* x_new,
+                      void* stream) {
+  int rc = check_common(mode, k);
+  if (rc) return rc;
+  if (!grid || !shift || !x_old || !x_new) return fail(SF_EINVAL, "null pointer");
+  for (int i = 0; i < 3; ++i)
+    if (shift[i] != 0 && shift[i] != 1) return fail(SF_EINVAL, "shift entries must be 0 or 1");
+  cudaStream_t st = (cudaStream_t)stream;
+#define CALL(K, M) launch_copy_uncovered<K, M>(grid, shift, x_old, x_new, st)
   SF_DISPATCH(k, mode, CALL);
 #undef CALL
 }

@@ -200,6 +200,22 @@ def refresh_ghost_cells(comm: SlabComm, sl: SlabLevel, x_ext: torch.Tensor):
                   send_hi=loc[loc.numel() - GHOST_CELLS * L:], recv_hi=x_ext[x_ext.numel() - sl.h_hi * L:])
 
 
+def refresh_ghost_cells_start(comm: SlabComm, sl: SlabLevel, x_ext: torch.Tensor):
+    """refresh_ghost_cells posted asynchronously (NCCL: on its stream); finish with comm.exchange_finish."""
+    if comm.world == 1:
+        return None
+    L = sl.cell_layer
+    loc = x_ext[sl.local_slice]
+    return comm.exchange_start(send_lo=loc[:GHOST_CELLS * L], recv_lo=x_ext[:sl.h_lo * L],
+                               send_hi=loc[loc.numel() - GHOST_CELLS * L:],
+                               recv_hi=x_ext[x_ext.numel() - sl.h_hi * L:])
+
+
+# Q7 smoother on z-slabs: the ghost-cell refresh of each colour overlaps the colour's interior tiles
+# (sf_smooth_colour_zrange), the boundary tiles run once the cells have landed
+OVERLAP_SMOOTHER = True
+
+
 def _grid(n: int, nz: int, lo=None, hi=None) -> _native.SfGrid:
     return _native.SfGrid(n, n, nz, lo, hi)
 
@@ -324,14 +340,34 @@ class DistributedMultigrid:
         cur, nxt = x_ext, tmp
         lib = _native.lib()
         g = self._ext_grid(sl)
+        nz_ext = sl.nz + sl.h_lo + sl.h_hi
+        overlap = self.comm.world > 1 and hier.degree == 7 and OVERLAP_SMOOTHER
         for shift in self.config.smoother_ordering:
             if min(sl.n // 2 - s for s in shift) < 1:
                 continue
-            self._refresh(sl, cur)
-            rc = lib.sf_smooth_colour(mode.code, hier.degree, g, self.mg._shift_arrays[shift],
-                                      _native.host_ptr(lm.cell_op), _native.host_ptr(table), device.ptr(cur),
-                                      device.ptr(b_ext), device.ptr(nxt), device.stream_ptr())
-            _native.check(rc, "sf_smooth_colour")
+            sh = self.mg._shift_arrays[shift]
+            args = (_native.host_ptr(lm.cell_op), _native.host_ptr(table), device.ptr(cur), device.ptr(b_ext),
+                    device.ptr(nxt), device.stream_ptr())
+            sz = shift[2]
+            # interior tiles (first cell c): read x on cells c-1..c+2, none of them a ghost cell
+            lo = sl.h_lo + 1 + ((sl.h_lo + 1 - sz) & 1)
+            hi = nz_ext - sl.h_hi - 3
+            hi -= (hi - sz) & 1
+            if overlap and hi >= lo:
+                handle = refresh_ghost_cells_start(self.comm, sl, cur)
+                rc = lib.sf_smooth_colour_zrange(mode.code, hier.degree, g, sh, lo, hi + 2, *args)
+                _native.check(rc, "sf_smooth_colour_zrange")
+                self.comm.exchange_finish(handle)
+                for z0, z1 in ((sz, lo), (hi + 2, nz_ext - sz)):
+                    rc = lib.sf_smooth_colour_zrange(mode.code, hier.degree, g, sh, z0, z1, *args)
+                    _native.check(rc, "sf_smooth_colour_zrange")
+                rc = lib.sf_copy_uncovered(mode.code, hier.degree, g, sh, device.ptr(cur), device.ptr(nxt),
+                                           device.stream_ptr())
+                _native.check(rc, "sf_copy_uncovered")
+            else:
+                self._refresh(sl, cur)
+                rc = lib.sf_smooth_colour(mode.code, hier.degree, g, sh, *args)
+                _native.check(rc, "sf_smooth_colour")
             cur, nxt = nxt, cur
         if cur is not x_ext:
             x_ext.copy_(cur)
@@ -448,5 +484,6 @@ def scatter_slab(x_global, comm: SlabComm, sl: SlabLevel) -> torch.Tensor:
 
 
 __all__ = ["SlabComm", "SlabLevel", "slab_levels", "DistributedOperator", "DistributedMultigrid",
-           "fgmres_distributed", "run_solve_distributed", "scatter_slab", "exchange_face_planes", "refresh_ghost_cells", "GHOST_CELLS"]
+           "fgmres_distributed", "run_solve_distributed", "scatter_slab", "exchange_face_planes", "refresh_ghost_cells",
+           "refresh_ghost_cells_start", "GHOST_CELLS", "OVERLAP_SMOOTHER"]
 

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     lib.sf_abi_version.restype = ctypes.c_int
     from paper_2407_09621_b200 import _native
 
-    assert lib.sf_abi_version() == _native.ABI_VERSION == 3
+    assert lib.sf_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_library_is_sm100a_only():
@@ -123,7 +123,7 @@ def test_abi_mismatch_is_an_import_error(tmp_path, monkeypatch):
     from paper_2407_09621_b200 import _native
 
     src = tmp_path / "old.c"
-    src.write_text("int sf_abi_version(void) { return 2; }\n")
+    src.write_text("int sf_abi_version(void) { return 4; }\n")
     so = tmp_path / "libold.so"
     subprocess.run(["gcc", "-shared", "-fPIC", "-o", str(so), str(src)], check=True)
     monkeypatch.setattr(_native, "LIB_PATH", str(so))
