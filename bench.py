@@ -309,8 +309,8 @@ def main():
             from record_traffic import source_hash
 
             rec = json.load(open(traffic))
-            if rec.get("source_hash") == source_hash():
-                roofline["traffic"] = rec.get(f"k{k}_l{lvl}_fp64")
+            if rec.get("source_hash") == source_hash() and rec.get(f"k{k}_l{lvl}_fp64"):
+                roofline["traffic"] = rec[f"k{k}_l{lvl}_fp64"]
                 roofline["traffic_source"] = "profiles/vmult_traffic.json (ncu dram bytes, same kernel sources)"
         except Exception:
             pass
