@@ -198,23 +198,25 @@ def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Ten
                   slab_cells: int | None = None):
     """v = A u for HOST u, v: z-slabs of the vector flow host -> HBM -> host on three streams.
 
-    Slab i's copy-in (with the K ghost planes on each side it needs), its vmult (sf_vmult with
-    ghost_lo/ghost_hi pointing at those planes -- the same mechanism as the multi-GPU halo) and its
-    copy-out run on separate streams, so the host-link transfers in both directions overlap each
-    other and the kernel.  Two device buffers per direction (double buffering).
+    Every cell layer of u crosses the host link exactly once, into a device-resident copy of u: slab i's
+    copy-in brings its layers up to and including the first layer of slab i + 1 (its upper ghost), so its
+    lower ghost is already resident from slab i - 1.  Slab i's vmult (sf_vmult with ghost_lo / ghost_hi
+    pointing at the neighbouring layers -- the same mechanism as the multi-GPU halo) and its copy-out run on
+    separate streams, so the transfers in both directions overlap each other and the kernel; the output
+    is double buffered.
     """
     n, K = hier.n_cells(level), hier.degree + 1
     layer = K * (n * K) ** 2  # one cell layer of dofs
     if slab_cells is None:
-        slab_cells = max(2, (n // 8) & ~1)  # 16 cells at level 7: 87% of the measured 92 GB/s duplex link (tools/pcie_probe.py)
+        slab_cells = max(2, (n // 16) & ~1)  # 8 cells at level 7 (tools/e2e_time.py: 5.8 GDoF/s vs 5.6 at 16)
     slab_cells = min(slab_cells, n)
     dt = mode.torch_dtype
-    key = (torch.cuda.current_device(), dt, slab_cells, layer)
+    key = (torch.cuda.current_device(), dt, slab_cells, layer, n)
     bufs = _STREAM_BUFS.get(key)
     if bufs is None:
         for k_old in [k for k in _STREAM_BUFS if k[0] == key[0]]:  # keep one set per device
             del _STREAM_BUFS[k_old]
-        bufs = {"in": [torch.empty((slab_cells + 2) * layer, dtype=dt, device="cuda") for _ in range(2)],
+        bufs = {"in": torch.empty(n * layer, dtype=dt, device="cuda"),
                 "out": [torch.empty(slab_cells * layer, dtype=dt, device="cuda") for _ in range(2)],
                 "streams": [torch.cuda.Stream() for _ in range(3)]}
         _STREAM_BUFS[key] = bufs
@@ -222,37 +224,35 @@ def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Ten
     main = torch.cuda.current_stream()
     for s in (s_in, s_run, s_out):
         s.wait_stream(main)
-    in_free = [None, None]   # vmult finished reading in[b]
     out_free = [None, None]  # copy-out finished reading out[b]
     lm = hier.matrices(level)
     L = _native.lib()
-    es = u.element_size()
+    dev = bufs["in"]
+    es = dev.element_size()
+    base = dev.data_ptr()
+    copied_to = 0  # cell layers of u resident on the device
     for i, z0 in enumerate(range(0, n, slab_cells)):
         b = i & 1
         z1 = min(n, z0 + slab_cells)
-        lo, hi = int(z0 > 0), int(z1 < n)
-        dbuf, obuf = bufs["in"][b], bufs["out"][b]
+        obuf = bufs["out"][b]
+        need = min(n, z1 + 1)  # this slab and its upper ghost layer
         with torch.cuda.stream(s_in):
-            if in_free[b] is not None:
-                s_in.wait_event(in_free[b])
-            a0, a1 = (z0 - lo) * layer, (z1 + hi) * layer
-            dbuf[: a1 - a0].copy_(u[a0:a1], non_blocking=True)
+            dev[copied_to * layer:need * layer].copy_(u[copied_to * layer:need * layer], non_blocking=True)
             loaded = torch.cuda.Event()
             loaded.record(s_in)
+        copied_to = need
         s_run.wait_event(loaded)
         if out_free[b] is not None:
             s_run.wait_event(out_free[b])
-        base = dbuf.data_ptr()
-        loc = base + lo * layer * es                       # first dof of the slab itself
-        ghost_lo = base if lo else None                    # the K planes just below: dbuf's first layer
-        ghost_hi = loc + (z1 - z0) * layer * es if hi else None                 # K planes just above
+        loc = base + z0 * layer * es
+        ghost_lo = base + (z0 - 1) * layer * es if z0 > 0 else None
+        ghost_hi = base + z1 * layer * es if z1 < n else None
         grid = _native.SfGrid(n, n, z1 - z0, ghost_lo, ghost_hi)
         rc = L.sf_vmult(mode.code, hier.degree, grid, _native.host_ptr(lm.cell_op), loc, obuf.data_ptr(), 1,
                         s_run.cuda_stream)
         _native.check(rc, "sf_vmult (streamed)")
         done = torch.cuda.Event()
         done.record(s_run)
-        in_free[b] = done
         with torch.cuda.stream(s_out):
             s_out.wait_event(done)
             v[z0 * layer:z1 * layer].copy_(obuf[: (z1 - z0) * layer], non_blocking=True)
