@@ -314,62 +314,72 @@ __device__ __forceinline__ void st_a(unsigned h, unsigned d, unsigned off, const
 
 // Halo words: 16 bytes per line (axis, p, q) = packed halves
 //   [alpha_h lo, beta_h lo | alpha_h hi, beta_h hi | alpha_d lo, beta_d lo | alpha_d hi, beta_d hi]
-// (k rows of the halo MMA; see pack_halo).  A face writes its two 32-bit words (lo: 0, 2; hi: 1, 3).
+// (k rows of the halo MMA; see pack_halo), written whole by one lane (put_line).
 // fp16: alpha is a demoted operand (no residual half); beta keeps its residual half.
 // ZT (tcgen05 kernels): the z-axis lines are ordered (x, y) -- line index q * 16 + p -- as the z stage's
 // MMA rows are.
+// the full halo word of a line from both faces' (alpha, beta): one 16-byte store
 template <int MODE, bool ZT = false>
-__device__ __forceinline__ void put_face(char* sm, int axis, int p, int q, int hi, float alpha, float beta) {
-  unsigned h, d;
-  demote_pair<MODE_FP16_EC>(alpha, beta, h, d);
-  if constexpr (MODE != MODE_FP16_EC) d &= 0xffff0000u;
-  const int line = (ZT && axis == 2) ? q * 16 + p : p * 16 + q;
-  unsigned* w = reinterpret_cast<unsigned*>(sm + (ZT ? UM_HALO : SM_HALO) + (axis * 256 + line) * 16);
-  w[hi] = h;
-  w[2 + hi] = d;
+__device__ __forceinline__ void put_line(char* sm, int axis, int line, float al, float bl, float ah, float bh) {
+  unsigned hl, dl, hh, dh;
+  demote_pair<MODE_FP16_EC>(al, bl, hl, dl);
+  demote_pair<MODE_FP16_EC>(ah, bh, hh, dh);
+  if constexpr (MODE != MODE_FP16_EC) {
+    dl &= 0xffff0000u;
+    dh &= 0xffff0000u;
+  }
+  *reinterpret_cast<uint4*>(sm + (ZT ? UM_HALO : SM_HALO) + (axis * 256 + line) * 16) = make_uint4(hl, hh, dl, dh);
 }
 
-// Tangential mass of one face's (alpha, beta) trace planes on the tensor cores (16 x 16 f32 planes,
-// pitch 17, A fragments gathered from shared memory with demotion).  along_p = false: mass along q
-// (row = p, k = q); true: along p (row = q, k = p).  to_halo: write the face's halo words, else the
-// f32 planes in place.
+// Tangential mass of both faces' (alpha, beta) trace planes of one axis on the tensor cores (16 x 16 f32
+// planes, pitch 17, A fragments gathered from shared memory with demotion), output columns 8 nt .. 8 nt + 7
+// only (M_line is block diagonal, so they need the k block nt alone; two warps split an axis).  along_p =
+// false: mass along q (row = p, k = q); true: along p (row = q, k = p).  to_halo: write the lines' full halo
+// words (both faces at once: no partial-word stores), else the f32 planes in place.  A face whose bit in
+// `on` is clear (domain boundary) contributes zero.
 template <int MODE, bool ZT = false>
-__device__ __forceinline__ void face_mass(const HTile<MODE>& T, float* pa, bool along_p, bool to_halo, int axis,
-                                          int hi, const HOpFrag& bm) {
-  float o[2][2][4];  // [alpha / beta][nt][i]
+__device__ __forceinline__ void face_mass(const HTile<MODE>& T, float* pa, int on, bool along_p, bool to_halo,
+                                          int axis, int nt, const HOpFrag& bm) {
+  float o[2][2][4];  // [face][alpha / beta][i]
 #pragma unroll
-  for (int ab = 0; ab < 2; ++ab) {
-    const float* P = pa + ab * PLS;
-    auto at = [&](int row, int k) -> float { return along_p ? P[k * PLP + row] : P[row * PLP + k]; };
-    float v[2][4];
+  for (int f = 0; f < 2; ++f)
 #pragma unroll
-    for (int kb = 0; kb < 2; ++kb) {
-      v[kb][0] = at(T.g, 8 * kb + 2 * T.t);
-      v[kb][1] = at(T.g, 8 * kb + 2 * T.t + 1);
-      v[kb][2] = at(T.g + 8, 8 * kb + 2 * T.t);
-      v[kb][3] = at(T.g + 8, 8 * kb + 2 * T.t + 1);
-    }
-    HFrag a;
-    to_frag<MODE>(v, a);  // same register order as an accumulator fragment
-    HAcc<MODE> acc;
-    acc.zero();
-    mma_bd<MODE>(acc, a, bm);
-    acc.vals(o[ab]);
-  }
-  __syncwarp();
+    for (int ab = 0; ab < 2; ++ab) {
 #pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
+      for (int i = 0; i < 4; ++i) o[f][ab][i] = 0.f;
+      if (!((on >> f) & 1)) continue;
+      const float* P = pa + (2 * f + ab) * PLS;
+      auto at = [&](int row, int k) -> float { return along_p ? P[k * PLP + row] : P[row * PLP + k]; };
+      const int k0 = 8 * nt + 2 * T.t;
+      unsigned h0, d0, h1, d1;
+      demote_pair<MODE>(at(T.g, k0), at(T.g, k0 + 1), h0, d0);
+      demote_pair<MODE>(at(T.g + 8, k0), at(T.g + 8, k0 + 1), h1, d1);
+      const unsigned bh = nt ? bm.h[3] : bm.h[0];
+      hmma8(o[f][ab], h0, h1, bh);
+      if constexpr (MODE == MODE_FP16_EC) {
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+        hmma16(c, h0, h1, d0, d1, nt ? bm.d[3] : bm.d[0], bh);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = T.g + 8 * (i >> 1), n = 8 * nt + 2 * T.t + (i & 1);
-      const int p = along_p ? n : row, qq = along_p ? row : n;
-      if (to_halo) {
-        put_face<MODE, ZT>(T.sm, axis, p, qq, hi, o[0][nt][i], o[1][nt][i]);
-      } else {
-        pa[p * PLP + qq] = o[0][nt][i];
-        pa[PLS + p * PLP + qq] = o[1][nt][i];
+        for (int i = 0; i < 4; ++i) o[f][ab][i] = fmaf(c[i], kInvEc, o[f][ab][i]);
       }
     }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = T.g + 8 * (i >> 1), n = 8 * nt + 2 * T.t + (i & 1);
+    const int p = along_p ? n : row, qq = along_p ? row : n;
+    if (to_halo) {
+      const int line = (ZT && axis == 2) ? qq * 16 + p : p * 16 + qq;
+      put_line<MODE, ZT>(T.sm, axis, line, o[0][0][i], o[0][1][i], o[1][0][i], o[1][1][i]);
+    } else {
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+        if ((on >> f) & 1) {
+          pa[(2 * f) * PLS + p * PLP + qq] = o[f][0][i];
+          pa[(2 * f + 1) * PLS + p * PLP + qq] = o[f][1][i];
+        }
+    }
+  }
 }
 
 // face traces of a neighbour line of KK values w (nearest node last for lo, first for hi):
@@ -650,30 +660,24 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   //     L_line[kind]).
   HOpFrag bm;
   ld_op(bm, tab->M, T.lane);
-  {
-    const int axis = 1 + (T.warp >> 1), hi = T.warp & 1, f = 2 * axis + hi;
-    float* pa = tr + (2 * f) * PLS;
-    if ((T.nbm >> f) & 1) {
-      face_mass<MODE, UM>(T, pa, false, axis == 1, axis, hi, bm);
-    } else if (axis == 1) {
-      for (int i = T.lane; i < 256; i += 32) put_face<MODE, UM>(smem, 1, i >> 4, i & 15, hi, 0.f, 0.f);
-    }
+  // phase a: warps 0, 1 the y faces (halo words), warps 2, 3 the z faces along q (f32 in place); each warp
+  // one column block of both faces
+  const int mnt = T.warp & 1;
+  if (T.warp < 2) {
+    face_mass<MODE, UM>(T, tr + 4 * PLS, (T.nbm >> 2) & 3, false, true, 1, mnt, bm);
+  } else {
+    face_mass<MODE, UM>(T, tr + 8 * PLS, (T.nbm >> 4) & 3, false, false, 2, mnt, bm);
   }
   __syncthreads();
-  if (T.warp >= 2) {
-    const int hi = T.warp & 1, f = 4 + hi;
-    if ((T.nbm >> f) & 1) {
-      face_mass<MODE, UM>(T, tr + (2 * f) * PLS, true, true, 2, hi, bm);
-    } else {
-      for (int i = T.lane; i < 256; i += 32) put_face<MODE, UM>(smem, 2, i >> 4, i & 15, hi, 0.f, 0.f);
-    }
+  // phase b: warps 0, 1 the z faces along p (halo words), warps 2, 3 pack the x faces (no mass)
+  if (T.warp < 2) {
+    face_mass<MODE, UM>(T, tr + 8 * PLS, (T.nbm >> 4) & 3, true, true, 2, mnt, bm);
   } else {
-    const int hi = T.warp & 1;
-    const bool on = (T.nbm >> hi) & 1;
-    const float* pa = tr + (2 * hi) * PLS;
-    for (int i = T.lane; i < 256; i += 32) {
-      const int p = i >> 4, qq = i & 15;
-      put_face<MODE, UM>(smem, 0, p, qq, hi, on ? pa[p * PLP + qq] : 0.f, on ? pa[PLS + p * PLP + qq] : 0.f);
+    const bool onl = T.nbm & 1, onh = (T.nbm >> 1) & 1;
+    for (int i = T.lane + 32 * mnt; i < 256; i += 64) {
+      const int o = (i >> 4) * PLP + (i & 15);
+      put_line<MODE, UM>(smem, 0, i, onl ? tr[o] : 0.f, onl ? tr[PLS + o] : 0.f, onh ? tr[2 * PLS + o] : 0.f,
+                         onh ? tr[3 * PLS + o] : 0.f);
     }
   }
   if constexpr (UM) {
@@ -1414,7 +1418,7 @@ static void pack_op_frags(int mode, const double* Op /* [16][16] */, HOp& dst) {
   }
 }
 
-// halo B words (see mma_halo / put_face): k rows 0: alpha_lo coupling urow (outputs < KK), 1: beta_lo ->
+// halo B words (see mma_halo / put_line): k rows 0: alpha_lo coupling urow (outputs < KK), 1: beta_lo ->
 // output 0, 2: alpha_hi coupling ucol (outputs >= 16 - KK), 3: beta_hi -> output 15; EC corr rows 4..7
 // carry the main halves against the data's residual halves; fp16 rows 5, 7 add beta's residual / 2048.
 static void pack_halo(int mode, int KK, const double* ucol, const double* urow, uint4* dst /* [32] */) {
