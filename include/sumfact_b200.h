@@ -30,7 +30,8 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 4  /* 2: sf_div, SF_LINCOMB_MAX_TERMS; 3: sf_quad_*; 4: sf_smooth_colour_zrange, sf_copy_uncovered */
+#define SF_ABI_VERSION 5  /* 2: sf_div, SF_LINCOMB_MAX_TERMS; 3: sf_quad_*; 4: sf_smooth_colour_zrange,
+                            sf_copy_uncovered; 5: sf_dense_apply */
 #define SF_MAX_DEGREE 7
 
 #define SF_OK 0
@@ -156,6 +157,13 @@ int sf_axpby(long long n, double alpha, const double* x, double beta, double* y,
 
 /* float variant used inside low-precision V-cycles: y = alpha * x + beta * y (fp32). */
 int sf_axpby_f32(long long n, float alpha, const float* x, float beta, float* y, void* stream);
+
+/* y = A x, A dense n x n fp64 row-major on the device (n <= 2^20): the coarse-level solve as a product with the
+ * explicit inverse of the mode's demoted coarse matrix, one launch per V-cycle.  x_dtype / y_dtype: 0 f64,
+ * 1 f32; demote16 != 0 rounds x to binary16 first (the fp16 mode's bs = demote16(bs)).  Deterministic.
+ * Replaces scipy.linalg.lu_solve(factor, bs)                     multigrid.py:230-239. */
+int sf_dense_apply(long long n, const double* A, const void* x, int x_dtype, int demote16, void* y, int y_dtype,
+                   void* stream);
 
 /* ---- device pre/post-processing with general data (discretization.py:317-459) ----
  * Level with n cells per axis, degree k (K = k + 1 nodes), q Gauss points per cell axis (k + 2 or k + 3);

@@ -19,7 +19,7 @@ SF_EUNSUPPORTED = -2
 SF_ECUDA = -3
 SF_DOT_SCRATCH = 1024
 SF_LINCOMB_MAX_TERMS = 128  # include/sumfact_b200.h
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_DEGREE = 7
 
 
@@ -66,6 +66,7 @@ def lib():
             "sf_axpby": ([c_ll, c_d, c_p, c_d, c_p, c_p], c_i),
             "sf_div": ([c_ll, c_p, c_d, c_p, c_p], c_i),
             "sf_axpby_f32": ([c_ll, c_f, c_p, c_f, c_p, c_p], c_i),
+            "sf_dense_apply": ([c_ll, c_p, c_p, c_i, c_i, c_p, c_i, c_p], c_i),
             "sf_contract": ([c_i, c_ll, c_i, c_ll, c_i, c_p, c_p, c_p, c_p], c_i),
             "sf_contract_last_error": ([], ctypes.c_char_p),
             "sf_half_last_error": ([], ctypes.c_char_p),
@@ -97,11 +98,11 @@ EXPORTED = ("sf_abi_version", "sf_last_error", "sf_vmult", "sf_vmult_zrange", "s
             "sf_prolongate_add", "sf_patch_apply", "sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpby", "sf_axpby_f32",
             "sf_contract", "sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_div", "sf_quad_error",
             "sf_quad_load", "sf_face_load",
-            "sf_smooth_colour_zrange", "sf_copy_uncovered")
+            "sf_smooth_colour_zrange", "sf_copy_uncovered", "sf_dense_apply")
 
 # which thread-local error buffer each entry point writes (each module clears its own on entry)
 _VEC = {"sf_convert", "sf_dot", "sf_axpy_dev", "sf_axpy_dot", "sf_dot2", "sf_lincomb", "sf_axpby", "sf_axpby_f32",
-        "sf_div"}
+        "sf_div", "sf_dense_apply"}
 _HALF = {"sf_to_half", "sf_from_half", "sf_demote16", "sf_ec_split", "sf_ec_matmul"}
 
 
@@ -113,7 +114,7 @@ def _error_message(what: str) -> str:
     elif name in _HALF:
         getter = L.sf_half_last_error
     elif name in ("sf_quad_error", "sf_quad_load", "sf_face_load",
-            "sf_smooth_colour_zrange", "sf_copy_uncovered"):
+            "sf_smooth_colour_zrange", "sf_copy_uncovered", "sf_dense_apply"):
         getter = L.sf_quad_last_error
     elif name == "sf_contract":
         getter = L.sf_contract_last_error

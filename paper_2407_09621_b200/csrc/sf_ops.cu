@@ -196,28 +196,48 @@ __global__ void __launch_bounds__(kThreads) k_colour(const typename MT<MODE>::S*
   }
 }
 
-// cells not covered by a shifted colour keep their value in the ping-pong copy
-template <typename S>
-__global__ void k_copy_slabs(const S* __restrict__ xo, S* __restrict__ xn, int K, int nx, int ny, int nz, int sx,
-                             int sy_, int sz_) {
-  long long Ax = (long long)nx * K, Ay = (long long)ny * K, Az = (long long)nz * K;
-  long long n_x = sx ? 2LL * K * Ay * Az : 0;
-  long long n_y = sy_ ? 2LL * K * Ax * Az : 0;
-  long long n_z = sz_ ? 2LL * K * Ax * Ay : 0;
-  long long total = n_x + n_y + n_z;
+// cells not covered by a shifted colour keep their value in the ping-pong copy: the K-point boundary slabs of
+// every shifted axis, as contiguous runs (z: two ranges of whole planes, y: two row blocks per plane, x: two
+// K-point pieces per row) copied in 16-byte vectors V when K points are a whole number of them
+template <typename V>
+__global__ void k_copy_slabs(const V* __restrict__ xo, V* __restrict__ xn, int Kv, int K, int Axv, int Ay, int Az,
+                             int sx, int sy_, int sz_) {
+  const long long plane = (long long)Ay * Axv;
+  const long long cz = sz_ ? 2LL * K * plane : 0;
+  const long long cy = sy_ ? 2LL * Az * K * Axv : 0;
+  const long long cx = sx ? 2LL * Az * Ay * Kv : 0;
+  const long long total = cz + cy + cx;
+  const int runy = K * Axv;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    long long X, Y, Z, r = i;
-    if (r < n_z) {  // z slabs: planes [0,K) and [Az-K, Az)
-      X = r % Ax; r /= Ax; Y = r % Ay; r /= Ay; Z = r < K ? r : Az - 2 * K + r;
-    } else if ((r -= n_z) < n_y) {
-      X = r % Ax; r /= Ax; long long yy = r % (2 * K); Z = r / (2 * K); Y = yy < K ? yy : Ay - 2 * K + yy;
+    long long o;
+    if (i < cz) {
+      const long long zr = K * plane;
+      o = i < zr ? i : (Az - 2LL * K) * plane + i;
+    } else if (i < cz + cy) {
+      const long long j = i - cz;
+      const long long Z = j / (2 * runy);
+      const int r = (int)(j - Z * 2 * runy);
+      o = Z * plane + (r < runy ? r : (long long)(Ay - 2 * K) * Axv + r);
     } else {
-      r -= n_y;
-      long long xx = r % (2 * K); r /= 2 * K; Y = r % Ay; Z = r / Ay; X = xx < K ? xx : Ax - 2 * K + xx;
+      const long long j = i - cz - cy;
+      const long long row = j / (2 * Kv);
+      const int r = (int)(j - row * 2 * Kv);
+      o = row * Axv + (r < Kv ? r : Axv - 2 * Kv + r);
     }
-    long long o = (Z * Ay + Y) * Ax + X;
     xn[o] = xo[o];
+  }
+}
+
+template <typename S>
+static void copy_slabs(const S* xo, S* xn, int K, const sf_grid* gr, const int* shift, cudaStream_t st) {
+  const int Ax = gr->nx * K, Ay = gr->ny * K, Az = gr->nz * K;
+  if ((K * sizeof(S)) % 16 == 0) {
+    constexpr int w = 16 / sizeof(S);
+    k_copy_slabs<uint4><<<148 * 4, 256, 0, st>>>((const uint4*)xo, (uint4*)xn, K / w, K, Ax / w, Ay, Az, shift[0],
+                                                 shift[1], shift[2]);
+  } else {
+    k_copy_slabs<S><<<148 * 4, 256, 0, st>>>(xo, xn, K, K, Ax, Ay, Az, shift[0], shift[1], shift[2]);
   }
 }
 
@@ -760,8 +780,7 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
     if ((rc = check_launch("sf_smooth_colour"))) return rc;
   }
   if (copy && (shift[0] || shift[1] || shift[2])) {
-    k_copy_slabs<S><<<148 * 4, 256, 0, st>>>((const S*)xo, (S*)xn, K, gr->nx, gr->ny, gr->nz, shift[0], shift[1],
-                                             shift[2]);
+    copy_slabs<S>((const S*)xo, (S*)xn, K, gr, shift, st);
     return check_launch("sf_smooth_colour slabs");
   }
   return SF_OK;
@@ -771,8 +790,7 @@ template <int K, int MODE>
 static int launch_copy_uncovered(const sf_grid* gr, const int* shift, const void* xo, void* xn, cudaStream_t st) {
   using S = typename MT<MODE>::S;
   if (!(shift[0] || shift[1] || shift[2])) return SF_OK;
-  k_copy_slabs<S><<<148 * 4, 256, 0, st>>>((const S*)xo, (S*)xn, K, gr->nx, gr->ny, gr->nz, shift[0], shift[1],
-                                           shift[2]);
+  copy_slabs<S>((const S*)xo, (S*)xn, K, gr, shift, st);
   return check_launch("sf_copy_uncovered");
 }
 

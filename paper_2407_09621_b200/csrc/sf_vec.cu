@@ -2,6 +2,7 @@
 // precision boundary (krylov.py:49-137, multigrid.py:262-266).  128-bit
 // coalesced grid-stride loops; the dot product is a fixed-shape two-pass tree
 // (no atomics), so repeated runs are bitwise identical (SPEC determinism).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -160,6 +161,27 @@ __global__ void k_lincomb(long long n, int m, const LinComb lc, double* __restri
   }
 }
 
+// y = A x for the coarse level's explicit inverse (A dense n x n fp64, row-major): one warp per row, lanes
+// stride the columns, fixed xor-tree reduction (deterministic).  x is read in its storage type and, for the
+// fp16 mode, demoted to binary16 first (multigrid.py:230-239: bs = demote16(bs)); y is rounded to its type.
+template <typename X, typename Y>
+__global__ void k_dense_apply(int n, const double* __restrict__ A, const X* __restrict__ x, int demote,
+                              Y* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += (gridDim.x * blockDim.x) >> 5) {
+    const double* a = A + (long long)row * n;
+    double s = 0.0;
+    for (int c = lane; c < n; c += 32) {
+      double xv = (double)__ldg(&x[c]);
+      if (demote) xv = (double)__half2float(__float2half_rn((float)xv));
+      s = fma(__ldg(&a[c]), xv, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[row] = (Y)s;
+  }
+}
+
 thread_local char g_err[256] = "";
 
 // every entry point clears the buffer first, and every SF_EINVAL carries a message
@@ -280,6 +302,29 @@ int sf_div(long long n, const double* x, double d, double* y, void* stream) {
   if (n == 0) return SF_OK;
   k_div<<<grid_for(n, 4), kThreads, 0, (cudaStream_t)stream>>>(n, x, d, y);
   return launched("sf_div");
+}
+
+int sf_dense_apply(long long n, const double* A, const void* x, int x_dtype, int demote16, void* y, int y_dtype,
+                   void* stream) {
+  g_err[0] = 0;
+  if (n < 0 || n > (1LL << 20) || (n && (!A || !x || !y)))
+    return invalid("sf_dense_apply", "length outside [0, 2^20] or null pointer");
+  if ((x_dtype != 0 && x_dtype != 1) || (y_dtype != 0 && y_dtype != 1))
+    return invalid("sf_dense_apply", "dtype codes must be 0 (f64) or 1 (f32)");
+  if (n == 0) return SF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nn = (int)n;
+  long long blocks = (n * 32 + kThreads - 1) / kThreads;
+  const int g = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
+  if (x_dtype == 0 && y_dtype == 0)
+    k_dense_apply<double, double><<<g, kThreads, 0, st>>>(nn, A, (const double*)x, demote16, (double*)y);
+  else if (x_dtype == 1 && y_dtype == 1)
+    k_dense_apply<float, float><<<g, kThreads, 0, st>>>(nn, A, (const float*)x, demote16, (float*)y);
+  else if (x_dtype == 0)
+    k_dense_apply<double, float><<<g, kThreads, 0, st>>>(nn, A, (const double*)x, demote16, (float*)y);
+  else
+    k_dense_apply<float, double><<<g, kThreads, 0, st>>>(nn, A, (const float*)x, demote16, (double*)y);
+  return launched("sf_dense_apply");
 }
 
 }  // extern "C"

@@ -129,3 +129,15 @@ def convert(src: torch.Tensor, dst: torch.Tensor):
     code = {torch.float64: 0, torch.float32: 1}
     _native.check(_native.lib().sf_convert(src.numel(), ptr(src), code[src.dtype], ptr(dst), code[dst.dtype],
                                            stream_ptr()), "sf_convert")
+
+
+def dense_apply(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, demote16: bool = False):
+    """y = A x (A dense fp64 n x n on the device; x, y f64 or f32; demote16 rounds x to binary16 first)."""
+    code = {torch.float64: 0, torch.float32: 1}
+    if A.dtype != torch.float64 or A.dim() != 2 or A.shape[0] != A.shape[1] or not A.is_contiguous():
+        raise ValueError("A must be a contiguous square fp64 matrix")
+    n = A.shape[0]
+    if x.numel() != n or y.numel() != n:
+        raise ValueError("vector lengths must match the matrix")
+    _native.check(_native.lib().sf_dense_apply(n, ptr(A), ptr(x), code[x.dtype], int(demote16), ptr(y),
+                                               code[y.dtype], stream_ptr()), "sf_dense_apply")

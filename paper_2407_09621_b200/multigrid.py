@@ -162,6 +162,9 @@ def prolongate(hier: MeshHierarchy, coarse_level: int, e, mode: PrecisionMode = 
 # ------------------------------------------------------------ preconditioner
 
 
+COARSE_INVERSE_MAX = 16384  # coarse unknowns up to which the solve is a product with the explicit inverse
+
+
 class MultigridPreconditioner:
     """V-cycle on a mesh hierarchy, usable as a right preconditioner (multigrid.py:146-270)."""
 
@@ -234,7 +237,9 @@ class MultigridPreconditioner:
         return self._coarse_cache["dense"]
 
     def _coarse_factor(self, mode: PrecisionMode):
-        """multigrid.py:215-228 -- LU of the coarse matrix with operands demoted per mode."""
+        """multigrid.py:215-228 -- the coarse matrix with operands demoted per mode, factorised once.  Up to
+        COARSE_INVERSE_MAX unknowns the setup also forms its explicit inverse (fp64, from the LU factors) so that
+        every V-cycle's coarse solve is one sf_dense_apply launch instead of two triangular solves."""
         if mode not in self._coarse_cache:
             A = self._coarse_matrix()
             if mode is PrecisionMode.FP64:
@@ -248,8 +253,12 @@ class MultigridPreconditioner:
                 main = A32.half().float()
                 resid = ((A32 - main) * 2048.0).half().float()
                 Ad = main + resid / 2048.0
-            LU, piv = torch.linalg.lu_factor(Ad)
-            self._coarse_cache[mode] = (LU, piv)
+            if Ad.shape[0] <= COARSE_INVERSE_MAX:
+                LU, piv = torch.linalg.lu_factor(Ad.double())
+                eye = torch.eye(Ad.shape[0], dtype=torch.float64, device=Ad.device)
+                self._coarse_cache[mode] = ("inverse", torch.linalg.lu_solve(LU, piv, eye).contiguous())
+            else:
+                self._coarse_cache[mode] = ("lu",) + tuple(torch.linalg.lu_factor(Ad))
         return self._coarse_cache[mode]
 
     def setup(self):
@@ -259,8 +268,13 @@ class MultigridPreconditioner:
         return self
 
     def _coarse_solve_device(self, b: torch.Tensor, mode: PrecisionMode) -> torch.Tensor:
-        LU, piv = self._coarse_factor(mode)
-        bs = b.to(mode.torch_dtype)
+        fac = self._coarse_factor(mode)
+        bs = b.to(mode.torch_dtype).contiguous()
+        if fac[0] == "inverse":
+            x = torch.empty_like(bs)
+            device.dense_apply(fac[1], bs, x, demote16=mode is PrecisionMode.FP16)
+            return x
+        _, LU, piv = fac
         if mode is PrecisionMode.FP16:
             bs = bs.half().float()
         x = torch.linalg.lu_solve(LU, piv, bs.to(LU.dtype).reshape(-1, 1)).reshape(-1)

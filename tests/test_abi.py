@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     lib.sf_abi_version.restype = ctypes.c_int
     from paper_2407_09621_b200 import _native
 
-    assert lib.sf_abi_version() == _native.ABI_VERSION == 4
+    assert lib.sf_abi_version() == _native.ABI_VERSION == 5
 
 
 def test_library_is_sm100a_only():
@@ -97,6 +97,8 @@ def test_vector_entry_points_validate_with_messages():
         ("sf_axpy_dot", lambda: L.sf_axpy_dot(8, 1.0, None, None, None, None, None, None, None), "null"),
         ("sf_dot2", lambda: L.sf_dot2(-1, None, None, None, None, None, None, None), "negative"),
         ("sf_div", lambda: L.sf_div(8, None, 2.0, None, None), "null"),
+        ("sf_dense_apply", lambda: L.sf_dense_apply(8, None, out, 0, 0, out, 0, None), "null"),
+        ("sf_dense_apply", lambda: L.sf_dense_apply(8, out, out, 2, 0, out, 0, None), "dtype"),
         ("sf_convert", lambda: L.sf_convert(4, out, 3, out, 0, None), "dtype"),
     ]
     for name, call, frag in cases:

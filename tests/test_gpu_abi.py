@@ -156,3 +156,37 @@ def test_fused_mgs_toggle_is_bitwise_for_both_solvers(monkeypatch, solver):
     assert ra.iterations == rb.iterations
     assert ra.residual_history == rb.residual_history
     assert torch.equal(xa, xb)
+
+
+@pytest.mark.parametrize("xd,yd,dem", [(torch.float64, torch.float64, False), (torch.float32, torch.float32, False),
+                                       (torch.float32, torch.float32, True), (torch.float64, torch.float32, False),
+                                       (torch.float32, torch.float64, False)])
+def test_dense_apply_matches_matmul(xd, yd, dem):
+    """The coarse solve's product with the explicit inverse (sf_dense_apply) against an fp64 matmul."""
+    from paper_2407_09621_b200 import device
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for n in (1, 37, 512, 4096):
+        A = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+        x = torch.randn(n, dtype=torch.float64, device="cuda", generator=g).to(xd)
+        y = torch.empty(n, dtype=yd, device="cuda")
+        device.dense_apply(A, x, y, demote16=dem)
+        xr = x.float().half().double() if dem else x.double()
+        ref = A @ xr
+        tol = 1e-13 if yd == torch.float64 else 2e-7
+        assert ((y.double() - ref).abs().max() / ref.abs().max()).item() <= tol, (n, xd, yd, dem)
+        y2 = torch.empty_like(y)
+        device.dense_apply(A, x, y2, demote16=dem)
+        assert torch.equal(y, y2)  # deterministic
+
+
+def test_coarse_solve_uses_the_inverse_kernel():
+    import paper_2407_09621_b200 as sf
+
+    hier = sf.build_hierarchy(2, 3)
+    mg = sf.MultigridPreconditioner(hier).setup()
+    assert mg._coarse_factor(sf.PrecisionMode.FP64)[0] == "inverse"
+    A = mg._coarse_matrix()
+    b = torch.randn(A.shape[0], dtype=torch.float64, device="cuda")
+    x = mg.coarse_solve(b)
+    assert (torch.linalg.norm(A @ x - b) / torch.linalg.norm(b)).item() <= 1e-12

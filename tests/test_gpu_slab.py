@@ -34,10 +34,10 @@ def test_distributed_fgmres_solve_matches_single_gpu(world, k, lvl, mode):
         assert r["its_dist"] == r["its_single"], r
         assert r["solve_rel_err"] <= 1e-8, r
         assert r["run_solve_dist_its"] == r["run_solve_its"], r
-        # (Q7 at this size: the L2 error is the solver's algebraic error, so the FP16-EC value carries the
-        # rounding-level differences of the slab V-cycle)
+        # (Q7 at this size: the L2 error (2.4e-14) is the solver's algebraic error, so it carries the
+        # rounding-level differences of the slab V-cycle: relative 1e-6 plus an absolute 1e-18 in fp64)
         tol = 1e-6 if mode == "fp64" else 1e-2
-        assert abs(r["run_solve_dist_l2"] - r["run_solve_l2"]) <= tol * r["run_solve_l2"], r
+        assert abs(r["run_solve_dist_l2"] - r["run_solve_l2"]) <= tol * r["run_solve_l2"] + 1e-18, r
 
 
 def test_distributed_solve_memory_is_slab_local():
