@@ -8,7 +8,7 @@ D = hier.n_dofs(7)
 u = torch.randn(D, dtype=torch.float64).pin_memory()
 v = torch.empty_like(u).pin_memory()
 out = {}
-for sc in (4, 8, 16):
+for sc in (2, 4, 6, 8):
     dz._stream_vmult(hier, 7, u, v, sf.PrecisionMode.FP64, slab_cells=sc)
     torch.cuda.synchronize()
     t = time.perf_counter()
