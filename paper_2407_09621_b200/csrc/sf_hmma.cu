@@ -62,7 +62,7 @@ constexpr int SM_TR = SM_BH;                      // 12 planes: (face * 2 + alph
 constexpr int SM_XST = SM_TR + 12 * PLS * 4;      // [hi][256 rows][KK <= 8] f32
 constexpr int SM_EXP_A = SM_HALO + 3 * 256 * 16, SM_EXP_B = SM_XST + 2 * 256 * 8 * 4;
 constexpr int SM_EXP = SM_EXP_A > SM_EXP_B ? SM_EXP_A : SM_EXP_B;
-constexpr int kSmem = SM_EXP + 16;
+constexpr int kSmem = SM_EXP + 32;  // exponent slots: [0..3] input, [4..7] residual (one per warp)
 // tcgen05 (UMMA) kernels: two operand buffers P0 / P1, each a binary16 main-half tensor and (at + UM_D)
 // the EC residual-half tensor in canonical no-swizzle layouts; halo words, operator B tables, the
 // mbarrier, the TMEM base and the exponent words after them.  During the prologue P1 and the halo
@@ -77,7 +77,7 @@ constexpr int UM_BAR = UM_TAB + UM_NOPS * 1024;              // mbarrier (8 B), 
 constexpr int UM_EXP = UM_BAR + 16;
 constexpr int UM_TR = UM_P1;                                 // prologue: f32 trace planes (13 KB)
 constexpr int UM_XST = UM_TR + 12 * PLS * 4;                 // prologue: staged x layers (16 KB), over halo
-constexpr int kSmemU = UM_EXP + 16;
+constexpr int kSmemU = UM_EXP + 32;
 static_assert(UM_XST + 2 * 256 * 8 * 4 <= UM_TAB, "prologue scratch must not reach the operator tables");
 
 __device__ __forceinline__ int hidx(int z, int y, int x) {
@@ -90,6 +90,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// CTA maximum of |v| without a shared word to reset (and so without a reset / atomic race): each warp
+// reduces its lanes (REDUX) and stores its slot; a barrier later, slots_max reads the 4 slots.  Non-positive
+// and NaN values are ignored, huge ones clamped (as smax in sf_common.cuh).  Deterministic.
+__device__ __forceinline__ void warp_max_store(int* slots, float v) {
+  const float a = fabsf(v);
+  const unsigned b = a > 0.f ? __float_as_uint(a < 3.0e38f ? a : 3.0e38f) : 0u;
+  const unsigned m = __reduce_max_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0) slots[threadIdx.x >> 5] = (int)m;
+}
+__device__ __forceinline__ float slots_max(const int* slots) {
+  const int4 s = *reinterpret_cast<const int4*>(slots);
+  return __int_as_float(max(max(s.x, s.y), max(s.z, s.w)));
+}
 
 __device__ __forceinline__ void ldsm4(unsigned (&r)[4], unsigned addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -131,15 +145,29 @@ __device__ __forceinline__ void hmma8(float (&d)[4], unsigned a0, unsigned a1, u
 // d = half(2048 (x - h))).  x - h is exact in f32 (one mixed-precision FHFMA per element).
 template <int MODE>
 __device__ __forceinline__ void demote_pair(float x0, float x1, unsigned& h, unsigned& d) {
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(h) : "f"(x1), "f"(x0));
   if constexpr (MODE == MODE_FP16_EC) {
-    float r0, r1;
-    asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n"
-        " fma.rn.f32.f16 %0, lo, %5, %3;\n fma.rn.f32.f16 %1, hi, %5, %4;\n}\n"
-        : "=f"(r0), "=f"(r1)
-        : "r"(h), "f"(x0), "f"(x1), "h"((unsigned short)0xBC00));  // -1.0 in binary16
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(d) : "f"(r1 * kEc), "f"(r0 * kEc));
+    // one block: the two residuals come out of the FHFMAs as a register pair, scaled by one packed
+    // FMUL2 (Blackwell f32x2) -- the same IEEE products as two FMULs
+    asm("{\n .reg .b16 lo, hi;\n .reg .f32 r0, r1;\n .reg .b64 rr;\n"
+        " cvt.rn.f16x2.f32 %0, %3, %2;\n mov.b32 {lo, hi}, %0;\n"
+        " fma.rn.f32.f16 r0, lo, %4, %2;\n fma.rn.f32.f16 r1, hi, %4, %3;\n"
+        " mov.b64 rr, {r0, r1};\n mul.rn.f32x2 rr, rr, %5;\n mov.b64 {r0, r1}, rr;\n"
+        " cvt.rn.f16x2.f32 %1, r1, r0;\n}\n"
+        : "=r"(h), "=r"(d)
+        : "f"(x0), "f"(x1), "h"((unsigned short)0xBC00),  // -1.0 in binary16
+          "l"(0x4500000045000000ull));                     // (2048, 2048)
+  } else {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(h) : "f"(x1), "f"(x0));
   }
+}
+
+// (v0, v1) = (c0, c1) * 2^-11 + (m0, m1): the EC recombination of two adjacent accumulator entries in one
+// packed FFMA2 (same IEEE results as two FFMAs)
+__device__ __forceinline__ void ec_combine2(float c0, float c1, float m0, float m1, float& v0, float& v1) {
+  asm("{\n .reg .b64 a, b, r;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n"
+      " fma.rn.f32x2 r, a, %6, b;\n mov.b64 {%0, %1}, r;\n}\n"
+      : "=f"(v0), "=f"(v1)
+      : "f"(c0), "f"(c1), "f"(m0), "f"(m1), "l"(0x3A0000003A000000ull));  // (2^-11, 2^-11)
 }
 
 // A 16-line x 16-output accumulator: two n8 tiles; EC keeps main and corr.
@@ -161,7 +189,10 @@ struct HAcc {
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[nt][i] = val(nt, i);
+      for (int i = 0; i < 4; i += 2) {
+        if constexpr (MODE == MODE_FP16_EC) ec_combine2(c[nt][i], c[nt][i + 1], m[nt][i], m[nt][i + 1], v[nt][i], v[nt][i + 1]);
+        else v[nt][i] = m[nt][i], v[nt][i + 1] = m[nt][i + 1];
+      }
   }
 };
 
@@ -261,7 +292,7 @@ template <int MODE>
 struct HTile {
   char* sm;
   unsigned s0;  // shared-window address of the smem base
-  int* s_exp;   // block-exponent words ([0] input, [1] residual)
+  int* s_exp;   // block-exponent slots, one per warp: [0..3] input, [4..7] residual (warp_max_store)
   int eu;       // input block exponent: u^ = 2^eu u
   int cx, cy, cz;
   int sy, sz;   // element strides of y and z (tile-local offsets stay below 16 sz < 2^31)
@@ -471,7 +502,6 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     const uint4 w = __ldg(&tab->halo[T.lane]);
     T.hb[0] = w.x; T.hb[1] = w.y; T.hb[2] = w.z; T.hb[3] = w.w;
   }
-  if (threadIdx.x == 0) T.s_exp[0] = T.s_exp[1] = 0;
   const int tid = threadIdx.x;
   const int sy = T.sy, sz = T.sz;
   const long long tile_base = (long long)(T.cz * KK) * sz + (long long)(T.cy * KK) * sy + T.cx * KK;
@@ -537,7 +567,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
       }
     }
   }
-  smax(&T.s_exp[0], mx);
+  warp_max_store(T.s_exp, mx);
   float cl[KK], chi[KK];  // beta coefficients: lo neighbour ucol, hi neighbour urow
 #pragma unroll
   for (int c = 0; c < KK; ++c) {
@@ -550,7 +580,7 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     }
   }
   __syncthreads();
-  T.eu = block_exp(__int_as_float(T.s_exp[0]));
+  T.eu = block_exp(slots_max(T.s_exp));
   const float us = pow2f(T.eu);
   __half* uh = reinterpret_cast<__half*>(smem + SM_UH);
   __half* ud = reinterpret_cast<__half*>(smem + SM_UD);
@@ -837,13 +867,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   ld_op(bv, tab->Vf[kz], T.lane);
   // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
   const float os = pow2f(-(op.sc.aA + T.eu));
+  float mx = 0.f;
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
                              {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
-    float mx = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
@@ -851,10 +881,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
         rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
         mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
       }
-    smax(&T.s_exp[1], mx);
   }
+  warp_max_store(T.s_exp + 4, mx);
   __syncthreads();  // all z-stage reads of U/B done, residual exponent complete
-  const int er = block_exp(__int_as_float(T.s_exp[1]));
+  const int er = block_exp(slots_max(T.s_exp + 4));
   const float rs = pow2f(er);
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
@@ -1294,13 +1324,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
   ld_op(bm, tab->M, T.lane);
   ld_op(bl, tab->L[T.kind[2]], T.lane);
   const float os = pow2f(-(op.sc.aA + T.eu));
+  float mx = 0.f;
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
     const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
                              {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
     z_lines<MODE>(T, y, bm, bl, rr[yy]);
-    float mx = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
@@ -1308,10 +1338,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
         rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
         mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
       }
-    smax(&T.s_exp[1], mx);
   }
+  warp_max_store(T.s_exp + 4, mx);
   __syncthreads();
-  const int er = block_exp(__int_as_float(T.s_exp[1]));
+  const int er = block_exp(slots_max(T.s_exp + 4));
   const float rs = pow2f(er);
   unsigned p0 = __ldg(&pt->PT[0][0][T.lane]), p1 = __ldg(&pt->PT[0][1][T.lane]);
   unsigned q0 = 0, q1 = 0;
