@@ -127,9 +127,19 @@ __global__ void k_dot_final(const double* __restrict__ part, double* __restrict_
 }
 
 // y = x / d elementwise (IEEE division, as the reference's V = [b / beta], w / h_next, krylov.py:57,106)
+// 16-byte accesses when both vectors are 16-byte aligned (the tail element, if any, by thread 0)
 __global__ void k_div(long long n, const double* __restrict__ x, double d, double* __restrict__ y) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = x[i] / d;
+  const long long stride = (long long)gridDim.x * blockDim.x, i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((((unsigned long long)x | (unsigned long long)y) & 15) == 0) {
+    const long long n2 = n >> 1;
+    for (long long i = i0; i < n2; i += stride) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(x) + i);
+      reinterpret_cast<double2*>(y)[i] = make_double2(v.x / d, v.y / d);
+    }
+    if ((n & 1) && i0 == 0) y[n - 1] = x[n - 1] / d;
+  } else {
+    for (long long i = i0; i < n; i += stride) y[i] = x[i] / d;
+  }
 }
 
 __global__ void k_axpy_dev(long long n, double sign, const double* __restrict__ coef, const double* __restrict__ x,

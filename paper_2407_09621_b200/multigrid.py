@@ -307,17 +307,21 @@ class MultigridPreconditioner:
         for _ in range(cfg.post_smooth_steps):
             self._smooth_device(level, x, b, mode)
 
-    def vcycle_device(self, x64: torch.Tensor, b64: torch.Tensor, level: int, out64: torch.Tensor):
-        """fp64 device in/out; conversion to the storage dtype only here (multigrid.py:257-266)."""
+    def vcycle_device(self, x64: torch.Tensor | None, b64: torch.Tensor, level: int, out64: torch.Tensor):
+        """fp64 device in/out; conversion to the storage dtype only here (multigrid.py:257-266).  x64 = None:
+        zero initial guess (the preconditioner's apply), written straight into the storage-dtype buffer."""
         mode = self.config.mode
-        if mode is PrecisionMode.FP64:
-            xs = self._buf("x", level, mode)
+        xs = self._buf("x", level, mode)
+        if x64 is None:
+            xs.zero_()
+        elif mode is PrecisionMode.FP64:
             xs.copy_(x64)
+        else:
+            device.convert(x64, xs)
+        if mode is PrecisionMode.FP64:
             bs = b64
         else:
-            xs = self._buf("x", level, mode)
             bs = self._buf("rhs", level, mode)
-            device.convert(x64, xs)
             device.convert(b64, bs)
         self._vcycle_device(level, xs, bs)
         device.convert(xs, out64)
@@ -344,8 +348,7 @@ class MultigridPreconditioner:
             if self.use_graph:
                 return self._apply_graph(bt, level)
             out = torch.empty_like(bt)
-            zero = self._zero64(bt.numel())
-            return self.vcycle_device(zero, bt, level, out)
+            return self.vcycle_device(None, bt, level, out)
         return self.vcycle(np.zeros(np.asarray(b).size), b, level)
 
     # ------------------------------------------------------- CUDA graph
@@ -364,26 +367,18 @@ class MultigridPreconditioner:
         if ent is None:
             b_in = torch.empty_like(b)
             out = torch.empty_like(b)
-            zero = self._zero64(b.numel())
             b_in.copy_(b)
-            self.vcycle_device(zero, b_in, level, out)  # warm-up: workspaces, tables, LU factors
+            self.vcycle_device(None, b_in, level, out)  # warm-up: workspaces, tables, LU factors
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.vcycle_device(zero, b_in, level, out)
+                self.vcycle_device(None, b_in, level, out)
             ent = (g, b_in, out)
             self._buffers[key] = ent
         g, b_in, out = ent
         b_in.copy_(b)
         g.replay()
         return out.clone()
-
-    def _zero64(self, n):
-        z = self._buffers.get(("zero64", n))
-        if z is None:
-            z = torch.zeros(n, dtype=torch.float64, device="cuda")
-            self._buffers[("zero64", n)] = z
-        return z
 
 
 __all__ = ["default_ordering", "VCycleConfig", "PatchSolver", "patch_inverse_apply", "restrict", "prolongate",

@@ -27,7 +27,8 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
 agg = collections.defaultdict(lambda: [0, 0.0])
 for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA:
-        name = e.name.split("(")[0].replace("void ", "")[:60]
+        name = e.name.replace("void ", "").replace("(anonymous namespace)::", "")
+        name = name.split("(")[0][:60] or e.name[:60]
         agg[name][0] += 1
         agg[name][1] += e.device_time_total / 1000.0 if hasattr(e, "device_time_total") else e.cuda_time_total / 1000.0
 tot = sum(v[1] for v in agg.values())
