@@ -62,7 +62,9 @@ constexpr int SM_TR = SM_BH;                      // 12 planes: (face * 2 + alph
 constexpr int SM_XST = SM_TR + 12 * PLS * 4;      // [hi][256 rows][KK <= 8] f32
 constexpr int SM_EXP_A = SM_HALO + 3 * 256 * 16, SM_EXP_B = SM_XST + 2 * 256 * 8 * 4;
 constexpr int SM_EXP = SM_EXP_A > SM_EXP_B ? SM_EXP_A : SM_EXP_B;
-constexpr int kSmem = SM_EXP + 32;  // exponent slots: [0..3] input, [4..7] residual (one per warp)
+constexpr int kSmem = SM_EXP + 32;
+constexpr int XOP = 260;  // colour pass: f32 x_old tile staged over the dead B buffers, z pitch (floats)
+static_assert(SM_BH + 16 * XOP * 4 <= SM_HALO, "x_old staging must fit the B buffers");  // exponent slots: [0..3] input, [4..7] residual (one per warp)
 // tcgen05 (UMMA) kernels: two operand buffers P0 / P1, each a binary16 main-half tensor and (at + UM_D)
 // the EC residual-half tensor in canonical no-swizzle layouts; halo words, operator B tables, the
 // mbarrier, the TMEM base and the exponent words after them.  During the prologue P1 and the halo
@@ -884,6 +886,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   }
   warp_max_store(T.s_exp + 4, mx);
   __syncthreads();  // all z-stage reads of U/B done, residual exponent complete
+  // Q7: the x_old tile -> the B buffers (dead from here on) by cp.async, so its latency hides behind the
+  // transforms instead of stalling the final stage ([z][y][x] f32, z pitch XOP: conflict-free final reads;
+  // EC smoothing step 8.62 -> 8.20 ms at Q7 l6).  The line tiles (KK < 8) keep the register loads across the
+  // last barrier (staging measured 2.6 % slower for Q3).
+  constexpr bool kStageXold = KK == 8;
+  float* xold = reinterpret_cast<float*>(smem + SM_BH);
+  if constexpr (kStageXold) {
+    const float* src = xo + base;
+#pragma unroll
+    for (int k2 = 0; k2 < 4096 / 4 / kThreads; ++k2) {
+      const int c = threadIdx.x + kThreads * k2, x4 = (c & 3) * 4, y = (c >> 2) & 15, z = c >> 6;
+      cp_async16(xold + z * XOP + y * 16 + x4, src + z * T.sz + y * T.sy + x4);
+    }
+  }
   const int er = block_exp(slots_max(T.s_exp + 4));
   const float rs = pow2f(er);
 #pragma unroll
@@ -979,12 +995,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
     }
     __syncwarp();
   }
-  // x_old values of this warp's final rows in flight across the barrier (L2 latency hidden behind it)
-  const float* xb = xo + base;
   float* nb = xn + base;
-  float xv4[4][2][4];
+  float xv4[kStageXold ? 1 : 4][2][4];
+  if constexpr (kStageXold) {
+    cp_async_wait_all();  // the staged x_old tile
+  } else {  // x_old values of this warp's final rows in flight across the barrier
 #pragma unroll
-  for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, xb, 4 * T.warp + yy, xv4[yy]);
+    for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, xo + base, 4 * T.warp + yy, xv4[yy]);
+  }
   __syncthreads();
   // z lines: backward V_z, x_new = x_old + correction (back to true units)
   ld_op(bv, tab->Vb[kz], T.lane);
@@ -992,7 +1010,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
-    const float (&xv)[2][4] = xv4[yy];
     HFrag a;
     ld_a<MODE>(a, T.UH(), T.UD(), T.oz(y), true);
     HAcc<MODE> acc;
@@ -1008,7 +1025,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
         for (int h8 = 0; h8 < 2; ++h8) {
           const int i = 2 * h8 + i1;
           if (KK < 8 && (T.g + 8 * h8 < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
-          p[8 * h8] = fmaf(acc.val(nt, i), cs, xv[nt][i]);
+          const float xv = kStageXold ? xold[z * XOP + y * 16 + T.g + 8 * h8] : xv4[kStageXold ? 0 : yy][nt][i];
+          p[8 * h8] = fmaf(acc.val(nt, i), cs, xv);
         }
       }
   }
