@@ -1367,7 +1367,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
     q0 = __ldg(&pt->PT[1][0][T.lane]);
     q1 = __ldg(&pt->PT[1][1][T.lane]);
   }
-  float* S1 = reinterpret_cast<float*>(smem + SM_UH);  // [zc][y][x], plane pitch 260
+  // restriction stages on the tensor cores: every stage contracts 16 fine points into 8 coarse ones with P^T
+  // (B fragments p / q), one m16 tile of lines per MMA; stage outputs are recombined (main + corr / 2048) and
+  // re-split by the next stage as the reference's per-contraction semantics do.
+  float* S1 = reinterpret_cast<float*>(smem + SM_UH);  // z stage out: [zc][y][x], y pitch 20, zc pitch 324
+  constexpr int S1Y = 20, S1Z = 324, S2R = 24;         // (conflict-free fragment stores and gathers)
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) {
     const int y = 4 * T.warp + yy;
@@ -1386,50 +1390,72 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int xx = T.g + 8 * (i >> 1), zc = 2 * T.t + (i & 1);
-      S1[zc * 260 + y * 16 + xx] = MODE == MODE_FP16_EC ? m[i] + c[i] / kEc : m[i];
+      S1[zc * S1Z + y * S1Y + xx] = MODE == MODE_FP16_EC ? m[i] + c[i] / kEc : m[i];
     }
   }
   __syncthreads();
-  float* S2 = reinterpret_cast<float*>(smem + SM_BH);  // [zc][yc][x]
-  {  // y lines (zc, x): 128 lines, one per thread
-    const int xx = threadIdx.x & 15, zc = threadIdx.x >> 4;
-    Op<MODE> w[16];
+  float* S2 = reinterpret_cast<float*>(smem + SM_BH);  // y stage out: [zc][yc][x], row (zc, yc) pitch 24
+  // y stage: lines (zc, x), one m16 tile (rows x) per zc plane, two planes per warp; k = y
 #pragma unroll
-    for (int y = 0; y < 16; ++y) w[y] = prep<MODE>(S1[zc * 260 + y * 16 + xx]);
+  for (int j = 0; j < 2; ++j) {
+    const int zc = 2 * T.warp + j;
+    const float* P1 = S1 + zc * S1Z;
+    float v[2][4];
 #pragma unroll
-    for (int yc = 0; yc < 8; ++yc) {
-      Acc<MODE> s;
+    for (int kb = 0; kb < 2; ++kb) {
+      const int y0 = 8 * kb + 2 * T.t;
+      v[kb][0] = P1[y0 * S1Y + T.g];
+      v[kb][1] = P1[(y0 + 1) * S1Y + T.g];
+      v[kb][2] = P1[y0 * S1Y + T.g + 8];
+      v[kb][3] = P1[(y0 + 1) * S1Y + T.g + 8];
+    }
+    HFrag a;
+    to_frag<MODE>(v, a);
+    float m[4] = {0.f, 0.f, 0.f, 0.f}, c[4] = {0.f, 0.f, 0.f, 0.f};
+    hmma16(m, a.h[0], a.h[1], a.h[2], a.h[3], p0, p1);
+    if constexpr (MODE == MODE_FP16_EC) {
+      hmma16(c, a.h[0], a.h[1], a.h[2], a.h[3], q0, q1);
+      hmma16(c, a.d[0], a.d[1], a.d[2], a.d[3], p0, p1);
+    }
 #pragma unroll
-      for (int y = 0; y < 16; ++y) {
-        ME<MODE> e;
-        e.h = __ldg(&pt->P[0][y][yc]);
-        if constexpr (MODE == MODE_FP16_EC) e.d = __ldg(&pt->P[1][y][yc]);
-        s.fma(e, w[y]);
-      }
-      S2[(zc * 8 + yc) * 16 + xx] = s.result();
+    for (int i = 0; i < 4; ++i) {  // row x = g + 8 (i >> 1), column yc = 2t + (i & 1)
+      const int xx = T.g + 8 * (i >> 1), yc = 2 * T.t + (i & 1);
+      S2[(zc * 8 + yc) * S2R + xx] = MODE == MODE_FP16_EC ? m[i] + c[i] / kEc : m[i];
     }
   }
   __syncthreads();
-  if (threadIdx.x < 64) {  // x lines (zc, yc) -> coarse (true units)
-    const int yc = threadIdx.x & 7, zc = threadIdx.x >> 3;
-    Op<MODE> w[16];
+  {  // x stage: lines (zc, yc), one m16 tile (zc = 2 warp + row / 8, yc = row % 8) per warp; k = x -> coarse
+    const float* R0 = S2 + (16 * T.warp + T.g) * S2R;
+    const float* R1 = R0 + 8 * S2R;
+    float v[2][4];
 #pragma unroll
-    for (int xx = 0; xx < 16; ++xx) w[xx] = prep<MODE>(S2[(zc * 8 + yc) * 16 + xx]);
+    for (int kb = 0; kb < 2; ++kb) {
+      const int x0 = 8 * kb + 2 * T.t;
+      const float2 a0 = *reinterpret_cast<const float2*>(R0 + x0), a1 = *reinterpret_cast<const float2*>(R1 + x0);
+      v[kb][0] = a0.x;
+      v[kb][1] = a0.y;
+      v[kb][2] = a1.x;
+      v[kb][3] = a1.y;
+    }
+    HFrag a;
+    to_frag<MODE>(v, a);
+    float m[4] = {0.f, 0.f, 0.f, 0.f}, c[4] = {0.f, 0.f, 0.f, 0.f};
+    hmma16(m, a.h[0], a.h[1], a.h[2], a.h[3], p0, p1);
+    if constexpr (MODE == MODE_FP16_EC) {
+      hmma16(c, a.h[0], a.h[1], a.h[2], a.h[3], q0, q1);
+      hmma16(c, a.d[0], a.d[1], a.d[2], a.d[3], p0, p1);
+    }
     const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
-    float* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
-                 (T.cx / 2) * KK;
     const float back = pow2f(-er);
 #pragma unroll
-    for (int xc = 0; xc < 8; ++xc) {
-      Acc<MODE> s;
-#pragma unroll
-      for (int xx = 0; xx < 16; ++xx) {
-        ME<MODE> e;
-        e.h = __ldg(&pt->P[0][xx][xc]);
-        if constexpr (MODE == MODE_FP16_EC) e.d = __ldg(&pt->P[1][xx][xc]);
-        s.fma(e, w[xx]);
-      }
-      out[xc] = s.result() * back;
+    for (int h8 = 0; h8 < 2; ++h8) {  // rows g (h8 = 0) and g + 8: zc = 2 warp + h8, yc = g; columns xc = 2t, 2t+1
+      const int zc = 2 * T.warp + h8, yc = T.g;
+      float* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
+                   (T.cx / 2) * KK + 2 * T.t;
+      const float r0 = MODE == MODE_FP16_EC ? m[2 * h8] + c[2 * h8] / kEc : m[2 * h8];
+      const float r1 = MODE == MODE_FP16_EC ? m[2 * h8 + 1] + c[2 * h8 + 1] / kEc : m[2 * h8 + 1];
+      out[0] = r0 * back;
+      out[1] = r1 * back;
     }
   }
 }
