@@ -1460,6 +1460,118 @@ __global__ void __launch_bounds__(kThreads, 4) k_resid_restrict_h8(const float* 
   }
 }
 
+// Prolongation + add on the tensor cores (multigrid.py:128-143, then x + e): one CTA per 16^3 fine tile = one
+// 8^3 block of coarse points; three stages z -> y -> x, each a 8 -> 16 contraction with the line embedding E
+// (blockdiag of the cell-pair embedding; m16n8k8 MMAs, EC correction stacked into one k16 MMA), the stage
+// outputs recombined and re-split per contraction; the x stage adds into the fine tile, which cp.async staged
+// into shared memory at the start.  Shared-memory pitches keep every fragment gather / store conflict-free.
+struct HETab {
+  unsigned B[2][2][32];  // [h / d][nt][lane]: E (16 fine x 8 coarse) as the m16n8k8 B operand, n = 8 nt + g
+};
+constexpr int PQ1Y = 12, PQ1Z = 100, PQ2Y = 8, PQ2Z = 132, PXY = 24, PXZ = 384;
+
+template <int MODE>
+__device__ __forceinline__ void prolong_mma(unsigned ah0, unsigned ah1, unsigned ad0, unsigned ad1,
+                                            const unsigned (&bh)[2], const unsigned (&bd)[2], float (&o)[2][4]) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    float m[4] = {0.f, 0.f, 0.f, 0.f};
+    hmma8(m, ah0, ah1, bh[nt]);
+    if constexpr (MODE == MODE_FP16_EC) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      hmma16(c, ah0, ah1, ad0, ad1, bd[nt], bh[nt]);
+      ec_combine2(c[0], c[1], m[0], m[1], o[nt][0], o[nt][1]);
+      ec_combine2(c[2], c[3], m[2], m[3], o[nt][2], o[nt][3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[nt][i] = m[i];
+    }
+  }
+}
+
+template <int MODE, int KK>
+__global__ void __launch_bounds__(kThreads) k_prolong_h8(const float* __restrict__ ec, float* __restrict__ fine,
+                                                         int ncx, int ncy, int ncz, const HETab* __restrict__ et) {
+  __shared__ float Q1[16 * PQ1Z];                 // z stage out [z][yc][xc]
+  __shared__ float Q2[16 * PQ2Z];                 // y stage out [z][y][xc]
+  __shared__ __align__(16) float X[16 * PXZ];     // fine tile [z][y][x]
+  __shared__ __align__(16) int slots[4];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const long long csy = (long long)ncx * KK, csz = csy * (long long)ncy * KK;
+  const long long fsy = 2 * csy, fsz = 2 * fsy * (long long)ncy * KK;
+  const float* eb = ec + (long long)(8 * blockIdx.z) * csz + (long long)(8 * blockIdx.y) * csy + 8 * blockIdx.x;
+  float* fb = fine + (long long)(16 * blockIdx.z) * fsz + (long long)(16 * blockIdx.y) * fsy + 16 * blockIdx.x;
+#pragma unroll
+  for (int k2 = 0; k2 < 1024 / kThreads; ++k2) {  // the fine tile -> X (consumed by the x stage)
+    const int c = tid + kThreads * k2, ch = c & 3, row = c >> 2, y = row & 15, z = row >> 4;
+    cp_async16(X + z * PXZ + y * PXY + 4 * ch, fb + z * fsz + y * fsy + 4 * ch);
+  }
+  unsigned bh[2], bd[2];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    bh[nt] = __ldg(&et->B[0][nt][lane]);
+    bd[nt] = MODE == MODE_FP16_EC ? __ldg(&et->B[1][nt][lane]) : 0u;
+  }
+  // z stage: lines (yc, xc) = rows 16 w + g (yc = 2 w) and + 8 (yc = 2 w + 1), xc = g; k = zc
+  float v[4];
+#pragma unroll
+  for (int h8 = 0; h8 < 2; ++h8)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) v[2 * h8 + j] = __ldg(eb + (2 * t + j) * csz + (2 * w + h8) * csy + g);
+  warp_max_store(slots, fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))));
+  __syncthreads();
+  const int eu = block_exp(slots_max(slots));
+  const float us = pow2f(eu);
+  unsigned ah0, ah1, ad0 = 0u, ad1 = 0u;
+  demote_pair<MODE>(v[0] * us, v[1] * us, ah0, ad0);
+  demote_pair<MODE>(v[2] * us, v[3] * us, ah1, ad1);
+  float o[2][4];
+  prolong_mma<MODE>(ah0, ah1, ad0, ad1, bh, bd, o);
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Q1[(8 * nt + 2 * t + (i & 1)) * PQ1Z + (2 * w + (i >> 1)) * PQ1Y + g] = o[nt][i];
+  __syncthreads();
+  // y stage: lines (z, xc) = rows g (z = 2 j) and g + 8 (z = 2 j + 1), xc = g; k = yc; two tiles per warp
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const int z0 = 2 * (2 * w + jj);
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) v[2 * h8 + j] = Q1[(z0 + h8) * PQ1Z + (2 * t + j) * PQ1Y + g];
+    demote_pair<MODE>(v[0], v[1], ah0, ad0);
+    demote_pair<MODE>(v[2], v[3], ah1, ad1);
+    prolong_mma<MODE>(ah0, ah1, ad0, ad1, bh, bd, o);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Q2[(z0 + (i >> 1)) * PQ2Z + (8 * nt + 2 * t + (i & 1)) * PQ2Y + g] = o[nt][i];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // x stage: lines (z, y) = rows g (y = g) and g + 8, one z plane per tile, four per warp; k = xc; += fine
+  const float back = pow2f(-eu);
+#pragma unroll 1
+  for (int zz = 0; zz < 4; ++zz) {
+    const int z = 4 * w + zz;
+    const float2 a0 = *reinterpret_cast<const float2*>(Q2 + z * PQ2Z + g * PQ2Y + 2 * t);
+    const float2 a1 = *reinterpret_cast<const float2*>(Q2 + z * PQ2Z + (g + 8) * PQ2Y + 2 * t);
+    demote_pair<MODE>(a0.x, a0.y, ah0, ad0);
+    demote_pair<MODE>(a1.x, a1.y, ah1, ad1);
+    prolong_mma<MODE>(ah0, ah1, ad0, ad1, bh, bd, o);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        const int y = g + 8 * h8, x = 8 * nt + 2 * t;
+        const float2 xo = *reinterpret_cast<const float2*>(X + z * PXZ + y * PXY + x);
+        *reinterpret_cast<float2*>(fb + z * fsz + y * fsy + x) =
+            make_float2(fmaf(o[nt][2 * h8], back, xo.x), fmaf(o[nt][2 * h8 + 1], back, xo.y));
+      }
+  }
+}
+
 // ------------------------------------------------------------- host side
 static unsigned short half_bits(float x) {
   const __half h = __float2half_rn(x);
@@ -1832,7 +1944,66 @@ static int resid_restrict_t(const Geom& g0, const double* opd, const double* emb
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+static std::vector<std::pair<std::vector<double>, void*>> g_ecache;
+
+static const HETab* etables(int mode, const double* embd_raw, int KK) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(embd_raw, embd_raw + 2 * KK * KK);
+  key.push_back((double)dev);
+  key.push_back((double)mode);
+  key.push_back((double)KK);
+  double E[16 * 8] = {};  // 16-point fine line <- 8 coarse points
+  for (int c = 0; c < 16 / (2 * KK); ++c)
+    for (int i = 0; i < 2 * KK; ++i)
+      for (int j = 0; j < KK; ++j) E[(c * 2 * KK + i) * 8 + c * KK + j] = embd_raw[i * KK + j];
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& e : g_ecache)
+    if (e.first == key) return reinterpret_cast<const HETab*>(e.second);
+  HETab t;
+  std::memset(&t, 0, sizeof(t));
+  for (int nt = 0; nt < 2; ++nt)
+    for (int ln = 0; ln < 32; ++ln) {
+      const int n = 8 * nt + (ln >> 2), k0 = 2 * (ln & 3);
+      unsigned short h0, d0, h1, d1;
+      split_host(mode, E[n * 8 + k0], h0, d0);
+      split_host(mode, E[n * 8 + k0 + 1], h1, d1);
+      t.B[0][nt][ln] = (unsigned)h0 | ((unsigned)h1 << 16);
+      t.B[1][nt][ln] = (unsigned)d0 | ((unsigned)d1 << 16);
+    }
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(HETab)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &t, sizeof(HETab), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_ecache.push_back({std::move(key), d});
+  return reinterpret_cast<const HETab*>(d);
+}
+
+template <int MODE, int KK>
+static int prolong_t(int ncx, int ncy, int ncz, const double* embd, const void* e, void* fine, cudaStream_t st) {
+  if ((ncx * KK) % 8 || (ncy * KK) % 8 || (ncz * KK) % 8 || ncz * KK / 8 > 65535 || ncy * KK / 8 > 65535)
+    return kUseGeneric;
+  const HETab* et = etables(MODE, embd, KK);
+  if (!et) return -3;
+  const dim3 grid(ncx * KK / 8, ncy * KK / 8, ncz * KK / 8);
+  k_prolong_h8<MODE, KK><<<grid, kThreads, 0, st>>>((const float*)e, (float*)fine, ncx, ncy, ncz, et);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 }  // namespace hm
+
+int launch_prolong_hmma(int mode, int k_nodes, int ncx, int ncy, int ncz, const double* embd, const void* e,
+                        void* fine, cudaStream_t st) {
+  const bool ec = mode == MODE_FP16_EC;
+  switch (k_nodes) {
+    case 8: return ec ? hm::prolong_t<MODE_FP16_EC, 8>(ncx, ncy, ncz, embd, e, fine, st)
+                      : hm::prolong_t<MODE_FP16, 8>(ncx, ncy, ncz, embd, e, fine, st);
+    case 4: return ec ? hm::prolong_t<MODE_FP16_EC, 4>(ncx, ncy, ncz, embd, e, fine, st)
+                      : hm::prolong_t<MODE_FP16, 4>(ncx, ncy, ncz, embd, e, fine, st);
+    case 2: return ec ? hm::prolong_t<MODE_FP16_EC, 2>(ncx, ncy, ncz, embd, e, fine, st)
+                      : hm::prolong_t<MODE_FP16, 2>(ncx, ncy, ncz, embd, e, fine, st);
+    default: return kUseGeneric;
+  }
+}
 
 int launch_vmult_hmma_line(int mode, int k_nodes, const Geom& g, const double* opd, const void* u, void* v, int batch,
                            cudaStream_t st) {

@@ -855,6 +855,12 @@ static int launch_resid_restrict(const sf_grid* gr, const double* opd, const dou
 template <int K, int MODE>
 static int launch_prolong_add(const sf_grid* coarse, const double* embd, const void* e, void* fine, cudaStream_t st) {
   if (!coarse || coarse->nx < 1 || coarse->ny < 1 || coarse->nz < 1) return fail(SF_EINVAL, "bad coarse grid");
+  if constexpr ((K == 8 || K == 4 || K == 2) && (MODE == MODE_FP16 || MODE == MODE_FP16_EC)) {
+    if (!use_generic()) {
+      const int r = launch_prolong_hmma(MODE, K, coarse->nx, coarse->ny, coarse->nz, embd, e, fine, st);
+      if (r != kUseGeneric) return r ? check_launch("sf_prolongate_add (hmma)") : SF_OK;
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   constexpr int B = 2 * K;
   using S = typename MT<MODE>::S;
