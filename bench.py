@@ -189,8 +189,9 @@ def main():
     from paper_2407_09621_b200.discretization import vmult_device
 
     local = int(os.environ.get("LOCAL_RANK", 0))
-    # SUMFACT_B200_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the N>1 path on a 1-GPU box)
-    shared = os.environ.get("SUMFACT_B200_SHARE_GPU") == "1"
+    # SUMFACT_B200_SHARE_GPU=1, or more ranks than visible GPUs: every rank on cuda:0 over gloo (exercises the
+    # N>1 path on a 1-GPU box; the throughput of such a run is not a scaling number)
+    shared = os.environ.get("SUMFACT_B200_SHARE_GPU") == "1" or world > torch.cuda.device_count()
     if shared:
         local = 0
     torch.cuda.set_device(local)
@@ -321,7 +322,8 @@ def main():
            "config": {"workload": f"Q{k} DG-SIPG Laplace vmult, fp64, {n}x{n}x{n * world} cells "
                                   f"({world * D} DoF; {D} per GPU)",
                       "degree": k, "level": lvl, "dofs_per_gpu": D,
-                      "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                      "parallelism": (f"z-slab x{world}" + (" (ranks sharing one GPU over gloo: not a scaling point)"
+                                                             if shared else "")) if world > 1 else "single GPU",
                       "l2_flush": f"not needed: u, v = 2 x {8 * D / 1e9:.2f} GB per GPU >> 126 MB L2"},
            "tflops_reference_equivalent": value * 1e9 * ref_flops_per_dof(k, lvl) / 1e12,
            "roofline": roofline, "clocks": clk,
