@@ -74,7 +74,10 @@ int sf_vmult_zrange(int mode, int k, const sf_grid* grid, int z0, int z1, const 
 
 /* One colour of the multiplicative vertex-patch smoother: x_new = x_old + sum over
  * the colour's patches of P^-1 (b - A x_old)|patch; uncovered cells copied.
- * shift[i] in {0,1} along tensor axis i (x = 0).  x_old != x_new.
+ * shift[i] in {0,1} along tensor axis i (x = 0).  x_old != x_new.  x_old = NULL: the current iterate is zero
+ * (a V-cycle's first, unshifted colour): r = b, no operator application, bitwise the pass on a zero vector;
+ * SF_EINVAL for a shifted colour, SF_EUNSUPPORTED where only the generic kernel applies (degrees other than
+ * 7 / 3 / 1, grids the tensor-core tiles do not cover) -- the caller then passes the zero vector.
  * Replaces one iteration of the colour loop of MultigridPreconditioner.smooth
  *                                                          multigrid.py:186-203 (PatchSolver.apply_batch :71-83). */
 int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, const double* level_op,

@@ -160,7 +160,9 @@ __device__ __forceinline__ void full_group(const double (*l)[4], const double* a
 // V_x (registers) | V_y | V_z -> +x_old -> HBM; '|' = shared-memory transpose.
 // KK = 8: one patch per tile line; KK = 4 / 2: a 16-point line holds 2 / 4 patches and the
 // transforms are blockdiag(V_patch) (line tables built per line boundary kind).
-template <int KK = 8, class S = double>
+// XZ: zero current iterate (x_old = NULL: the first, unshifted colour of a V-cycle's pre-smoothing): r = b, the
+// operator stages and the x_old reads are skipped; bitwise the full pass on a zero vector.
+template <int KK = 8, class S = double, bool XZ = false>
 __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict__ xo,
                                                             const S* __restrict__ b, S* __restrict__ xn,
                                                             Geom g, LevelOp<KK, MODE_FP64> op,
@@ -169,20 +171,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict
   Tile T;
   int batch;
   if (!tile_setup_band<KK>(T, smem, g, bd, batch)) return;
-  prefetch_tile_rows_l2<KK>(T, b);
-  prefetch_ahead_l2<KK>(g, bd, T, xo);
   Frags f;
   Halo h;
-  init_frags<KK>(T, op, f, h);
-  prologue_fast<KK>(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-  xy_stages<S>(T, f, h);
-  __syncthreads();
+  if constexpr (!XZ) {
+    prefetch_tile_rows_l2<KK>(T, b);
+    prefetch_ahead_l2<KK>(g, bd, T, xo);
+    init_frags<KK>(T, op, f, h);
+    prologue_fast<KK>(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
+    xy_stages<S>(T, f, h);
+    __syncthreads();
+  }
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
   const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   double V[2][4];
   // ---- z lines: residual and forward V_z^T (chained in registers), out in T layout
-  load_l(T, f, kz);
+  if constexpr (!XZ) load_l(T, f, kz);
   load_frag(&tab->Vfp[kz][0][0], V, lane);
   {
     double t[2][2][2][2];
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict
       const int y = 2 * w + yy;
 #pragma unroll
       for (int g8 = 0; g8 < 2; ++g8) {
-        double acc[2][2];
-        z_group(T, f, h, y, 8 * g8, acc);
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        if constexpr (!XZ) z_group(T, f, h, y, 8 * g8, acc);
         const int x = 8 * g8 + r;
         double a[4];
 #pragma unroll
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict
           const int z = 8 * nb + c2 + i;
           if (KK < 8 && (x < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
           const long long o = off0 + (long long)z * T.sz + (long long)y * T.sy + x;
-          xn[o] = (S)((double)__ldg(xo + o) + rd<S>(acc[nb][i]));
+          xn[o] = (S)((XZ ? 0.0 : (double)__ldg(xo + o)) + rd<S>(acc[nb][i]));
         }
     }
   }
@@ -644,6 +648,9 @@ static int launch_colour_line(const Geom& g0, const double* opd, const double* e
     kern<<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op, tab, bd);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
+  if (!xo)  // zero iterate (unshifted colour only; checked by the caller)
+    return f32 ? go(k_colour_dmma<KK, float, true>, (const float*)nullptr)
+               : go(k_colour_dmma<KK, double, true>, (const double*)nullptr);
   return f32 ? go(k_colour_dmma<KK, float>, (const float*)nullptr)
              : go(k_colour_dmma<KK, double>, (const double*)nullptr);
 }
@@ -798,6 +805,9 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
                                                                          tab, bd);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
+  if (!xo)  // zero iterate (unshifted colour only; checked by the caller)
+    return f32 ? go(dm::k_colour_dmma<8, float, true>, (const float*)nullptr)
+               : go(dm::k_colour_dmma<8, double, true>, (const double*)nullptr);
   return f32 ? go(dm::k_colour_dmma<8, float>, (const float*)nullptr)
              : go(dm::k_colour_dmma<8, double>, (const double*)nullptr);
 }

@@ -456,9 +456,8 @@ __device__ __forceinline__ bool band_tile_id(const Geom& g, const dm::Band& bd, 
 // KK = cell size: 8 (2-cell tiles) or 4 / 2 (16-point tile lines of 4 / 8 cells).
 // Tile order: the banded 3-D grid of the FP64 kernels (dm::band_tile, no integer divisions).
 template <int MODE, int KK = K, bool UM = false>
-__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const dm::Band& bd,
-                                           const LevelOp<KK, MODE>& op, const HTables* tab, const float*& u,
-                                           int& batch, const float* __restrict__ pf = nullptr, int tile_id = -1) {
+__device__ __forceinline__ bool tile_setup(HTile<MODE>& T, char* smem, const Geom& g, const dm::Band& bd,
+                                           const HTables* tab, int& batch, int tile_id = -1) {
   constexpr int CPL = 16 / KK;
   int tx, ty, tz;
   if (tile_id < 0) {
@@ -466,7 +465,6 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
   } else if (!band_tile_id(g, bd, tile_id, tx, ty, tz, batch)) {
     return false;
   }
-  u += (long long)batch * g.batch_stride;
   T.sm = smem;
   T.s0 = smem_u32(smem);
   T.s_exp = reinterpret_cast<int*>(smem + (UM ? UM_EXP : SM_EXP));
@@ -504,6 +502,16 @@ __device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geo
     const uint4 w = __ldg(&tab->halo[T.lane]);
     T.hb[0] = w.x; T.hb[1] = w.y; T.hb[2] = w.z; T.hb[3] = w.w;
   }
+  return true;
+}
+
+template <int MODE, int KK = K, bool UM = false>
+__device__ __forceinline__ bool tile_front(HTile<MODE>& T, char* smem, const Geom& g, const dm::Band& bd,
+                                           const LevelOp<KK, MODE>& op, const HTables* tab, const float*& u,
+                                           int& batch, const float* __restrict__ pf = nullptr, int tile_id = -1) {
+  constexpr int CPL = 16 / KK;
+  if (!tile_setup<MODE, KK, UM>(T, smem, g, bd, tab, batch, tile_id)) return false;
+  u += (long long)batch * g.batch_stride;
   const int tid = threadIdx.x;
   const int sy = T.sy, sz = T.sz;
   const long long tile_base = (long long)(T.cz * KK) * sz + (long long)(T.cy * KK) * sy + T.cx * KK;
@@ -845,7 +853,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_vmult_h8(const float* __restric
 
 // smoother colour pass: residual r = b - A x on the tile, fast-diagonalisation patch solve
 // V (x3) Lambda^-1 V^T (x3) r, x_new = x_old + correction (sf_dmma.cu k_colour_dmma8 stage order)
-template <int MODE, int KK = K>
+// XZ: the current iterate is zero (the first, unshifted colour of a V-cycle's pre-smoothing, x_old = NULL in
+// sf_smooth_colour): r = b - A 0 = b exactly, so the operator stages and the x_old reads are skipped; the
+// results are bitwise those of the full pass on a zero vector.
+template <int MODE, int KK = K, bool XZ = false>
 __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restrict__ xo, const float* __restrict__ b,
                                                           float* __restrict__ xn, Geom g, dm::Band bd,
                                                           LevelOp<KK, MODE> op, const HTables* __restrict__ tab,
@@ -854,35 +865,50 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   constexpr bool kBDV = KK < 8;  // Q3 / Q1: the line transform is blockdiag of the patches' V
   HTile<MODE> T;
   int batch;
-  const float* xin = xo;
-  if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
+  if constexpr (XZ) {
+    if (!tile_setup<MODE, KK>(T, smem, g, bd, tab, batch)) return;
+  } else {
+    const float* xin = xo;
+    if (!tile_front<MODE, KK>(T, smem, g, bd, op, tab, xin, batch, b)) return;
+  }
   const int kx = T.kind[0], ky = T.kind[1], kz = T.kind[2];
   const long long base = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
   const float* bb = b + base;
   float rr[4][2][4];  // b of this warp's rows (in flight across the barrier), then the residual
 #pragma unroll
   for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, bb, 4 * T.warp + yy, rr[yy]);
-  __syncthreads();
-  HOpFrag bm, bl, bv;
-  ld_op(bm, tab->M, T.lane);
-  ld_op(bl, tab->L[kz], T.lane);
-  ld_op(bv, tab->Vf[kz], T.lane);
-  // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
-  const float os = pow2f(-(op.sc.aA + T.eu));
+  HOpFrag bv;
   float mx = 0.f;
+  if constexpr (XZ) {
 #pragma unroll
-  for (int yy = 0; yy < 4; ++yy) {
-    const int y = 4 * T.warp + yy;
-    const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
-                             {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
-    z_lines<MODE>(T, y, bm, bl, rr[yy]);
+    for (int yy = 0; yy < 4; ++yy)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
-        mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
-      }
+        for (int i = 0; i < 4; ++i) mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
+    ld_op(bv, tab->Vf[kz], T.lane);
+  } else {
+    __syncthreads();
+    HOpFrag bm, bl;
+    ld_op(bm, tab->M, T.lane);
+    ld_op(bl, tab->L[kz], T.lane);
+    ld_op(bv, tab->Vf[kz], T.lane);
+    // z lines: residual r = b - A x (true units) -> block exponent -> forward V_z^T in registers
+    const float os = pow2f(-(op.sc.aA + T.eu));
+#pragma unroll
+    for (int yy = 0; yy < 4; ++yy) {
+      const int y = 4 * T.warp + yy;
+      const float bvv[2][4] = {{rr[yy][0][0], rr[yy][0][1], rr[yy][0][2], rr[yy][0][3]},
+                               {rr[yy][1][0], rr[yy][1][1], rr[yy][1][2], rr[yy][1][3]}};
+      z_lines<MODE>(T, y, bm, bl, rr[yy]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          rr[yy][nt][i] = fmaf(-rr[yy][nt][i], os, bvv[nt][i]);
+          mx = fmaxf(mx, fabsf(rr[yy][nt][i]));
+        }
+    }
   }
   warp_max_store(T.s_exp + 4, mx);
   __syncthreads();  // all z-stage reads of U/B done, residual exponent complete
@@ -890,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
   // transforms instead of stalling the final stage ([z][y][x] f32, z pitch XOP: conflict-free final reads;
   // EC smoothing step 8.62 -> 8.20 ms at Q7 l6).  The line tiles (KK < 8) keep the register loads across the
   // last barrier (staging measured 2.6 % slower for Q3).
-  constexpr bool kStageXold = KK == 8;
+  constexpr bool kStageXold = KK == 8 && !XZ;
   float* xold = reinterpret_cast<float*>(smem + SM_BH);
   if constexpr (kStageXold) {
     const float* src = xo + base;
@@ -996,10 +1022,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
     __syncwarp();
   }
   float* nb = xn + base;
-  float xv4[kStageXold ? 1 : 4][2][4];
+  float xv4[kStageXold || XZ ? 1 : 4][2][4];
   if constexpr (kStageXold) {
     cp_async_wait_all();  // the staged x_old tile
-  } else {  // x_old values of this warp's final rows in flight across the barrier
+  } else if constexpr (!XZ) {  // x_old values of this warp's final rows in flight across the barrier
 #pragma unroll
     for (int yy = 0; yy < 4; ++yy) ld_row<MODE>(T, xo + base, 4 * T.warp + yy, xv4[yy]);
   }
@@ -1025,7 +1051,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_colour_h8(const float* __restri
         for (int h8 = 0; h8 < 2; ++h8) {
           const int i = 2 * h8 + i1;
           if (KK < 8 && (T.g + 8 * h8 < T.skip[0] || y < T.skip[1] || z < T.skip[2])) continue;
-          const float xv = kStageXold ? xold[z * XOP + y * 16 + T.g + 8 * h8] : xv4[kStageXold ? 0 : yy][nt][i];
+          const float xv = XZ ? 0.f : kStageXold ? xold[z * XOP + y * 16 + T.g + 8 * h8]
+                                                 : xv4[kStageXold || XZ ? 0 : yy][nt][i];
           p[8 * h8] = fmaf(acc.val(nt, i), cs, xv);
         }
       }
@@ -1880,8 +1907,14 @@ static int colour_t(const Geom& g0, const double* opd, const double* eigd, const
   const HTables* tab = tables(MODE, opd, eigd, KK, &den);
   if (!tab || !den) return -3;
   auto op = pack_op_h<MODE, KK>(opd, eigd);
-  if (!smem_attr(k_colour_h8<MODE, KK>)) return -3;
   const dm::Band bd = dm::make_band(g);
+  if (!xo) {  // zero iterate (unshifted colour only; checked by the caller)
+    if (!smem_attr(k_colour_h8<MODE, KK, true>)) return -3;
+    k_colour_h8<MODE, KK, true><<<band_grid(g, bd, 1), kThreads, kSmem, st>>>(nullptr, (const float*)b, (float*)xn,
+                                                                              g, bd, op, tab, den);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  }
+  if (!smem_attr(k_colour_h8<MODE, KK>)) return -3;
   k_colour_h8<MODE, KK><<<band_grid(g, bd, 1), kThreads, kSmem, st>>>((const float*)xo, (const float*)b, (float*)xn,
                                                                       g, bd, op, tab, den);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;

@@ -727,6 +727,7 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
   }
   if (g.ntx < 1 || g.nty < 1 || g.ntz < 1) {
     if (!copy) return SF_OK;
+    if (!xo) return fail(SF_EUNSUPPORTED, "zero-iterate colour pass on a grid without patches");
     // colour without patches: x_new = x_old
     size_t bytes = (size_t)gr->nx * gr->ny * gr->nz * K * K * K * sizeof(S);
     if (cudaMemcpyAsync(xn, xo, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -768,6 +769,7 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
     }
   }
   if (!done) {
+    if (!xo) return fail(SF_EUNSUPPORTED, "zero-iterate colour pass: this grid takes the generic kernel");
     Prepared<K, MODE> pr(opd, eigd);
     auto op = pack_op<K, MODE>(pr.opd);
     op.sc = pr.sc;
@@ -976,12 +978,17 @@ int sf_smooth_colour(int mode, int k, const sf_grid* grid, const int* shift, con
                      const double* patch_eig, const void* x_old, const void* b, void* x_new, void* stream) {
   int rc = check_common(mode, k);
   if (rc) return rc;
-  if (!shift || !x_old || !b || !x_new || !level_op || !patch_eig) return fail(SF_EINVAL, "null pointer");
+  if (!shift || !b || !x_new || !level_op || !patch_eig) return fail(SF_EINVAL, "null pointer");
   SF_ALIGNED(x_old, b, x_new);
   if (misaligned_grid(grid)) return fail(SF_EINVAL, "ghost planes must be 16-byte aligned");
   for (int i = 0; i < 3; ++i)
     if (shift[i] != 0 && shift[i] != 1) return fail(SF_EINVAL, "shift entries must be 0 or 1");
   if (x_old == x_new) return fail(SF_EINVAL, "x_old and x_new must be distinct buffers");
+  if (!x_old) {  // zero current iterate: only the unshifted colour (every cell covered), only the tensor-core paths
+    if (shift[0] || shift[1] || shift[2]) return fail(SF_EINVAL, "x_old may be NULL only for the unshifted colour");
+    if (!(k == 7 || k == 3 || k == 1) || use_generic())
+      return fail(SF_EUNSUPPORTED, "zero-iterate colour pass: Q7 / Q3 / Q1 tensor-core kernels only");
+  }
   cudaStream_t st = (cudaStream_t)stream;
 #define CALL(K, M) launch_colour<K, M>(grid, shift, level_op, patch_eig, x_old, b, x_new, st)
   SF_DISPATCH(k, mode, CALL);

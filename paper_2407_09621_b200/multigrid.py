@@ -198,8 +198,11 @@ class MultigridPreconditioner:
         return t
 
     # ------------------------------------------------------------ smoother
-    def _smooth_device(self, level: int, x: torch.Tensor, b: torch.Tensor, mode: PrecisionMode):
-        """One multiplicative sweep in place on device x (multigrid.py:172-204)."""
+    def _smooth_device(self, level: int, x: torch.Tensor, b: torch.Tensor, mode: PrecisionMode,
+                       x_zero: bool = False):
+        """One multiplicative sweep in place on device x (multigrid.py:172-204).  x_zero: x is known to be zero
+        (a V-cycle's first pre-smoothing step); an unshifted first colour then runs the zero-iterate kernel
+        (r = b: no operator application, no x_old reads), bitwise the same result."""
         hier = self.hier
         n = hier.n_cells(level)
         lm = hier.matrices(level)
@@ -208,14 +211,20 @@ class MultigridPreconditioner:
         cur, nxt = x, tmp
         L = _native.lib()
         g = hier.grid(level)
+        first = True
         for shift in self.config.smoother_ordering:
             if min(n // 2 - s for s in shift) < 1:
                 continue
-            rc = L.sf_smooth_colour(mode.code, hier.degree, g, self._shift_arrays[shift],
-                                    _native.host_ptr(lm.cell_op), _native.host_ptr(table), device.ptr(cur),
-                                    device.ptr(b), device.ptr(nxt), device.stream_ptr())
+            args = (mode.code, hier.degree, g, self._shift_arrays[shift], _native.host_ptr(lm.cell_op),
+                    _native.host_ptr(table))
+            rc = _native.SF_EUNSUPPORTED
+            if first and x_zero and not any(shift):
+                rc = L.sf_smooth_colour(*args, None, device.ptr(b), device.ptr(nxt), device.stream_ptr())
+            if rc == _native.SF_EUNSUPPORTED:
+                rc = L.sf_smooth_colour(*args, device.ptr(cur), device.ptr(b), device.ptr(nxt), device.stream_ptr())
             _native.check(rc, "sf_smooth_colour")
             cur, nxt = nxt, cur
+            first = False
         if cur is not x:
             x.copy_(cur)
 
@@ -289,20 +298,20 @@ class MultigridPreconditioner:
         return device.to_host(x, mode.storage_dtype) if host else x
 
     # --------------------------------------------------------------- V-cycle
-    def _vcycle_device(self, level: int, x: torch.Tensor, b: torch.Tensor):
-        """multigrid.py:243-255, in place on device x (storage dtype)."""
+    def _vcycle_device(self, level: int, x: torch.Tensor, b: torch.Tensor, x_zero: bool = False):
+        """multigrid.py:243-255, in place on device x (storage dtype); x_zero: x is zero on entry."""
         cfg = self.config
         mode = cfg.mode
         if level == cfg.coarse_level:
             x.copy_(self._coarse_solve_device(b, mode))
             return
-        for _ in range(cfg.pre_smooth_steps):
-            self._smooth_device(level, x, b, mode)
+        for i in range(cfg.pre_smooth_steps):
+            self._smooth_device(level, x, b, mode, x_zero=x_zero and i == 0)
         rc = self._buf("rhs", level - 1, mode)
         restrict_device(self.hier, level, b, rc, mode, x=x)
         e = self._buf("x", level - 1, mode)
         e.zero_()
-        self._vcycle_device(level - 1, e, rc)
+        self._vcycle_device(level - 1, e, rc, x_zero=True)
         prolongate_add_device(self.hier, level - 1, e, x, mode)
         for _ in range(cfg.post_smooth_steps):
             self._smooth_device(level, x, b, mode)
@@ -323,7 +332,7 @@ class MultigridPreconditioner:
         else:
             bs = self._buf("rhs", level, mode)
             device.convert(b64, bs)
-        self._vcycle_device(level, xs, bs)
+        self._vcycle_device(level, xs, bs, x_zero=x64 is None)
         device.convert(xs, out64)
         return out64
 

@@ -100,6 +100,9 @@ def test_vector_entry_points_validate_with_messages():
         ("sf_dense_apply", lambda: L.sf_dense_apply(8, None, out, 0, 0, out, 0, None), "null"),
         ("sf_dense_apply", lambda: L.sf_dense_apply(8, out, out, 2, 0, out, 0, None), "dtype"),
         ("sf_convert", lambda: L.sf_convert(4, out, 3, out, 0, None), "dtype"),
+        ("sf_smooth_colour", lambda: L.sf_smooth_colour(3, 7, _native.SfGrid(4, 4, 4, None, None),
+                                                        (ctypes.c_int * 3)(1, 0, 0), out, out, None, out,
+                                                        ctypes.c_void_p(32), None), "unshifted colour"),
     ]
     for name, call, frag in cases:
         assert call() == _native.SF_EINVAL, name

@@ -52,3 +52,41 @@ def test_solve_bitwise_reproducible(mode):
     b = sf.run_solve(3, 5, mode, keep_solution=True)
     assert a.report.residual_history == b.report.residual_history
     assert torch.equal(torch.as_tensor(a.x), torch.as_tensor(b.x))
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 4), (3, 5), (1, 6), (2, 3)])
+def test_zero_iterate_colour_pass_is_bitwise_the_full_pass(k, lvl):
+    """sf_smooth_colour with x_old = NULL (the V-cycle's first unshifted colour on a zero iterate) against the
+    full pass on an explicit zero vector; degree 2 has no tensor-core colour kernel and reports
+    SF_EUNSUPPORTED, shifted colours are SF_EINVAL."""
+    import ctypes
+
+    from paper_2407_09621_b200 import _native, device
+
+    hier = sf.build_hierarchy(lvl, k)
+    n = hier.n_dofs(lvl)
+    L = _native.lib()
+    lm = hier.matrices(lvl)
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(8))
+    for m in MODES:
+        mg = sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=m))
+        table = mg.solvers[lvl].table
+        bs = b.to(m.torch_dtype)
+        zero = torch.zeros(n, dtype=m.torch_dtype, device="cuda")
+        full = torch.empty_like(zero)
+        fast = torch.full_like(zero, float("nan"))
+        s0 = (ctypes.c_int * 3)(0, 0, 0)
+        args = (m.code, k, hier.grid(lvl), s0, _native.host_ptr(lm.cell_op), _native.host_ptr(table))
+        _native.check(L.sf_smooth_colour(*args, device.ptr(zero), device.ptr(bs), device.ptr(full), device.stream_ptr()),
+                      "sf_smooth_colour")
+        rc = L.sf_smooth_colour(*args, None, device.ptr(bs), device.ptr(fast), device.stream_ptr())
+        if k == 2:
+            assert rc == _native.SF_EUNSUPPORTED
+            continue
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert torch.equal(fast, full), (k, lvl, m)
+        s1 = (ctypes.c_int * 3)(1, 0, 0)
+        assert L.sf_smooth_colour(m.code, k, hier.grid(lvl), s1, _native.host_ptr(lm.cell_op),
+                                  _native.host_ptr(table), None, device.ptr(bs), device.ptr(fast),
+                                  device.stream_ptr()) == _native.SF_EINVAL
