@@ -166,11 +166,15 @@ template <int KK = 8, class S = double, bool XZ = false>
 __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict__ xo,
                                                             const S* __restrict__ b, S* __restrict__ xn,
                                                             Geom g, LevelOp<KK, MODE_FP64> op,
-                                                            const Tables8* __restrict__ tab, Band bd) {
+                                                            const Tables8* __restrict__ tab, Band bd,
+                                                            int copy_unc = 0) {
   extern __shared__ __align__(128) double smem[];
   Tile T;
   int batch;
   if (!tile_setup_band<KK>(T, smem, g, bd, batch)) return;
+  if constexpr (KK == 8 && !XZ) {
+    if (copy_unc) copy_uncovered_ext<S, kThreads>(g, T.cx, T.cy, T.cz, xo, xn);
+  }
   Frags f;
   Halo h;
   if constexpr (!XZ) {
@@ -645,7 +649,8 @@ static int launch_colour_line(const Geom& g0, const double* opd, const double* e
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTile) != cudaSuccess)
       return -3;
     const Band bd = make_band(g);
-    kern<<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op, tab, bd);
+    kern<<<dim3(g.ntx, bd.by, bd.zb), kThreads, kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op, tab, bd,
+                                                                 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
   if (!xo)  // zero iterate (unshifted colour only; checked by the caller)
@@ -785,7 +790,7 @@ int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* opd, const
 }
 
 int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, const void* xo, const void* b, void* xn,
-                        cudaStream_t st, bool f32) {
+                        cudaStream_t st, bool f32, bool copy_unc) {
   if (!dm::offsets32(g)) return kUseGeneric;
   std::vector<double> o32, e32;
   if (f32) {
@@ -802,7 +807,7 @@ int launch_colour_dmma8(const Geom& g, const double* opd, const double* eigd, co
     if (err != cudaSuccess) return -3;
     const dm::Band bd = dm::make_band(g);
     kern<<<dim3(g.ntx, bd.by, bd.zb), dm::kThreads, dm::kSmemTile, st>>>((const S*)xo, (const S*)b, (S*)xn, g, op,
-                                                                         tab, bd);
+                                                                         tab, bd, copy_unc ? 1 : 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
   if (!xo)  // zero iterate (unshifted colour only; checked by the caller)

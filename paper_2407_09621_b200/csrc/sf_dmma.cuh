@@ -123,6 +123,37 @@ __device__ __forceinline__ int face_src(const Geom& g, int axis, int hi, int c0)
   return 1;
 }
 
+// Shifted Q7 colours leave the first / last cell layer of every shifted axis uncovered; the ping-pong copy
+// keeps x_old there.  Fused into the colour kernels: the CTA of a tile at the start (end) of a shifted axis
+// also copies the uncovered cells of its box extended by that layer (the extended boxes partition the grid,
+// so every uncovered cell is copied exactly once), 16-byte chunks, threads strided.  S = storage type.
+template <typename S, int NT>
+__device__ __forceinline__ void copy_uncovered_ext(const Geom& g, int cx, int cy, int cz, const S* __restrict__ xo,
+                                                   S* __restrict__ xn) {
+  const int c[3] = {cx, cy, cz}, n[3] = {g.nx, g.ny, g.nz}, sh[3] = {g.tx0 & 1, g.ty0 & 1, g.tz0 & 1};
+  int lo[3], ext[3];
+  bool any = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = c[a];
+    ext[a] = 2;
+    if (sh[a] && c[a] == 1) { lo[a] = 0; ++ext[a]; any = true; }
+    if (sh[a] && c[a] + 2 == n[a] - 1) { ++ext[a]; any = true; }
+  }
+  if (!any) return;
+  constexpr int VPR = 8 * (int)sizeof(S) / 16;  // 16-byte chunks per 8-point row
+  const long long sy = (long long)g.nx * 8, sz = sy * g.ny * 8;
+  const int total = ext[0] * ext[1] * ext[2] * 64 * VPR;
+  for (int i = threadIdx.x; i < total; i += NT) {
+    const int ch = i % VPR, r = i / VPR, row = r & 63, cell = r >> 6;
+    const int X = lo[0] + cell % ext[0], Y = lo[1] + (cell / ext[0]) % ext[1], Z = lo[2] + cell / (ext[0] * ext[1]);
+    if (X >= cx && X <= cx + 1 && Y >= cy && Y <= cy + 1 && Z >= cz && Z <= cz + 1) continue;  // this tile
+    const long long o = (long long)(Z * 8 + (row >> 3)) * sz + (long long)(Y * 8 + (row & 7)) * sy + X * 8 +
+                        ch * (16 / (int)sizeof(S));
+    *reinterpret_cast<uint4*>(xn + o) = __ldg(reinterpret_cast<const uint4*>(xo + o));
+  }
+}
+
 // Banded 3-D launch (replaces per-thread integer divisions of a linear tile id): grid =
 // (ntx, band rows `by`, ntz * nbands [* batch]); launch order x, y-in-band, z, band -- the
 // L2-aware order of tile_coords<K>.  Returns false for the idle CTAs of a partial last band.

@@ -182,8 +182,9 @@ int launch_vmult_dmma8(const Geom& g, const double* level_op, const void* u, voi
 // FP64 Q7 smoother colour pass on DMMA (sf_dmma.cu)
 int launch_colour_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* patch_eig,
                             const void* x_old, const void* b, void* x_new, cudaStream_t st, bool f32 = false);
+// copy_unc: the kernel also copies the shifted colour's uncovered cells (then the caller does not)
 int launch_colour_dmma8(const Geom& g, const double* level_op, const double* patch_eig, const void* x_old,
-                        const void* b, void* x_new, cudaStream_t st, bool f32 = false);
+                        const void* b, void* x_new, cudaStream_t st, bool f32 = false, bool copy_unc = false);
 // FP64 Q7 residual + restriction on DMMA (sf_dmma.cu)
 int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* level_op, const double* embedding,
                                     const void* x, const void* b, void* coarse, cudaStream_t st, bool f32 = false);

@@ -735,12 +735,17 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
     return SF_OK;
   }
   bool done = false;
+  // the Q7 DMMA kernels copy the uncovered cells themselves (whole-grid launches only; fusing it into the binary16
+  // kernel measured 5 % slower there, so those keep the separate copy)
+  const bool fuse_copy = copy && z0 < 0 && (shift[0] || shift[1] || shift[2]);
+  bool copied = false;
   if constexpr (K == 8 && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
     if (!use_generic()) {
-      const int r = launch_colour_dmma8(g, opd, eigd, xo, b, xn, st, MODE == MODE_FP32);
+      const int r = launch_colour_dmma8(g, opd, eigd, xo, b, xn, st, MODE == MODE_FP32, fuse_copy);
       if (r != kUseGeneric) {
         if (r) return check_launch("sf_smooth_colour (dmma)");
         done = true;
+        copied = fuse_copy;
       }
     }
   }
@@ -781,7 +786,7 @@ static int launch_colour(const sf_grid* gr, const int* shift, const double* opd,
                                                                         eig);
     if ((rc = check_launch("sf_smooth_colour"))) return rc;
   }
-  if (copy && (shift[0] || shift[1] || shift[2])) {
+  if (copy && !copied && (shift[0] || shift[1] || shift[2])) {
     copy_slabs<S>((const S*)xo, (S*)xn, K, gr, shift, st);
     return check_launch("sf_smooth_colour slabs");
   }
