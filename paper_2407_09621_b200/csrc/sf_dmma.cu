@@ -497,6 +497,134 @@ static const PTab8* ptables8(const double* embd_raw, int KK = 8) {
   return reinterpret_cast<const PTab8*>(d);
 }
 
+// Prolongation + add on DMMA (multigrid.py:128-143, then x + e): one CTA (8 warps) per 16^3 fine tile = one 8^3
+// block of coarse points; z -> y -> x stages, each an 8 -> 16 contraction with the line embedding E
+// (blockdiag of the cell-pair embedding; m8n8k4, 2 k-chunks x 2 n-blocks per 8-line group); stage outputs are
+// rounded to the storage type S as the reference stores them; the fine tile is staged by cp.async at the start
+// and updated in the x stage.  Shared pitches: conflict-free C-fragment stores and (mostly) A gathers.
+struct ETab8 {
+  double B[2][2][32];  // [nb][kc][lane]: E[8 nb + (lane >> 2)][4 kc + (lane & 3)]
+};
+constexpr int EQ1Y = 12, EQ1Z = 98, EQ2Y = 10, EQ2Z = 162, EXY = 24, EXZ = 384;
+
+template <int KK, class S>
+__global__ void __launch_bounds__(kThreads, 2) k_prolong_dmma(const S* __restrict__ ec, S* __restrict__ fine,
+                                                             int ncx, int ncy, int ncz,
+                                                             const ETab8* __restrict__ et) {
+  extern __shared__ __align__(128) double smem[];
+  double* Q1 = smem;                                  // z stage out [z][yc][xc]
+  double* Q2 = Q1 + 16 * EQ1Z;                        // y stage out [z][y][xc]
+  S* X = reinterpret_cast<S*>(Q2 + 16 * EQ2Z);        // fine tile [z][y][x]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, r = lane >> 2, k4 = lane & 3;
+  const long long csy = (long long)ncx * KK, csz = csy * (long long)ncy * KK;
+  const long long fsy = 2 * csy, fsz = 2 * fsy * (long long)ncy * KK;
+  const S* eb = ec + (long long)(8 * blockIdx.z) * csz + (long long)(8 * blockIdx.y) * csy + 8 * blockIdx.x;
+  S* fb = fine + (long long)(16 * blockIdx.z) * fsz + (long long)(16 * blockIdx.y) * fsy + 16 * blockIdx.x;
+  constexpr int CPR = 16 * (int)sizeof(S) / 16, NCH = 256 * CPR / kThreads;  // 16-byte chunks per fine row
+#pragma unroll
+  for (int k2 = 0; k2 < NCH; ++k2) {
+    const int c = tid + kThreads * k2, ch = c % CPR, row = c / CPR, y = row & 15, z = row >> 4;
+    const int e = ch * (16 / (int)sizeof(S));
+    cp_async16(X + z * EXZ + y * EXY + e, fb + z * fsz + y * fsy + e);
+  }
+  double bf[2][2];
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) bf[nb][kc] = __ldg(&et->B[nb][kc][lane]);
+  auto group = [&](const double (&a)[2], double (&acc)[2][2]) {
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      acc[nb][0] = acc[nb][1] = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(acc[nb][0], acc[nb][1], a[kc], bf[nb][kc]);
+    }
+  };
+  {  // z stage: warp w = coarse row yc, lines xc = r; k = zc
+    double a[2], acc[2][2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) a[kc] = (double)__ldg(eb + (4 * kc + k4) * csz + w * csy + r);
+    group(a, acc);
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) Q1[(8 * nb + 2 * k4 + i) * EQ1Z + w * EQ1Y + r] = rd<S>(acc[nb][i]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {  // y stage: plane z = 2 w + j, lines xc = r; k = yc
+    const int z = 2 * w + j;
+    double a[2], acc[2][2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) a[kc] = Q1[z * EQ1Z + (4 * kc + k4) * EQ1Y + r];
+    group(a, acc);
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) Q2[z * EQ2Z + (8 * nb + 2 * k4 + i) * EQ2Y + r] = rd<S>(acc[nb][i]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // x stage: group (z, half h) = 4 w + j, lines y = 8 h + r; k = xc; += fine
+    const int z = (4 * w + j) >> 1, y = 8 * ((4 * w + j) & 1) + r;
+    double a[2], acc[2][2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) a[kc] = Q2[z * EQ2Z + y * EQ2Y + 4 * kc + k4];
+    group(a, acc);
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int x = 8 * nb + 2 * k4;
+      const S x0 = X[z * EXZ + y * EXY + x], x1 = X[z * EXZ + y * EXY + x + 1];
+      S* p = fb + z * fsz + y * fsy + x;
+      p[0] = (S)((double)x0 + rd<S>(acc[nb][0]));
+      p[1] = (S)((double)x1 + rd<S>(acc[nb][1]));
+    }
+  }
+}
+
+static std::vector<std::pair<std::vector<double>, void*>> g_etabs;
+
+static const ETab8* etables8(const double* embd_raw, int KK) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<double> key(embd_raw, embd_raw + 2 * KK * KK);
+  key.push_back((double)dev);
+  key.push_back((double)KK);
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_etabs)
+    if (e.first == key) return reinterpret_cast<const ETab8*>(e.second);
+  double E[16 * 8] = {};
+  for (int c = 0; c < 16 / (2 * KK); ++c)
+    for (int i = 0; i < 2 * KK; ++i)
+      for (int j = 0; j < KK; ++j) E[(c * 2 * KK + i) * 8 + c * KK + j] = embd_raw[i * KK + j];
+  ETab8 host;
+  for (int nb = 0; nb < 2; ++nb)
+    for (int kc = 0; kc < 2; ++kc)
+      for (int ln = 0; ln < 32; ++ln) host.B[nb][kc][ln] = E[(8 * nb + (ln >> 2)) * 8 + 4 * kc + (ln & 3)];
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(ETab8)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(ETab8), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  g_etabs.push_back({std::move(key), d});
+  return reinterpret_cast<const ETab8*>(d);
+}
+
+template <int KK, class S>
+static int launch_prolong_t(int ncx, int ncy, int ncz, const double* embd, const void* e, void* fine,
+                            cudaStream_t st) {
+  if ((ncx * KK) % 8 || (ncy * KK) % 8 || (ncz * KK) % 8 || ncz * KK / 8 > 65535 || ncy * KK / 8 > 65535)
+    return kUseGeneric;
+  if (!aligned16(e) || !aligned16(fine)) return kUseGeneric;
+  const ETab8* et = etables8(embd, KK);
+  if (!et) return -3;
+  const int smem = (int)(sizeof(double) * 16 * (EQ1Z + EQ2Z) + sizeof(S) * 16 * EXZ);
+  if (cudaFuncSetAttribute(k_prolong_dmma<KK, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return -3;
+  const dim3 grid(ncx * KK / 8, ncy * KK / 8, ncz * KK / 8);
+  k_prolong_dmma<KK, S><<<grid, kThreads, smem, st>>>((const S*)e, (S*)fine, ncx, ncy, ncz, et);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 // ---------------------------------------------------------------------------
 // Q1 / Q3 (K = 2, 4) on DMMA: the same 16^3-point tile, now (16/K)^3 cells.  A tile line is
 // 16 / K cells; its 1-D operators are the 16 x 16 line matrices -- blockdiag(M_cell) for the
@@ -887,5 +1015,20 @@ int launch_resid_restrict_dmma8(const Geom& g, const double* opd, const double* 
   };
   return f32 ? go(dm::k_resid_restrict_dmma<8, float>, (const float*)nullptr)
              : go(dm::k_resid_restrict_dmma<8, double>, (const double*)nullptr);
+}
+}  // namespace sf
+
+namespace sf {
+int launch_prolong_dmma(int k_nodes, int ncx, int ncy, int ncz, const double* embd, const void* e, void* fine,
+                        cudaStream_t st, bool f32) {
+  switch (k_nodes) {
+    case 8: return f32 ? dm::launch_prolong_t<8, float>(ncx, ncy, ncz, embd, e, fine, st)
+                       : dm::launch_prolong_t<8, double>(ncx, ncy, ncz, embd, e, fine, st);
+    case 4: return f32 ? dm::launch_prolong_t<4, float>(ncx, ncy, ncz, embd, e, fine, st)
+                       : dm::launch_prolong_t<4, double>(ncx, ncy, ncz, embd, e, fine, st);
+    case 2: return f32 ? dm::launch_prolong_t<2, float>(ncx, ncy, ncz, embd, e, fine, st)
+                       : dm::launch_prolong_t<2, double>(ncx, ncy, ncz, embd, e, fine, st);
+    default: return kUseGeneric;
+  }
 }
 }  // namespace sf

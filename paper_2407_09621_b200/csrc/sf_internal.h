@@ -191,6 +191,9 @@ int launch_resid_restrict_dmma_line(int k_nodes, const Geom& g, const double* le
 int launch_resid_restrict_dmma8(const Geom& g, const double* level_op, const double* embedding, const void* x,
                                 const void* b, void* coarse, cudaStream_t st, bool f32 = false);
 // FP16 / FP16-EC Q7 kernels on HMMA (sf_hmma.cu)
+// fp64 / fp32-storage prolongation + add on DMMA (sf_dmma.cu); kUseGeneric when the coarse grid does not tile
+int launch_prolong_dmma(int k_nodes, int ncx, int ncy, int ncz, const double* embedding, const void* e, void* fine,
+                        cudaStream_t st, bool f32);
 // binary16 prolongation + add on HMMA (sf_hmma.cu); kUseGeneric when the coarse grid does not tile
 int launch_prolong_hmma(int mode, int k_nodes, int ncx, int ncy, int ncz, const double* embedding, const void* e,
                         void* fine, cudaStream_t st);

@@ -868,6 +868,12 @@ static int launch_prolong_add(const sf_grid* coarse, const double* embd, const v
       if (r != kUseGeneric) return r ? check_launch("sf_prolongate_add (hmma)") : SF_OK;
     }
   }
+  if constexpr ((K == 8 || K == 4 || K == 2) && (MODE == MODE_FP64 || MODE == MODE_FP32)) {
+    if (!use_generic()) {
+      const int r = launch_prolong_dmma(K, coarse->nx, coarse->ny, coarse->nz, embd, e, fine, st, MODE == MODE_FP32);
+      if (r != kUseGeneric) return r ? check_launch("sf_prolongate_add (dmma)") : SF_OK;
+    }
+  }
   constexpr int TPC = Tpc<K>::value;
   constexpr int B = 2 * K;
   using S = typename MT<MODE>::S;
