@@ -424,44 +424,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const S* __
     }
   }
   __syncthreads();  // sB (dd) fully consumed
-  double* S1 = T.sB;  // [zc][y][x], plane pitch 258 (conflict-free 64-bit stores)
+  // y and x restriction stages on DMMA as well (8-line groups, the z stage's permuted-k P^T fragments pfr):
+  // S1 [zc][y][x] (y pitch 18, zc pitch 290) -> S2 [zc][yc][x] (yc pitch 18, zc pitch 146) -> coarse
+  constexpr int R1Y = 18, R1Z = 290, R2Y = 18, R2Z = 146;
+  double* S1 = T.sB;
 #pragma unroll
   for (int yy = 0; yy < 2; ++yy)
 #pragma unroll
     for (int g8 = 0; g8 < 2; ++g8)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) S1[(c2 + i) * 258 + (2 * w + yy) * 16 + 8 * g8 + r] = rd<S>(keep[yy][g8][i]);
+      for (int i = 0; i < 2; ++i) S1[(c2 + i) * R1Z + (2 * w + yy) * R1Y + 8 * g8 + r] = rd<S>(keep[yy][g8][i]);
   __syncthreads();
-  double* S2 = T.sU;  // [zc][yc][x]
-  if (threadIdx.x < 128) {  // y lines (zc, x)
-    const int xx = threadIdx.x & 15, zc = threadIdx.x >> 4;
-    double v[16];
+  double* S2 = T.sU;
 #pragma unroll
-    for (int y = 0; y < 16; ++y) v[y] = S1[zc * 258 + y * 16 + xx];
+  for (int j = 0; j < 2; ++j) {  // y stage: group (zc, x half) = 2 w + j, lines x = xb + r; k = y
+    const int gi = 2 * w + j, zc = gi >> 1, xb = 8 * (gi & 1);
+    double acc[2] = {0.0, 0.0};
 #pragma unroll
-    for (int yc = 0; yc < 8; ++yc) {
-      double s = 0.0;
-#pragma unroll
-      for (int y = 0; y < 16; ++y) s = fma(__ldg(&pt->P[y][yc]), v[y], s);
-      S2[(zc * 8 + yc) * 16 + xx] = rd<S>(s);
+    for (int kc = 0; kc < 4; ++kc) {
+      const int kp = 8 * (kc >> 1) + c2 + (kc & 1);
+      dmma(acc[0], acc[1], S1[zc * R1Z + kp * R1Y + xb + r], pfr[kc]);
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) S2[zc * R2Z + (c2 + i) * R2Y + xb + r] = rd<S>(acc[i]);
   }
   __syncthreads();
-  if (threadIdx.x < 64) {  // x lines (zc, yc) -> coarse
-    const int yc = threadIdx.x & 7, zc = threadIdx.x >> 3;
-    double v[16];
+  {  // x stage: group zc = w, lines yc = r; k = x -> coarse (xc = c2, c2 + 1)
+    double acc[2] = {0.0, 0.0};
 #pragma unroll
-    for (int xx = 0; xx < 16; ++xx) v[xx] = S2[(zc * 8 + yc) * 16 + xx];
-    const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
-    S* out = coarse + (long long)((T.cz / 2) * KK + zc) * szc + (long long)((T.cy / 2) * KK + yc) * syc +
-                  (T.cx / 2) * KK;
-#pragma unroll
-    for (int xc = 0; xc < 8; ++xc) {
-      double s = 0.0;
-#pragma unroll
-      for (int xx = 0; xx < 16; ++xx) s = fma(__ldg(&pt->P[xx][xc]), v[xx], s);
-      out[xc] = (S)s;
+    for (int kc = 0; kc < 4; ++kc) {
+      const int kp = 8 * (kc >> 1) + c2 + (kc & 1);
+      dmma(acc[0], acc[1], S2[w * R2Z + r * R2Y + kp], pfr[kc]);
     }
+    const long long syc = (long long)(g.nx / 2) * KK, szc = syc * (long long)(g.ny / 2) * KK;
+    S* out = coarse + (long long)((T.cz / 2) * KK + w) * szc + (long long)((T.cy / 2) * KK + r) * syc +
+             (T.cx / 2) * KK + c2;
+    out[0] = (S)acc[0];
+    out[1] = (S)acc[1];
   }
 }
 
