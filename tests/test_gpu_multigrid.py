@@ -302,3 +302,28 @@ def test_graph_replayed_vcycle_is_identical(k, mode):
         assert torch.equal(got, eager)
     b2 = torch.from_numpy(unit(np.random.default_rng(10), hier.n_dofs(lvl))).cuda()
     assert torch.equal(mg.apply(b2, lvl), sf.MultigridPreconditioner(hier, sf.VCycleConfig(mode=mode)).apply(b2, lvl))
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 3), (1, 4)])
+@pytest.mark.parametrize("cfg", [dict(pre=2, post=1), dict(pre=1, post=3), dict(pre=1, post=1, coarse=2),
+                                 dict(pre=1, post=1, order="reversed")])
+def test_vcycle_configurations_match_oracle(k, lvl, cfg):
+    """V-cycle variants against the CPU oracle in fp64: two pre-smoothing steps (only the first starts from zero,
+    so only its first colour may take the zero-iterate pass), three post-smoothing steps, coarse level 2, and a
+    smoother ordering that starts with a shifted colour (the zero-iterate pass applies to the unshifted colour
+    only, so it is not taken)."""
+    from oracle import port
+
+    order = tuple(reversed(sf.default_ordering(3))) if cfg.get("order") == "reversed" else None
+    coarse = cfg.get("coarse", 1)
+    if coarse == 2 and k == 7:
+        pytest.skip("a Q7 level-2 coarse matrix (32768^2) makes the CPU oracle's dense LU take minutes")
+    hier = sf.build_hierarchy(lvl, k)
+    b = unit(np.random.default_rng(11), hier.n_dofs(lvl))
+    conf = sf.VCycleConfig(pre_smooth_steps=cfg["pre"], post_smooth_steps=cfg["post"], coarse_level=coarse)
+    if order is not None:
+        conf.smoother_ordering = order
+    got = sf.MultigridPreconditioner(hier, conf).apply(b, lvl)
+    ref = port.VCycle(port.Hierarchy(lvl, k), pre=cfg["pre"], post=cfg["post"], coarse_level=coarse,
+                      ordering=order).apply(b, lvl)
+    assert rel_l2(got, ref) <= 1e-10, rel_l2(got, ref)
