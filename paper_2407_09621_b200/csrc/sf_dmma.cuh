@@ -36,7 +36,12 @@ constexpr int TRW = 20;
 constexpr int kThreads = 256;
 constexpr size_t kSmemTile = sizeof(double) * (2 * VOL + 12 * TRP + 4 * 8 * 32);
 
-__device__ __forceinline__ int idxU(int z, int y, int x) { return z * PLANE + y * 16 + (x ^ ((y & 3) << 2)); }
+// U layout = the TMA 128-byte swizzle of a 16 x 16 x 16 fp64 box: 128-byte rows (z, y), 16-byte chunk x / 2
+// XORed with the row index mod 8 -- conflict-free for the x stage's A-fragment loads, and what
+// cp.async.bulk.tensor writes with CU_TENSOR_MAP_SWIZZLE_128B (the FP64 vmult loads its tile that way)
+__device__ __forceinline__ int idxU(int z, int y, int x) {
+  return z * PLANE + y * 16 + ((((x >> 1) ^ (y & 7)) << 1) | (x & 1));
+}
 __device__ __forceinline__ int swA(int y) { return ((y & 1) << 3) | ((y & 2) << 1); }  // {0,8,4,12}[y&3]
 __device__ __forceinline__ int idxA(int z, int y, int x) { return z * PLANE + y * 16 + (x ^ swA(y)); }
 __device__ __forceinline__ int idxC(int z, int y, int x) {
@@ -604,11 +609,10 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
       for (int i = 0; i < 16 / VEC; ++i) {
         const int z = z0 + (16 / NV) * i;
         const float* src = stg + z * 256 + y * 16 + x;
-        double* dst = &T.sU[idxU(z, y, x)];
 #pragma unroll
         for (int j = 0; j < VEC; j += 2) {
           const float2 v2 = *reinterpret_cast<const float2*>(src + j);
-          *reinterpret_cast<double2*>(dst + j) = make_double2(v2.x, v2.y);
+          *reinterpret_cast<double2*>(&T.sU[idxU(z, y, x + j)]) = make_double2(v2.x, v2.y);
         }
       }
     }
