@@ -325,7 +325,9 @@ def main():
                       "parallelism": (f"z-slab x{world}" + (" (ranks sharing one GPU over gloo: not a scaling point)"
                                                              if shared else "")) if world > 1 else "single GPU",
                       "l2_flush": f"not needed: u, v = 2 x {8 * D / 1e9:.2f} GB per GPU >> 126 MB L2"},
-           "tflops_reference_equivalent": value * 1e9 * ref_flops_per_dof(k, lvl) / 1e12,
+           # the reference's patch schedule would need this many flop per DoF (src/discretization.py:240-264);
+           # the kernel runs the cell-wise form (roofline.flops_per_dof), so this is a work-equivalence note only
+           "reference_schedule_flop_per_dof": ref_flops_per_dof(k, lvl),
            "roofline": roofline, "clocks": clk,
            # our kernels per timed step: one vmult; at N > 1 the interior + two boundary tile layers
            "gpu_launches": args.steps * (3 if world > 1 and n >= 3 * (16 // K if K in (2, 4) else 2) else 1)}
