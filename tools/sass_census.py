@@ -8,7 +8,7 @@ import subprocess
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2407_09621_b200",
                    "libsumfact_b200.so")
 KEYS = ["DMMA", "HMMA", "UTCHMMA", "UTCBAR", "LDTM", "LDSM", "STSM", "LDGSTS", "UTMALDG", "FFMA2", "FMUL2", "FHFMA",
-        "REDUX", "DFMA"]
+        "REDUX", "CREDUX", "DFMA"]
 WANT = ["k_vmult_dmma8", "k_colour_dmma", "k_resid_restrict_dmma", "k_prolong_dmma", "k_vmult_h8", "k_colour_h8",
         "k_resid_restrict_h8", "k_prolong_h8", "k_vmult_u8", "k_vmult_dmma_line", "k_axpy_dot_partial", "k_dense_apply"]
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
