@@ -52,7 +52,7 @@ __device__ __forceinline__ int idxT(int z, int y, int x) {
   return z * PLANE + y * 16 + (x ^ ((((z >> 1) + y) & 3) << 2));
 }
 __device__ __forceinline__ int idxG(int z, int y, int x) {
-  return z * PLANE + y * 16 + (x ^ (((y ^ (y >> 1)) & 3) << 2));
+  return z * PLANE + y * 16 + ((((x >> 1) ^ (y & 7)) << 1) | (x & 1));
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
