@@ -18,9 +18,8 @@
 //   y:  c = My a,  dd = Ly a (+ y halo) + My b      -- same warp, same planes, in place
 //   z:  v = Lz c (+ z halo) + Mz dd                 -- warp owns y rows, lines along x
 // Shared-memory layouts are XOR swizzles (the paper's conflict-free idea,
-// P:319) chosen so every A-fragment LDS.64 and C-fragment store of the three
-// stages is bank-conflict free:
-//   U layout : z*256 + y*16 + (x ^ 4(y&3))
+// P:319), chosen per stage and then A/B-measured (profiles/r02_vmult_fp64.md):
+//   U layout : z*256 + y*16 + 2((x/2) ^ (y&7)) + (x&1)   (the TMA 128-byte swizzle; see idxU)
 //   A layout : z*256 + y*16 + (x ^ {0,8,4,12}[y&3])
 //   C layout : z*256 + y*16 + (x ^ 4(((y>>1)+z)&3))
 #pragma once
@@ -47,7 +46,8 @@ __device__ __forceinline__ int idxA(int z, int y, int x) { return z * PLANE + y 
 __device__ __forceinline__ int idxC(int z, int y, int x) {
   return z * PLANE + y * 16 + (x ^ ((((y >> 1) + z) & 3) << 2));
 }
-// smoother layouts: T = C with the roles of y and z swapped, G = Gray-code swizzle
+// smoother layouts: T = C with the roles of y and z swapped; G = the U swizzle (was a Gray-code swizzle of
+// 32-byte groups; measured 0.4 % slower per smoothing step)
 __device__ __forceinline__ int idxT(int z, int y, int x) {
   return z * PLANE + y * 16 + (x ^ ((((z >> 1) + y) & 3) << 2));
 }
