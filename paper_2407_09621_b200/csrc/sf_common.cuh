@@ -194,11 +194,12 @@ struct Geom {
 // Tile id -> tile coordinates in an L2-aware order: y is cut into bands of BAND/ntx tile
 // rows; inside a band the order is x fastest, then y, then z.  A tile's z neighbours are then
 // ~BAND launches away (instead of ntx*nty), so the neighbour cell layers its face traces read
-// are still in L2 (profiles/r01_vmult_fp64.md).  BAND = tiles in ~16 MiB of
-// fp64 data: 512 for Q7 (32 KiB tiles), 4096 for Q3.
+// are still in L2 (profiles/r01_vmult_fp64.md).  BAND = tiles in ~8 MiB of
+// fp64 data: 256 for Q7 (32 KiB tiles; 4 tile rows at level 7), 2048 for Q3.  Round 2 A/B
+// (profiles/r02_vmult_fp64.md): 16 MiB 118.4, 8 MiB 120.3, 4 MiB 116.9, 32 MiB 112.6 GDoF/s.
 template <int K>
 constexpr int band_tiles() {
-  return (1 << 24) / (8 * K * K * K * 8) > 1 ? (1 << 24) / (8 * K * K * K * 8) : 1;
+  return (1 << 23) / (8 * K * K * K * 8) > 1 ? (1 << 23) / (8 * K * K * K * 8) : 1;
 }
 template <int K>
 __device__ __forceinline__ void tile_coords(const Geom& g, int id, int& tx, int& ty, int& tz) {
