@@ -18,6 +18,7 @@ sample of the same workload (Q7 level 5, 16.8 M DoF), rank 0 only.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import math
 import os
@@ -63,15 +64,21 @@ def kernel_flops_per_dof(k):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons during the timed region: a background `nvidia-smi -lms 100` started
+    (and waited for) before the warm-up, its samples kept only inside the host window of the timed region
+    (timestamp field), plus one synchronous query issued while the timed steps are queued on the GPU -- so a short
+    timed region still has samples."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
+        self.gpu = gpu_index
         self.path = tempfile.mktemp(suffix=".csv")
         self.fh = open(self.path, "w")
+        self.extra = []
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
@@ -79,7 +86,28 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_ready(self, timeout=5.0):
+        t = time.time()
+        while self.proc is not None and time.time() - t < timeout:
+            self.fh.flush()
+            if os.path.getsize(self.path) > 0:
+                return
+            time.sleep(0.05)
+
+    def start(self):
+        self.t0 = time.time()
+
+    def snapshot(self):
+        """One synchronous query (call it while the timed work is queued on the GPU)."""
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+            self.extra += [l for l in out.stdout.splitlines() if l.strip()]
+        except Exception:
+            pass
+
     def stop(self):
+        self.t1 = time.time()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -89,22 +117,33 @@ class ClockSampler:
         self.fh.close()
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+        def when(stamp):
+            try:
+                return datetime.datetime.strptime(stamp.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                return None
         try:
-            for line in open(self.path):
-                f = [x.strip() for x in line.split(",")]
-                if len(f) < 8:
-                    continue
-                try:
-                    sm.append(float(f[0]))
-                    mx = max(mx, float(f[1]))
-                except ValueError:
-                    continue
-                for name, val in zip(names, f[4:8]):
-                    if val.lower().startswith("active"):
-                        reasons.add(name)
+            lines = [(l, False) for l in open(self.path)] + [(l, True) for l in self.extra]
         except FileNotFoundError:
-            pass
-        os.unlink(self.path)
+            lines = [(l, True) for l in self.extra]
+        for line, inside in lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            ts = when(f[0])
+            if not inside and (ts is None or self.t0 is None or not (self.t0 - 0.05 <= ts <= self.t1 + 0.05)):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if os.path.exists(self.path):
+            os.unlink(self.path)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
@@ -235,21 +274,24 @@ def main():
         def step(timed=False):
             vmult_device(hier, lvl, u, v, P.FP64, grid=grid)
 
+    clocks = ClockSampler(local)
+    clocks.wait_ready()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    clocks.start()
     e0.record(stream)
     for _ in range(args.steps):
         step(timed=True)
     e1.record(stream)
+    clocks.snapshot()  # the timed steps are queued on the GPU: this query samples them
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
