@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_colour_dmma(const S* __restrict
     prefetch_ahead_l2<KK>(g, bd, T, xo);
     init_frags<KK>(T, op, f, h);
     prologue_fast<KK>(T, g, op, xo, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-    xy_stages<S>(T, f, h);
+    xy_stages<S, KK>(T, f, h);
     __syncthreads();
   }
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_resid_restrict_dmma(const S* __
   Halo h;
   init_frags<KK>(T, op, f, h);
   prologue_fast<KK>(T, g, op, x, f, &tab->L[0][0][0]);  // L fragments staged into smem (T.sLf)
-  xy_stages<S>(T, f, h);
+  xy_stages<S, KK>(T, f, h);
   __syncthreads();
   const int lane = T.lane, r = T.r, c2 = T.c2, w = T.warp;
   const long long off0 = (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_vmult_dmma_line(const S* __rest
   Halo h;
   init_frags<KK>(T, op, f, h);
   prologue_fast<KK>(T, g, op, u, f, &tab->L[0][0][0]);
-  xy_stages<S>(T, f, h);
+  xy_stages<S, KK>(T, f, h);
   __syncthreads();
   load_l(T, f, T.kind[2]);
   S* vb = v + (long long)(T.cz * KK) * T.sz + (long long)(T.cy * KK) * T.sy + T.cx * KK;

@@ -38,8 +38,12 @@ constexpr size_t kSmemTile = sizeof(double) * (2 * VOL + 12 * TRP + 4 * 8 * 32);
 // U layout = the TMA 128-byte swizzle of a 16 x 16 x 16 fp64 box: 128-byte rows (z, y), 16-byte chunk x / 2
 // XORed with the row index mod 8 -- conflict-free for the x stage's A-fragment loads, and what
 // cp.async.bulk.tensor writes with CU_TENSOR_MAP_SWIZZLE_128B (the FP64 vmult loads its tile that way)
+// (Q7 2-cell tiles; the 16-point line tiles of Q3 / Q1 keep the 32-byte XOR x ^ 4(y mod 4), which measured 1.3 %
+// faster for them: profiles/r02_vmult_fp64.md)
+template <int KK = 8>
 __device__ __forceinline__ int idxU(int z, int y, int x) {
-  return z * PLANE + y * 16 + ((((x >> 1) ^ (y & 7)) << 1) | (x & 1));
+  if constexpr (KK == 8) return z * PLANE + y * 16 + ((((x >> 1) ^ (y & 7)) << 1) | (x & 1));
+  else return z * PLANE + y * 16 + (x ^ ((y & 3) << 2));
 }
 __device__ __forceinline__ int swA(int y) { return ((y & 1) << 3) | ((y & 2) << 1); }  // {0,8,4,12}[y&3]
 __device__ __forceinline__ int idxA(int z, int y, int x) { return z * PLANE + y * 16 + (x ^ swA(y)); }
@@ -309,7 +313,7 @@ struct Halo {
 };
 
 // x and y stages on the warp's two z planes (in place: U <- a <- c, B <- b <- dd)
-template <class S = double>
+template <class S = double, int KK = 8>
 __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h) {
   for (int zz = 0; zz < 2; ++zz) {
     const int z = 2 * T.warp + zz;
@@ -320,7 +324,7 @@ __device__ __forceinline__ void xy_stages(const Tile& T, Frags& f, const Halo& h
       const int y = 8 * g8 + T.r;
       double a[4];
 #pragma unroll
-      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU(z, y, 4 * kc + T.k4)];
+      for (int kc = 0; kc < 4; ++kc) a[kc] = T.sU[idxU<KK>(z, y, 4 * kc + T.k4)];
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) ra[g8][nb][0] = ra[g8][nb][1] = rb[g8][nb][0] = rb[g8][nb][1] = 0.0;
       h.apply(T, rb[g8], 0, z * TRW + y);  // halo first: the DFMAs need no DMMA result
@@ -520,7 +524,7 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
     {  // tile: chunk (x2 = tid & 7, y = (tid >> 3) & 15, z = (tid >> 7) + 2i)
       const int x2 = tid & 7, y = (tid >> 3) & 15, z0 = tid >> 7;
       const S* src = ub + z0 * sz + y * sy + 2 * x2;
-      double* dst = &T.sU[idxU(z0, y, 2 * x2)];
+      double* dst = &T.sU[idxU<K>(z0, y, 2 * x2)];
 #pragma unroll
       for (int i = 0; i < 8; ++i) cp_async16(dst + i * 512, src + 2 * i * sz);
     }
@@ -612,7 +616,7 @@ __device__ __forceinline__ void prologue_fast(Tile& T, const Geom& g, const OpT&
 #pragma unroll
         for (int j = 0; j < VEC; j += 2) {
           const float2 v2 = *reinterpret_cast<const float2*>(src + j);
-          *reinterpret_cast<double2*>(&T.sU[idxU(z, y, x + j)]) = make_double2(v2.x, v2.y);
+          *reinterpret_cast<double2*>(&T.sU[idxU<K>(z, y, x + j)]) = make_double2(v2.x, v2.y);
         }
       }
     }
