@@ -327,3 +327,30 @@ def test_vcycle_configurations_match_oracle(k, lvl, cfg):
     ref = port.VCycle(port.Hierarchy(lvl, k), pre=cfg["pre"], post=cfg["post"], coarse_level=coarse,
                       ordering=order).apply(b, lvl)
     assert rel_l2(got, ref) <= 1e-10, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("k,lvl", [(7, 4), (3, 5), (1, 6)])
+@pytest.mark.parametrize("mode", [P.FP64, P.FP32, P.FP16, P.FP16_EC])
+def test_tensor_core_prolongation_matches_oracle(mode, k, lvl):
+    """x + P e on the tensor-core prolongation kernels (k_prolong_dmma / k_prolong_h8: several 16^3 fine tiles
+    per axis) against the CPU oracle's prolongate in the same mode."""
+    import torch
+
+    from oracle import port
+    from paper_2407_09621_b200.multigrid import prolongate_add_device
+
+    H = port.Hierarchy(lvl, k)
+    rng = np.random.default_rng(23)
+    e = unit(rng, H.n_dofs(lvl - 1))
+    x = unit(rng, H.n_dofs(lvl))
+    ref = x.astype(mode.storage_dtype) + port.prolongate(H, lvl - 1, e, mode.value)
+    ref64 = x + port.prolongate(H, lvl - 1, e, "fp64")
+    hier = sf.build_hierarchy(lvl, k)
+    et = torch.from_numpy(e).to("cuda", mode.torch_dtype)
+    xt = torch.from_numpy(x).to("cuda", mode.torch_dtype)
+    prolongate_add_device(hier, lvl - 1, et, xt, mode)
+    got = xt.cpu().numpy()
+    if mode is P.FP64:
+        assert rel_l2(got, ref) <= 1e-13
+    else:  # reference band: the oracle's own error in this mode against fp64, x4
+        assert rel_l2(got, ref64) <= 4.0 * rel_l2(ref, ref64) + 1e-7, (rel_l2(got, ref64), rel_l2(ref, ref64))
