@@ -248,8 +248,8 @@ def test_ec_solve_keeps_fp64_iteration_count_at_scale(k, lvl):
     assert res[P.FP16_EC][1] <= 1.5 * res[P.FP64][1] + 1e-12
 
 
-@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (1, 5), (3, 3)])
-@pytest.mark.parametrize("mode", [P.FP64, P.FP16, P.FP16_EC])
+@pytest.mark.parametrize("k,lvl", [(7, 3), (3, 4), (1, 5), (3, 3), (7, 4)])
+@pytest.mark.parametrize("mode", [P.FP64, P.FP32, P.FP16, P.FP16_EC])
 def test_fused_residual_restriction(mode, k, lvl):
     """sf_residual_restrict with x (the fused tensor-core kernels: Q7 patch tiles, Q3/Q1 line tiles)
     == restrict(b - A x)."""
