@@ -208,9 +208,10 @@ def _stream_vmult(hier: MeshHierarchy, level: int, u: torch.Tensor, v: torch.Ten
     n, K = hier.n_cells(level), hier.degree + 1
     layer = K * (n * K) ** 2  # one cell layer of dofs
     if slab_cells is None:
-        # 4 cells at level 7: tools/e2e_time.py 6.01 GDoF/s (2: 6.02, 8: 5.89, 16: 5.60) against the 6.14
-        # GDoF/s this box's host link allows (tools/link_probe.py: 49 GB/s each way with both directions busy)
-        slab_cells = max(2, (n // 32) & ~1)
+        # 2 cells at level 7: tools/e2e_time.py 5.89-5.91 GDoF/s (4 cells: 5.77-5.88; 8: 5.51-5.89; 16: 5.60)
+        # against the 5.7-6.1 GDoF/s the boxes' host links allow (tools/link_probe.py: 46-49 GB/s each way with
+        # both directions busy)
+        slab_cells = max(2, (n // 64) & ~1)
     slab_cells = min(slab_cells, n)
     dt = mode.torch_dtype
     key = (torch.cuda.current_device(), dt, slab_cells, layer, n)
